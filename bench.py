@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""EDiT layer-wise sync benchmark (BASELINE.json metric: "EDiT sync GB/s of params/round
+and % HBM+NVLink roofline at 1/2/4/8 B200").
+
+One step = one full sync round (Alg. 2 for every one of the 34 sync units of a
+Llama-shaped model) over this rank's shards, through the C ABI.
+Workload at N = 1: Llama-7B-shaped shards on a 1 x 1 mesh (the largest single-GPU
+configuration of BASELINE.json; 71.3 GB of local/anchor/momentum, far above L2).  With
+--gpus N the default mesh is 1 x N (every rank keeps a full 7B replica: weak scaling).
+
+Between steps, outside the timed region, every local is redrawn as
+cast(anchor - D) with a fresh inner-loop displacement D (synth/), so each timed round
+syncs a realistic pseudo-gradient (clip active, anomaly test live).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl edit|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import synth  # noqa: E402
+
+NOMINAL_HBM_GBS = 8000.0       # BASELINE.md roofline definition (nominal)
+NOMINAL_NVL_GBS = 900.0        # per direction per GPU (nominal)
+MEASURED_NVL_GBS = 770.0       # peer copy per direction, B200_PROFILING.md (measured on this pool)
+METRIC = "EDiT sync GB/s of params/round and % HBM+NVLink roofline at 1/2/4/8 B200"
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+def parse_mesh(s: str | None, world: int) -> tuple[int, int]:
+    if not s:
+        return 1, world
+    m, n = (int(x) for x in s.lower().split("x"))
+    if m * n != world:
+        raise SystemExit(f"mesh {s} needs {m * n} ranks, have {world}")
+    return m, n
+
+
+class Clocks:
+    """nvidia-smi sampler run DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+
+    def summary(self) -> dict:
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def oracle_cpu_baseline(model: str, dtype, target_s: float = 15.0) -> dict:
+    """The oracle (as it stands) on this host's cores, on a bounded sample of the workload:
+    the first X elements of the 7B layer-0 shard (1 x 1 mesh), X sized for ~target_s."""
+    import numpy as np
+
+    import oracle
+    from tests import parity
+    oracle.set_threads(os.cpu_count() or 1)
+    u = synth.llama_units(model)[1]
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def sample(x):
+        sub = synth.Unit(u.name + f"[:{x}]", x, ())
+        a = synth.shard_anchor(sub, 1, 1, 0, dev)
+        m = synth.shard_momentum(sub, 1, 1, 0, dev)
+        l = synth.shard_local(sub, 1, 1, 0, 0, a, dtype, dev)
+        return (parity.to_oracle_local(l)[None, None], a.cpu().numpy()[None], m.cpu().numpy()[None])
+
+    def run(x):
+        L, A, Mo = sample(x)
+        t0 = time.perf_counter()
+        oracle.sync_unit(oracle.Config(), L, A, Mo, [oracle.Ema()])
+        return time.perf_counter() - t0
+
+    x = 2_000_000
+    t = run(x)
+    x2 = int(min(u.numel, max(x, x * target_s / max(t, 1e-3))))
+    t2 = run(x2)
+    return {"value": 4.0 * x2 / t2 / 1e9, "unit": "GB/s", "cores": oracle.get_threads(), "kind": "oracle",
+            "sample": f"1 sync of the first {x2} params of the Llama-{model} layer-0 shard (1x1 mesh, "
+                      f"{'bf16' if dtype == torch.bfloat16 else 'f32'} local), {t2:.2f} s on {oracle.get_threads()} "
+                      "threads; fp32 pseudo-gradient bytes / s"}
+
+
+def reference_arm(args) -> None:
+    """--impl reference: the fp64 CPU oracle as it stands, on this host's cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from tests import parity
+    oracle.set_threads(os.cpu_count() or 1)
+    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    M, N = 1, 1
+    u = synth.llama_units(args.model)[1]
+    x = args.ref_sample
+    sub = synth.Unit(u.name + f"[:{x}]", x, ())
+    gen_dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+    a = synth.shard_anchor(sub, 1, M, 0, gen_dev)
+    m = synth.shard_momentum(sub, 1, M, 0, gen_dev)
+    A, Mo = a.cpu().numpy()[None], m.cpu().numpy()[None]
+    ema = [oracle.Ema(*synth.ema_seed(sub, 0)[:2], 10)]
+    times = []
+    for step in range(args.warmup + args.steps):
+        L = parity.to_oracle_local(synth.shard_local(sub, 1, M, 0, 0, torch.from_numpy(A[0]).to(gen_dev), dtype,
+                                                     gen_dev, round_salt=step))[None, None]
+        t0 = time.perf_counter()
+        L, A, Mo, ema, _ = oracle.sync_unit(oracle.Config(), L, A, Mo, ema)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+    total = sum(times)
+    value = 4.0 * x * len(times) / total / 1e9
+    cores = oracle.get_threads()
+    line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"llama-{args.model} shards, 1x1 mesh: bounded sample of {x} params of the "
+                                   "layer-0 shard per step (oracle throughput; same metric/unit)",
+                       "model_shape": args.model, "param_dtype": args.dtype},
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{x} params of the Llama-{args.model} layer-0 shard per step"},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="edit", choices=["edit", "reference"])
+    ap.add_argument("--model", default="7B", choices=list(synth.LLAMA))
+    ap.add_argument("--mesh", default=None, help="MxN shard x sync mesh (default 1xN)")
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--e2e-units", default="1,2,3", help="unit indices timed through the host-buffer API")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-sample", type=int, default=4_000_000)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: W >= 3
+
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2412_07210_b200 import EditSync, broadcast_unique_id
+
+    M, N = parse_mesh(args.mesh, world)
+    m_idx, n_idx = rank % M, rank // M
+    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    b_l = 2 if dtype == torch.bfloat16 else 4
+    units = synth.llama_units(args.model)
+    numel = [synth.shard_numel(u.numel, M) for u in units]
+    P_r = sum(numel)
+    uid = broadcast_unique_id() if world > 1 else None
+    sync = EditSync(numel, shard_dim=M, sync_dim=N, rank=rank, device=dev, param_dtype=dtype, unique_id=uid)
+    # EMA seeded at the expected module norm of each replica (synth recipe, R8)
+    import numpy as np
+    mu = np.array([[synth.ema_seed(u, n)[0] for n in range(N)] for u in units])
+    sync.set_ema(mu, 0.1 * mu, synth.Recipe().ema_warmup_rounds)
+
+    anchors, moms, locs = [], [], []
+    for i, u in enumerate(units):
+        a = synth.shard_anchor(u, i, M, m_idx, dev)
+        anchors.append(a)
+        moms.append(synth.shard_momentum(u, i, M, m_idx, dev))
+        locs.append(torch.empty(numel[i], dtype=dtype, device=dev))
+    torch.cuda.synchronize()
+
+    def redraw(step: int) -> None:
+        # "tau inner steps" of every worker, outside the timed region
+        for i, u in enumerate(units):
+            locs[i].copy_(synth.shard_local(u, i, M, m_idx, n_idx, anchors[i], dtype, dev, round_salt=step))
+
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+
+    def run_round():
+        for i in range(len(units)):
+            sync.layer_sync(i, locs[i], anchors[i], moms[i], stream)
+
+    for w in range(args.warmup):
+        redraw(w + 1)
+        barrier()
+        run_round()
+        torch.cuda.synchronize()
+
+    sync.set_profiling(True)
+    step_ms = []
+    phase_ms = {k: 0.0 for k in sync.PHASES}
+    k4_elems = 0
+    launches0 = sync.kernel_launches
+    clocks = Clocks(local_rank)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with clocks:
+        for s in range(args.steps):
+            redraw(args.warmup + s + 1)
+            barrier()
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            run_round()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            t = ev0.elapsed_time(ev1)
+            prof = sync.profile_collect()
+            for k, v in prof["ms"].items():
+                phase_ms[k] += v
+            k4_elems += prof["elements"]
+            if world > 1:
+                tt = torch.tensor([t], device=dev, dtype=torch.float64)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t = float(tt.item())
+            step_ms.append(t)
+    launches = sync.kernel_launches - launches0
+    sync.set_profiling(False)
+    clk = clocks.summary()
+    # every unit's outcome of the last round (checks nothing rolled back unexpectedly)
+    rollbacks = sum(int(sync.stats(i).rollback) for i in range(len(units)))
+    betas = [sync.stats(i).beta for i in (0, 1, len(units) - 1)]
+
+    total_ms = sum(step_ms)
+    ms_per_step = total_ms / len(step_ms)
+    bytes_per_rank_round = 4.0 * P_r
+    value = world * bytes_per_rank_round * len(step_ms) / (total_ms * 1e-3) / 1e9
+
+    peaks = measured_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    b_hbm = 16 + 2 * b_l                        # algorithmic HBM B/param
+    b_nvl = 8.0 * (N - 1) / N                   # NCCL bus bytes per direction per param
+    k4_ms = phase_ms["outer_update"]
+    k4_launches = args.steps * len(units)
+    k4_achieved = b_hbm * k4_elems / (k4_ms * 1e-3) / 1e9 if k4_ms > 0 else None
+    t_roof_nom = max(P_r * b_hbm / (NOMINAL_HBM_GBS * 1e9), P_r * b_nvl / (NOMINAL_NVL_GBS * 1e9)) * 1e3
+    t_roof_meas = max(P_r * b_hbm / (hbm_peak * 1e9), P_r * b_nvl / (MEASURED_NVL_GBS * 1e9)) * 1e3
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tinfo = json.load(f)
+        key = f"outer_update_{args.dtype}_{'S' if N > 1 else 'local'}"
+        if key in tinfo:
+            traffic = tinfo[key]["dram_bytes_per_elem"] * k4_elems / k4_launches
+
+    # e2e: same metric through the host-buffer C-ABI call (pinned host buffers; H2D of
+    # local/anchor/momentum and D2H of the three results inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        idx = [int(x) for x in args.e2e_units.split(",") if x.strip()]
+        h_loc = [locs[i].cpu().pin_memory() for i in idx]
+        h_anc = [anchors[i].cpu().pin_memory() for i in idx]
+        h_mom = [moms[i].cpu().pin_memory() for i in idx]
+        e_ms = []
+        for s in range(args.warmup + args.steps):
+            barrier()
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            for j, i in enumerate(idx):
+                sync.layer_sync_host(i, h_loc[j], h_anc[j], h_mom[j], stream)
+            sync.host_wait(stream)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            t = ev0.elapsed_time(ev1)
+            if world > 1:
+                tt = torch.tensor([t], device=dev, dtype=torch.float64)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t = float(tt.item())
+            if s >= args.warmup:
+                e_ms.append(t)
+        n_e = sum(numel[i] for i in idx)
+        e2e = {"value": world * 4.0 * n_e * len(e_ms) / (sum(e_ms) * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": (8 + b_l) * n_e, "d2h_bytes_per_step": (8 + b_l) * n_e,
+               "units": [units[i].name for i in idx],
+               "note": "host-buffer edit_layer_sync_host (CPU-offloaded anchor/momentum, P:123) over the "
+                       "listed units per step; pinned host memory, copies overlapped across units"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_cpu_baseline(args.model, dtype)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"llama-{args.model}-shaped shards, {M}x{N} shard x sync mesh, full sync round "
+                                   f"of {len(units)} units ({P_r} params/rank), {args.dtype} local + f32 "
+                                   "anchor/momentum",
+                       "mesh": f"{M}x{N}", "params_per_rank": P_r, "param_dtype": args.dtype,
+                       "l2": "inputs (%.1f GB/rank) larger than L2" % (P_r * (b_l + 8) / 1e9),
+                       "inner_steps": "locals redrawn as cast(anchor - D) between steps, outside the timed region"},
+            "roofline": {"bound": "hbm", "kernel": "outer_update (K4)", "achieved": k4_achieved, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": (k4_achieved / hbm_peak) if k4_achieved else None,
+                         "traffic": traffic, "algorithmic_bytes_per_param": b_hbm,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "_fallback" not in peaks
+                         else "fallback 6650 GB/s"},
+            "sync_roofline": {"t_roof_ms_nominal": t_roof_nom, "frac_nominal": t_roof_nom / ms_per_step,
+                              "t_roof_ms_measured": t_roof_meas, "frac_measured": t_roof_meas / ms_per_step,
+                              "bound": "hbm" if N == 1 else "nvlink", "hbm_B_per_param": b_hbm,
+                              "nvlink_B_per_param_per_dir": b_nvl},
+            "phases_ms_per_step": {k: v / args.steps for k, v in phase_ms.items()},
+            "per_gpu_GBps": bytes_per_rank_round / (ms_per_step * 1e-3) / 1e9,
+            "rollbacks_last_round": rollbacks, "beta_sample": betas,
+            "gpu_launches": launches, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    sync.close()
+    if world > 1:
+        dist.barrier(device_ids=[local_rank])
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

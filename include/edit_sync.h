@@ -1,0 +1,184 @@
+/*
+ * edit_sync.h -- C ABI of the B200-native EDiT layer-wise sync library
+ * (libedit_sync.so, built from paper_2412_07210_b200/csrc).
+ *
+ * What it computes: Sync() of PAPER.md Algorithm 2, the model
+ * synchronisation of EDiT with the pseudo-gradient penalty (Section 3.2,
+ * P:84-123), for ONE rank of an M x N device mesh (Section 3.1, P:61:
+ * M model sync groups of N workers = rows; N model shard groups of M workers =
+ * columns; K = M*N ranks, rank = sync_idx*M + shard_idx, reading R20 of
+ * DESIGN.md).  Per sync unit ("module") and call:
+ *
+ *   Delta   = anchor - local                             (Alg.2 l.442; sign R1)
+ *   G_n     = ||Delta_n||_2 over the whole module         (l.443, R5)
+ *   z-test against EMA (mu, sigma), G_n := inf if z > delta (l.444-446)
+ *   EMA update of every finite G_n (Eq. 1)
+ *   rollback iff no G_n finite (l.447-449, R11)
+ *   w_n     = exp(-G_n) / sum_j exp(-G_j)                 (Eq. 2, l.451)
+ *   Dbar    = sum_n w_n Delta_n over the sync group       (Eq. 3, l.452)
+ *   beta    = min(phi / (||Dbar|| + eps), 1)              (Eq. 4, l.453)
+ *   m       = mu m + beta Dbar ; anchor = anchor - nu (beta Dbar + mu m)
+ *                                                         (Eq. 5 + OuterOpt, l.454, R2)
+ *   local   = round_to_local_dtype(anchor)                (l.455)
+ *
+ * All device work is enqueued on the caller's stream; nothing here blocks the
+ * host except edit_sync_stats / get_state / set_state / destroy and init.
+ * There is no CPU fallback: without a CUDA device every call that needs one
+ * returns EDIT_ERR_CUDA.
+ */
+#ifndef EDIT_SYNC_H_
+#define EDIT_SYNC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EDIT_MAX_SYNC 8          /* N <= 8: one NVSwitch node                      */
+#define EDIT_MAX_SHARD 8         /* M <= 8                                         */
+#define EDIT_UNIQUE_ID_BYTES 128 /* == sizeof(ncclUniqueId)                        */
+
+typedef struct edit_sync* edit_sync_t;
+
+typedef enum {
+  EDIT_OK = 0,
+  EDIT_ERR_INVALID_ARG = 1, /* bad config / pointer / layer index / alignment    */
+  EDIT_ERR_CUDA = 2,        /* CUDA runtime error (text: edit_sync_last_error)   */
+  EDIT_ERR_NCCL = 3,        /* NCCL error                                        */
+  EDIT_ERR_STATE = 4,       /* handle poisoned by an earlier CUDA/NCCL error     */
+  EDIT_ERR_NO_MEMORY = 5    /* workspace too small / host allocation failed      */
+} edit_status_t;
+
+typedef enum { EDIT_BF16 = 0, EDIT_F32 = 1 } edit_dtype_t;
+
+/* Ablations of Section 4.5. */
+#define EDIT_NO_AE 1u /* w/o anomaly elimination: no z-test (non-finite G still excluded, R9) */
+#define EDIT_NO_WA 2u /* w/o weighted averaging: uniform 1/#finite                              */
+#define EDIT_NO_GC 4u /* w/o gradient clip: beta = 1                                            */
+
+typedef struct {
+  int32_t shard_dim;             /* M                                              */
+  int32_t sync_dim;              /* N; M*N = world size                             */
+  int32_t rank;                  /* 0 <= rank < M*N; sync_idx = rank / M, shard_idx = rank % M */
+  int32_t device;                /* CUDA ordinal this rank runs on                         */
+  int32_t num_layers;            /* L sync units                                           */
+  int32_t param_dtype;           /* edit_dtype_t of `local`; anchor/momentum are fp32      */
+  const int64_t* layer_numel;    /* [L] per-rank padded shard length (host memory, copied) */
+  float outer_lr;                /* nu    (0.8 / 1.0)                               */
+  float outer_momentum;          /* mu    (0.85 / 0.8)                              */
+  float clip_threshold;          /* phi   (10)                                      */
+  float clip_eps;                /* eps   (value unstated -> 1e-6, R12)             */
+  float anomaly_threshold;       /* delta (3)                                        */
+  float ema_alpha;               /* alpha (0.02)                                     */
+  int32_t ema_warmup_rounds;     /* EMA warm-up length (unstated -> 10, R8)          */
+  uint32_t flags;                /* EDIT_NO_AE | EDIT_NO_WA | EDIT_NO_GC                   */
+} edit_sync_config_t;
+
+/* Outcome of the last completed sync of one unit (device-written, D5). */
+typedef struct {
+  int64_t round;                     /* number of syncs of this unit so far            */
+  double G[EDIT_MAX_SYNC];           /* module-level ||Delta_n||, +inf if flagged       */
+  double z[EDIT_MAX_SYNC];           /* EMA z-score, NaN when the test was not applied */
+  double w[EDIT_MAX_SYNC];           /* Eq. 2 weights                                   */
+  int32_t anomalous[EDIT_MAX_SYNC];  /* 1 if G_n was set to infinity                    */
+  double G_bar;                      /* ||Dbar|| (module level), 0 on rollback          */
+  double beta;                       /* Eq. 4, 1 on rollback                            */
+  int32_t rollback;                  /* Alg. 2 l.448-449 taken                          */
+  int32_t num_sync;                  /* N                                               */
+  double ema_mu[EDIT_MAX_SYNC];      /* EMA after this sync, per replica n              */
+  double ema_sigma[EDIT_MAX_SYNC];
+  int64_t ema_count[EDIT_MAX_SYNC];
+} edit_layer_stats_t;
+
+/* EMA record of one (unit, replica): used by get_state / set_state. */
+typedef struct {
+  double mu;
+  double sigma;
+  int64_t count;
+  int64_t reserved;
+} edit_ema_t;
+
+/* Rank 0 creates the NCCL unique id; the caller broadcasts it to every rank
+ * (e.g. over a torch.distributed process group).  Not needed when M*N == 1. */
+edit_status_t edit_sync_get_unique_id(uint8_t id[EDIT_UNIQUE_ID_BYTES]);
+
+/* Device workspace the caller must provide to edit_sync_init (16-byte aligned,
+ * on cfg->device).  Holds the fp32 exchange buffer (N > 1: max layer_numel * 4 B),
+ * per-unit scratch, the EMA state [L][N] and the outcome records [L]. */
+edit_status_t edit_sync_workspace_bytes(const edit_sync_config_t* cfg, size_t* bytes);
+
+/* Collective over all M*N ranks (blocks until every rank has joined).
+ * Validates cfg (EDIT_ERR_INVALID_ARG for: null pointers; M, N < 1; M > 8;
+ * N > 8; rank outside [0, M*N); L < 1; negative numel; nu <= 0; mu outside
+ * [0, 1); phi <= 0; eps <= 0; alpha outside (0, 1]; delta <= 0; W < 0),
+ * creates the NCCL comms (global, sync = row, shard = column) and zeroes the
+ * EMA state (mu = sigma = 0, count = 0; R8).  The workspace stays owned by the
+ * caller and must outlive the handle. */
+edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDIT_UNIQUE_ID_BYTES],
+                             void* workspace, size_t workspace_bytes, edit_sync_t* out);
+
+/* Sync one unit (Alg. 2) in place:
+ *   local    [layer_numel[layer]] param_dtype, device  theta_{t,tau} in, theta_{t+1,0} out
+ *   anchor   [layer_numel[layer]] fp32, device         theta_t in, theta_{t+1} out
+ *   momentum [layer_numel[layer]] fp32, device         outer momentum, in/out
+ *   stream   cudaStream_t (NULL = legacy default stream)
+ * Buffers must be 16-byte aligned, must not alias each other or the workspace,
+ * and the zero-padded shard tail must be zero.  Every rank must call this for
+ * every unit in the same order (collective).  Enqueues only: no host sync, no
+ * data-dependent host branch (the rollback branch is taken on the device).
+ * EDIT_ERR_INVALID_ARG: null handle/pointer, layer outside [0, L), misalignment. */
+edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* anchor, float* momentum,
+                              void* stream);
+
+/* Host-buffer variant (the paper's CPU offload of the extra parameters and outer
+ * momentum): local/anchor/momentum live in host memory (page-locked for the
+ * copies to be asynchronous).  Per call: H2D of the three shards into one of two
+ * library-owned device staging slots (on an internal copy stream), the same device
+ * sync as edit_layer_sync on `stream`, then D2H of the three results back into the
+ * host buffers (on a second copy stream), so consecutive units overlap copy-in,
+ * compute and copy-out.  Staging is allocated on the first call (2 x max numel x
+ * (elem + 8) bytes).  The host buffers must stay valid and untouched until
+ * edit_sync_host_wait() on a stream has been reached. */
+edit_status_t edit_layer_sync_host(edit_sync_t h, int32_t layer, void* local_host, float* anchor_host,
+                                   float* momentum_host, void* stream);
+/* Makes `stream` wait until every outstanding host-variant copy-out has landed. */
+edit_status_t edit_sync_host_wait(edit_sync_t h, void* stream);
+
+/* Blocks until this unit's last enqueued sync has completed, then copies its
+ * outcome record to *out. */
+edit_status_t edit_sync_stats(edit_sync_t h, int32_t layer, edit_layer_stats_t* out);
+
+/* EMA state of every (unit, replica), row-major [L][N] edit_ema_t (host memory).
+ * get: *bytes in = capacity, out = size needed; set: bytes must equal L*N*sizeof(edit_ema_t).
+ * Both synchronise the device.  Used for checkpoint/resume and to seed tests. */
+edit_status_t edit_sync_get_state(edit_sync_t h, void* host_buf, size_t* bytes);
+edit_status_t edit_sync_set_state(edit_sync_t h, const void* host_buf, size_t bytes);
+
+/* Phase timing with CUDA events on the caller's stream (bench evidence, off by default).
+ * Phases: 0 = K1 pg_norm, 1 = norm gather + K2 decide, 2 = weighted all-reduce (N > 1),
+ * 3 = K3 + G_bar gather (N > 1), 4 = K4 outer_update.  collect() blocks until every unit
+ * synced since the last collect has completed and returns the per-phase sums (ms) over
+ * those syncs, plus the number of syncs and of elements the K4 launches processed. */
+#define EDIT_NUM_PHASES 5
+edit_status_t edit_sync_set_profiling(edit_sync_t h, int32_t enable);
+edit_status_t edit_sync_profile_collect(edit_sync_t h, double phase_ms[EDIT_NUM_PHASES], int64_t* syncs,
+                                        int64_t* elements);
+
+/* Number of kernels the library launched so far on this handle (bench evidence). */
+int64_t edit_sync_kernel_launches(edit_sync_t h);
+
+/* Frees library-owned resources (NCCL comms, ops, events); never the workspace. */
+edit_status_t edit_sync_destroy(edit_sync_t h);
+
+/* Text of the last error on the calling thread ("" if none). */
+const char* edit_sync_last_error(void);
+
+/* Library version string. */
+const char* edit_sync_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EDIT_SYNC_H_ */

@@ -1,0 +1,511 @@
+// api.cpp -- the C ABI of include/edit_sync.h: validation, NCCL communicators of the
+// M x N mesh (Alg. 1 l.400), workspace carving and the per-unit
+// enqueue sequence of Sync() (Alg. 2).
+//
+// Per unit, N > 1:
+//   K1 pg_norm(local, anchor -> S, ||Delta_shard||^2)
+//   ncclAllGather(1 fp64, global comm)          module norms + norm sync gamma
+//   K2 decide(-> w, rollback, EMA, record)
+//   ncclAllReduce(S, PreMulSum(w on device), sync comm)   Eq. 3 (l.452)
+//   K3 sumsq(S -> ||Dbar_shard||^2)
+//   ncclAllGather(1 fp64, shard comm)   (M > 1)           module-level G_bar
+//   K4 outer_update(S, anchor, momentum -> anchor, momentum, local)
+// N == 1: K1 (no S) -> [AllGather on the shard comm if M > 1] -> K2 -> K4 (recomputes
+// Delta from local and anchor): two HBM passes.
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace edit;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+edit_status_t fail(edit_status_t st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+  size_t s_off, s_bytes, scratch_off, ema_off, rec_off, total;
+};
+
+Layout layout_of(const edit_sync_config_t& c) {
+  Layout L{};
+  int64_t max_numel = 0;
+  for (int i = 0; i < c.num_layers; ++i) max_numel = std::max<int64_t>(max_numel, c.layer_numel[i]);
+  size_t off = 0;
+  L.s_off = off;
+  L.s_bytes = c.sync_dim > 1 ? align_up((size_t)max_numel * sizeof(float), 256) : 0;
+  off += L.s_bytes;
+  L.scratch_off = off;
+  off += align_up(sizeof(LayerScratch) * (size_t)c.num_layers, 256);
+  L.ema_off = off;
+  off += align_up(sizeof(edit_ema_t) * (size_t)c.num_layers * c.sync_dim, 256);
+  L.rec_off = off;
+  off += align_up(sizeof(edit_layer_stats_t) * (size_t)c.num_layers, 256);
+  L.total = off;
+  return L;
+}
+
+edit_status_t validate(const edit_sync_config_t* c) {
+  if (!c) return fail(EDIT_ERR_INVALID_ARG, "null config");
+  if (c->shard_dim < 1 || c->shard_dim > EDIT_MAX_SHARD)
+    return fail(EDIT_ERR_INVALID_ARG, "shard_dim (M) must be in [1, 8]");
+  if (c->sync_dim < 1 || c->sync_dim > EDIT_MAX_SYNC)
+    return fail(EDIT_ERR_INVALID_ARG, "sync_dim (N) must be in [1, 8]");
+  if (c->rank < 0 || c->rank >= c->shard_dim * c->sync_dim)
+    return fail(EDIT_ERR_INVALID_ARG, "rank must be in [0, M*N)");
+  if (c->num_layers < 1) return fail(EDIT_ERR_INVALID_ARG, "num_layers must be >= 1");
+  if (!c->layer_numel) return fail(EDIT_ERR_INVALID_ARG, "null layer_numel");
+  for (int i = 0; i < c->num_layers; ++i)
+    if (c->layer_numel[i] < 0) return fail(EDIT_ERR_INVALID_ARG, "negative layer_numel");
+  if (c->param_dtype != EDIT_BF16 && c->param_dtype != EDIT_F32)
+    return fail(EDIT_ERR_INVALID_ARG, "param_dtype must be EDIT_BF16 or EDIT_F32");
+  if (!(c->outer_lr > 0.f)) return fail(EDIT_ERR_INVALID_ARG, "outer_lr (nu) must be > 0");
+  if (!(c->outer_momentum >= 0.f && c->outer_momentum < 1.f))
+    return fail(EDIT_ERR_INVALID_ARG, "outer_momentum (mu) must be in [0, 1)");
+  if (!(c->clip_threshold > 0.f)) return fail(EDIT_ERR_INVALID_ARG, "clip_threshold (phi) must be > 0");
+  if (!(c->clip_eps > 0.f)) return fail(EDIT_ERR_INVALID_ARG, "clip_eps must be > 0");
+  if (!(c->ema_alpha > 0.f && c->ema_alpha <= 1.f))
+    return fail(EDIT_ERR_INVALID_ARG, "ema_alpha must be in (0, 1]");
+  if (!(c->anomaly_threshold > 0.f)) return fail(EDIT_ERR_INVALID_ARG, "anomaly_threshold (delta) must be > 0");
+  if (c->ema_warmup_rounds < 0) return fail(EDIT_ERR_INVALID_ARG, "ema_warmup_rounds must be >= 0");
+  if (c->flags & ~(EDIT_NO_AE | EDIT_NO_WA | EDIT_NO_GC)) return fail(EDIT_ERR_INVALID_ARG, "unknown flags");
+  return EDIT_OK;
+}
+
+}  // namespace
+
+struct edit_sync {
+  edit_sync_config_t cfg{};
+  std::vector<int64_t> numel;
+  int M = 1, N = 1, K = 1, sync_idx = 0, shard_idx = 0;
+  int num_sms = 0;
+  Occupancy occ{};
+  ncclComm_t global = nullptr, sync = nullptr, shard = nullptr;
+  std::vector<ncclRedOp_t> ops;  // per unit: PreMulSum with that unit's device weight
+  char* ws = nullptr;
+  float* S = nullptr;
+  LayerScratch* scratch = nullptr;
+  edit_ema_t* ema = nullptr;
+  edit_layer_stats_t* rec = nullptr;
+  std::vector<cudaEvent_t> done;  // per unit: recorded after its last kernel
+  // profiling: EDIT_NUM_PHASES + 1 timing events per unit, and the units pending collection
+  bool profiling = false;
+  std::vector<cudaEvent_t> prof;
+  std::vector<int32_t> pending;
+  // host-buffer variant: two device staging slots + copy-in / copy-out streams
+  char* staging = nullptr;
+  size_t slot_bytes = 0;
+  int next_slot = 0;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t slot_in[2] = {nullptr, nullptr}, slot_done[2] = {nullptr, nullptr},
+              slot_free[2] = {nullptr, nullptr};
+  bool poisoned = false;
+  int64_t launches = 0;
+};
+
+namespace {
+
+#define CUDA_TRY(h, expr)                                                                   \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      if (h) (h)->poisoned = true;                                                          \
+      return fail(EDIT_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_));         \
+    }                                                                                       \
+  } while (0)
+
+#define NCCL_TRY(h, expr)                                                                   \
+  do {                                                                                      \
+    ncclResult_t r_ = (expr);                                                               \
+    if (r_ != ncclSuccess) {                                                                \
+      if (h) (h)->poisoned = true;                                                          \
+      return fail(EDIT_ERR_NCCL, std::string(#expr ": ") + ncclGetErrorString(r_));         \
+    }                                                                                       \
+  } while (0)
+
+int grid_for(int64_t n, int blocks_per_sm, int num_sms) {
+  const int64_t want = (n / 8 + kThreads - 1) / kThreads;
+  const int64_t cap = std::min<int64_t>((int64_t)std::max(blocks_per_sm, 1) * num_sms, kMaxCtas);
+  return (int)std::max<int64_t>(1, std::min(want, cap));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* edit_sync_last_error(void) { return g_last_error.c_str(); }
+
+const char* edit_sync_version(void) { return "edit_sync 0.1 (sm_100a)"; }
+
+edit_status_t edit_sync_get_unique_id(uint8_t id[EDIT_UNIQUE_ID_BYTES]) {
+  static_assert(sizeof(ncclUniqueId) == EDIT_UNIQUE_ID_BYTES, "ncclUniqueId size");
+  if (!id) return fail(EDIT_ERR_INVALID_ARG, "null id");
+  ncclUniqueId u;
+  ncclResult_t r = ncclGetUniqueId(&u);
+  if (r != ncclSuccess) return fail(EDIT_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  memcpy(id, &u, sizeof u);
+  return EDIT_OK;
+}
+
+edit_status_t edit_sync_workspace_bytes(const edit_sync_config_t* cfg, size_t* bytes) {
+  edit_status_t st = validate(cfg);
+  if (st != EDIT_OK) return st;
+  if (!bytes) return fail(EDIT_ERR_INVALID_ARG, "null bytes");
+  *bytes = layout_of(*cfg).total;
+  return EDIT_OK;
+}
+
+edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDIT_UNIQUE_ID_BYTES],
+                             void* workspace, size_t workspace_bytes, edit_sync_t* out) {
+  edit_status_t st = validate(cfg);
+  if (st != EDIT_OK) return st;
+  if (!out) return fail(EDIT_ERR_INVALID_ARG, "null out");
+  *out = nullptr;
+  const Layout L = layout_of(*cfg);
+  if (!workspace) return fail(EDIT_ERR_INVALID_ARG, "null workspace");
+  if (((uintptr_t)workspace & 255u) != 0) return fail(EDIT_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  if (workspace_bytes < L.total) return fail(EDIT_ERR_NO_MEMORY, "workspace too small");
+  const int K = cfg->shard_dim * cfg->sync_dim;
+  if (K > 1 && !id) return fail(EDIT_ERR_INVALID_ARG, "null unique id for a multi-rank mesh");
+
+  edit_sync* h = new (std::nothrow) edit_sync();
+  if (!h) return fail(EDIT_ERR_NO_MEMORY, "host allocation");
+  h->cfg = *cfg;
+  h->numel.assign(cfg->layer_numel, cfg->layer_numel + cfg->num_layers);
+  h->cfg.layer_numel = h->numel.data();
+  h->M = cfg->shard_dim;
+  h->N = cfg->sync_dim;
+  h->K = K;
+  h->sync_idx = cfg->rank / h->M;   // row index n (R20)
+  h->shard_idx = cfg->rank % h->M;  // column index m
+
+  auto bail = [&](edit_status_t s) {
+    edit_sync_destroy(h);
+    return s;
+  };
+#define INIT_CUDA(expr)                                                                     \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return bail(fail(EDIT_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)));   \
+  } while (0)
+#define INIT_NCCL(expr)                                                                     \
+  do {                                                                                      \
+    ncclResult_t r_ = (expr);                                                               \
+    if (r_ != ncclSuccess)                                                                  \
+      return bail(fail(EDIT_ERR_NCCL, std::string(#expr ": ") + ncclGetErrorString(r_)));   \
+  } while (0)
+
+  INIT_CUDA(cudaSetDevice(cfg->device));
+  INIT_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
+  INIT_CUDA(query_occupancy(&h->occ));
+
+  h->ws = static_cast<char*>(workspace);
+  h->S = L.s_bytes ? reinterpret_cast<float*>(h->ws + L.s_off) : nullptr;
+  h->scratch = reinterpret_cast<LayerScratch*>(h->ws + L.scratch_off);
+  h->ema = reinterpret_cast<edit_ema_t*>(h->ws + L.ema_off);
+  h->rec = reinterpret_cast<edit_layer_stats_t*>(h->ws + L.rec_off);
+  // zero scratch (ticket counters), EMA (mu = sigma = 0, count = 0: R8) and records
+  INIT_CUDA(cudaMemset(h->ws + L.scratch_off, 0, L.total - L.scratch_off));
+  INIT_CUDA(cudaDeviceSynchronize());
+
+  h->done.assign(cfg->num_layers, nullptr);
+  for (auto& e : h->done) INIT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+
+  if (K > 1) {
+    ncclUniqueId u;
+    memcpy(&u, id, sizeof u);
+    INIT_NCCL(ncclCommInitRank(&h->global, K, u, cfg->rank));
+    // sync group (row): same shard index m, ordered by n; shard group (column): same n.
+    INIT_NCCL(ncclCommSplit(h->global, h->shard_idx, h->sync_idx, &h->sync, nullptr));
+    INIT_NCCL(ncclCommSplit(h->global, h->sync_idx, h->shard_idx, &h->shard, nullptr));
+    if (h->N > 1) {
+      h->ops.assign(cfg->num_layers, ncclRedOp_t{});
+      for (int l = 0; l < cfg->num_layers; ++l)
+        INIT_NCCL(ncclRedOpCreatePreMulSum(&h->ops[l], &h->scratch[l].w, ncclFloat32,
+                                           ncclScalarDevice, h->sync));
+    }
+  }
+#undef INIT_CUDA
+#undef INIT_NCCL
+  *out = h;
+  return EDIT_OK;
+}
+
+edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* anchor, float* momentum,
+                              void* stream) {
+  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
+  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  if (layer < 0 || layer >= h->cfg.num_layers) return fail(EDIT_ERR_INVALID_ARG, "layer out of range");
+  const int64_t n = h->numel[layer];
+  if (n > 0 && (!local || !anchor || !momentum)) return fail(EDIT_ERR_INVALID_ARG, "null buffer");
+  if ((((uintptr_t)local) | ((uintptr_t)anchor) | ((uintptr_t)momentum)) & 15u)
+    return fail(EDIT_ERR_INVALID_ARG, "buffers must be 16-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int dt = h->cfg.param_dtype;
+  LayerScratch* scr = &h->scratch[layer];
+  const int M = h->M, N = h->N;
+  int launched = 0;
+
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  cudaEvent_t* ev = h->profiling ? &h->prof[(size_t)layer * (EDIT_NUM_PHASES + 1)] : nullptr;
+  if (ev) CUDA_TRY(h, cudaEventRecord(ev[0], st));
+  // K1: Delta and its shard norm (Alg. 2 l.442-443)
+  float* S = N > 1 ? h->S : nullptr;
+  launched += launch_pg_norm(dt, local, anchor, S, n, scr,
+                             grid_for(n, h->occ.pg_norm[dt][S ? 1 : 0], h->num_sms), st);
+  CUDA_TRY(h, cudaGetLastError());
+  if (ev) CUDA_TRY(h, cudaEventRecord(ev[1], st));
+  // module norms of every replica on every rank: one K-scalar gather (R6)
+  const double* parts = &scr->send1;
+  if (h->K > 1) {
+    NCCL_TRY(h, ncclAllGather(&scr->send1, scr->recv1, 1, ncclFloat64, h->global, st));
+    parts = scr->recv1;
+  }
+  DecideArgs d{};
+  d.parts = parts;
+  d.M = M;
+  d.N = N;
+  d.my_n = h->sync_idx;
+  d.ema = h->ema + (size_t)layer * N;
+  d.rec = h->rec + layer;
+  d.w_out = &scr->w;
+  d.rollback_out = &scr->rollback;
+  d.gsq_out = &scr->gsq;
+  d.alpha = h->cfg.ema_alpha;
+  d.delta = h->cfg.anomaly_threshold;
+  d.warmup = h->cfg.ema_warmup_rounds;
+  d.flags = h->cfg.flags;
+  launched += launch_decide(d, st);
+  CUDA_TRY(h, cudaGetLastError());
+  if (ev) CUDA_TRY(h, cudaEventRecord(ev[2], st));
+
+  UpdateArgs u{};
+  u.local = local;
+  u.anchor = anchor;
+  u.momentum = momentum;
+  u.n = n;
+  u.rollback = &scr->rollback;
+  u.nu = h->cfg.outer_lr;
+  u.mu = h->cfg.outer_momentum;
+  u.phi = h->cfg.clip_threshold;
+  u.eps = h->cfg.clip_eps;
+  u.flags = h->cfg.flags;
+  u.rec = h->rec + layer;
+  if (N > 1) {
+    // Eq. 3: Dbar = sum_n w_n Delta_n, the weight applied inside NCCL (PreMulSum)
+    NCCL_TRY(h, ncclAllReduce(S, S, (size_t)n, ncclFloat32, h->ops[layer], h->sync, st));
+    if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
+    launched += launch_sumsq(S, n, scr, grid_for(n, h->occ.sumsq, h->num_sms), st);
+    CUDA_TRY(h, cudaGetLastError());
+    if (M > 1) {
+      NCCL_TRY(h, ncclAllGather(&scr->send2, scr->recv2, 1, ncclFloat64, h->shard, st));
+      u.gparts = scr->recv2;
+      u.n_gparts = M;
+    } else {
+      u.gparts = &scr->send2;
+      u.n_gparts = 1;
+    }
+    u.dbar = S;
+    if (ev) CUDA_TRY(h, cudaEventRecord(ev[4], st));
+  } else {
+    if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
+    if (ev) CUDA_TRY(h, cudaEventRecord(ev[4], st));
+    u.dbar = nullptr;  // Dbar = Delta, G_bar = G (module level)
+    u.gparts = &scr->gsq;
+    u.n_gparts = 1;
+  }
+  launched += launch_update(dt, u, grid_for(n, h->occ.update[dt][N > 1 ? 1 : 0], h->num_sms), st);
+  CUDA_TRY(h, cudaGetLastError());
+  if (ev) {
+    CUDA_TRY(h, cudaEventRecord(ev[5], st));
+    h->pending.push_back(layer);
+  }
+  CUDA_TRY(h, cudaEventRecord(h->done[layer], st));
+  h->launches += launched;
+  return EDIT_OK;
+}
+
+edit_status_t edit_layer_sync_host(edit_sync_t h, int32_t layer, void* local_host, float* anchor_host,
+                                   float* momentum_host, void* stream) {
+  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
+  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  if (layer < 0 || layer >= h->cfg.num_layers) return fail(EDIT_ERR_INVALID_ARG, "layer out of range");
+  const int64_t n = h->numel[layer];
+  if (n > 0 && (!local_host || !anchor_host || !momentum_host)) return fail(EDIT_ERR_INVALID_ARG, "null buffer");
+  const size_t esz = h->cfg.param_dtype == EDIT_BF16 ? 2 : 4;
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  if (!h->staging) {
+    int64_t max_numel = 0;
+    for (int64_t x : h->numel) max_numel = std::max(max_numel, x);
+    // per slot: anchor | momentum | local, each 256-byte aligned
+    h->slot_bytes = align_up((size_t)max_numel * 4, 256) * 2 + align_up((size_t)max_numel * esz, 256);
+    CUDA_TRY(h, cudaMalloc(reinterpret_cast<void**>(&h->staging), 2 * h->slot_bytes));
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->slot_in[i], cudaEventDisableTiming));
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->slot_done[i], cudaEventDisableTiming));
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->slot_free[i], cudaEventDisableTiming));
+      CUDA_TRY(h, cudaEventRecord(h->slot_free[i], h->d2h));
+    }
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int slot = h->next_slot;
+  h->next_slot ^= 1;
+  char* base = h->staging + (size_t)slot * h->slot_bytes;
+  const size_t fbytes = align_up((size_t)std::max<int64_t>(n, 1) * 4, 256);
+  float* anc = reinterpret_cast<float*>(base);
+  float* mom = reinterpret_cast<float*>(base + fbytes);
+  void* loc = base + 2 * fbytes;
+  // copy-in once the slot's previous copy-out has drained
+  CUDA_TRY(h, cudaStreamWaitEvent(h->h2d, h->slot_free[slot], 0));
+  CUDA_TRY(h, cudaMemcpyAsync(anc, anchor_host, (size_t)n * 4, cudaMemcpyHostToDevice, h->h2d));
+  CUDA_TRY(h, cudaMemcpyAsync(mom, momentum_host, (size_t)n * 4, cudaMemcpyHostToDevice, h->h2d));
+  CUDA_TRY(h, cudaMemcpyAsync(loc, local_host, (size_t)n * esz, cudaMemcpyHostToDevice, h->h2d));
+  CUDA_TRY(h, cudaEventRecord(h->slot_in[slot], h->h2d));
+  CUDA_TRY(h, cudaStreamWaitEvent(st, h->slot_in[slot], 0));
+  edit_status_t rc = edit_layer_sync(h, layer, loc, anc, mom, stream);
+  if (rc != EDIT_OK) return rc;
+  CUDA_TRY(h, cudaEventRecord(h->slot_done[slot], st));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->d2h, h->slot_done[slot], 0));
+  CUDA_TRY(h, cudaMemcpyAsync(anchor_host, anc, (size_t)n * 4, cudaMemcpyDeviceToHost, h->d2h));
+  CUDA_TRY(h, cudaMemcpyAsync(momentum_host, mom, (size_t)n * 4, cudaMemcpyDeviceToHost, h->d2h));
+  CUDA_TRY(h, cudaMemcpyAsync(local_host, loc, (size_t)n * esz, cudaMemcpyDeviceToHost, h->d2h));
+  CUDA_TRY(h, cudaEventRecord(h->slot_free[slot], h->d2h));
+  return EDIT_OK;
+}
+
+edit_status_t edit_sync_host_wait(edit_sync_t h, void* stream) {
+  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
+  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  if (!h->staging) return EDIT_OK;
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int i = 0; i < 2; ++i) CUDA_TRY(h, cudaStreamWaitEvent(st, h->slot_free[i], 0));
+  return EDIT_OK;
+}
+
+edit_status_t edit_sync_stats(edit_sync_t h, int32_t layer, edit_layer_stats_t* out) {
+  if (!h || !out) return fail(EDIT_ERR_INVALID_ARG, "null argument");
+  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  if (layer < 0 || layer >= h->cfg.num_layers) return fail(EDIT_ERR_INVALID_ARG, "layer out of range");
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  CUDA_TRY(h, cudaEventSynchronize(h->done[layer]));
+  if (h->global) {
+    ncclResult_t async_err = ncclSuccess;
+    NCCL_TRY(h, ncclCommGetAsyncError(h->global, &async_err));
+    if (async_err != ncclSuccess) {
+      h->poisoned = true;
+      return fail(EDIT_ERR_NCCL, std::string("async NCCL error: ") + ncclGetErrorString(async_err));
+    }
+  }
+  CUDA_TRY(h, cudaMemcpy(out, h->rec + layer, sizeof *out, cudaMemcpyDeviceToHost));
+  return EDIT_OK;
+}
+
+edit_status_t edit_sync_get_state(edit_sync_t h, void* host_buf, size_t* bytes) {
+  if (!h || !bytes) return fail(EDIT_ERR_INVALID_ARG, "null argument");
+  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  const size_t need = sizeof(edit_ema_t) * (size_t)h->cfg.num_layers * h->N;
+  if (!host_buf || *bytes < need) {
+    *bytes = need;
+    return host_buf ? fail(EDIT_ERR_NO_MEMORY, "state buffer too small") : EDIT_OK;
+  }
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  CUDA_TRY(h, cudaDeviceSynchronize());
+  CUDA_TRY(h, cudaMemcpy(host_buf, h->ema, need, cudaMemcpyDeviceToHost));
+  *bytes = need;
+  return EDIT_OK;
+}
+
+edit_status_t edit_sync_set_state(edit_sync_t h, const void* host_buf, size_t bytes) {
+  if (!h || !host_buf) return fail(EDIT_ERR_INVALID_ARG, "null argument");
+  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  const size_t need = sizeof(edit_ema_t) * (size_t)h->cfg.num_layers * h->N;
+  if (bytes != need) return fail(EDIT_ERR_INVALID_ARG, "state size must be L*N*sizeof(edit_ema_t)");
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  CUDA_TRY(h, cudaDeviceSynchronize());
+  CUDA_TRY(h, cudaMemcpy(h->ema, host_buf, need, cudaMemcpyHostToDevice));
+  return EDIT_OK;
+}
+
+edit_status_t edit_sync_set_profiling(edit_sync_t h, int32_t enable) {
+  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
+  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  if (enable && h->prof.empty()) {
+    h->prof.assign((size_t)h->cfg.num_layers * (EDIT_NUM_PHASES + 1), nullptr);
+    for (auto& e : h->prof) CUDA_TRY(h, cudaEventCreate(&e));
+  }
+  h->profiling = enable != 0;
+  h->pending.clear();
+  return EDIT_OK;
+}
+
+edit_status_t edit_sync_profile_collect(edit_sync_t h, double phase_ms[EDIT_NUM_PHASES], int64_t* syncs,
+                                        int64_t* elements) {
+  if (!h || !phase_ms) return fail(EDIT_ERR_INVALID_ARG, "null argument");
+  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  for (int p = 0; p < EDIT_NUM_PHASES; ++p) phase_ms[p] = 0.0;
+  int64_t elems = 0;
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  for (int32_t layer : h->pending) {
+    cudaEvent_t* ev = &h->prof[(size_t)layer * (EDIT_NUM_PHASES + 1)];
+    CUDA_TRY(h, cudaEventSynchronize(ev[EDIT_NUM_PHASES]));
+    for (int p = 0; p < EDIT_NUM_PHASES; ++p) {
+      float ms = 0.f;
+      CUDA_TRY(h, cudaEventElapsedTime(&ms, ev[p], ev[p + 1]));
+      phase_ms[p] += ms;
+    }
+    elems += h->numel[layer];
+  }
+  if (syncs) *syncs = (int64_t)h->pending.size();
+  if (elements) *elements = elems;
+  h->pending.clear();
+  return EDIT_OK;
+}
+
+int64_t edit_sync_kernel_launches(edit_sync_t h) { return h ? h->launches : -1; }
+
+edit_status_t edit_sync_destroy(edit_sync_t h) {
+  if (!h) return EDIT_OK;
+  edit_status_t st = EDIT_OK;
+  cudaSetDevice(h->cfg.device);
+  if (!h->poisoned) cudaDeviceSynchronize();
+  for (size_t l = 0; l < h->ops.size(); ++l)
+    if (h->sync) ncclRedOpDestroy(h->ops[l], h->sync);
+  if (h->shard) ncclCommDestroy(h->shard);
+  if (h->sync) ncclCommDestroy(h->sync);
+  if (h->global) ncclCommDestroy(h->global);
+  for (auto e : h->done)
+    if (e) cudaEventDestroy(e);
+  for (auto e : h->prof)
+    if (e) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (h->slot_in[i]) cudaEventDestroy(h->slot_in[i]);
+    if (h->slot_done[i]) cudaEventDestroy(h->slot_done[i]);
+    if (h->slot_free[i]) cudaEventDestroy(h->slot_free[i]);
+  }
+  if (h->h2d) cudaStreamDestroy(h->h2d);
+  if (h->d2h) cudaStreamDestroy(h->d2h);
+  if (h->staging) cudaFree(h->staging);
+  delete h;
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,363 @@
+// kernels.cu -- sm_100a kernels of the EDiT layer-wise sync (Alg. 2).
+//
+// The path is HBM-bound streaming plus reductions (no tensor cores):
+//   K1 pg_norm       Delta = anchor - local, sum Delta^2 (Alg.2 l.442-443); N > 1 also
+//                    writes Delta (non-finite -> 0, R9) into the fp32 exchange buffer S.
+//   K2 decide        one thread: module norms G_n, EMA z-test, Eq. 1, Eq. 2 weights,
+//                    rollback test (l.447-451).
+//   K3 sumsq         sum Dbar^2 of the all-reduced S (Eq. 4 numerator input).
+//   K4 outer_update  beta (Eq. 4) in the prologue; m = mu m + beta Dbar;
+//                    a = a - nu (beta Dbar + mu m); local = rne(a) (Eq. 5, l.454-455);
+//                    rollback branch local = rne(a) (l.449).  N == 1 recomputes
+//                    Dbar = Delta = a - local from the inputs (2-pass sync).
+// Every reduction is deterministic: a fixed grid for a given length, fixed per-thread
+// element sets, warp-shuffle/CTA trees, and the last CTA adding the per-CTA partials in
+// index order in fp64.
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include "internal.h"
+
+namespace edit {
+namespace {
+
+// ---------------------------------------------------------------- vector IO
+// 8 elements per thread-iteration: one 16-byte load of bf16 or two of fp32.
+__device__ __forceinline__ void load8(const float* __restrict__ p, float (&v)[8]) {
+  const float4 a = __ldcs(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void load8(const __nv_bfloat16* __restrict__ p, float (&v)[8]) {
+  const uint4 r = __ldcs(reinterpret_cast<const uint4*>(p));
+  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[2 * i] = __uint_as_float(w[i] << 16);
+    v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+__device__ __forceinline__ void store8(float* __restrict__ p, const float (&v)[8]) {
+  __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+  __stcs(reinterpret_cast<float4*>(p) + 1, make_float4(v[4], v[5], v[6], v[7]));
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* __restrict__ p, const float (&v)[8]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);  // RNE (R16)
+    w[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  __stcs(reinterpret_cast<uint4*>(p), make_uint4(w[0], w[1], w[2], w[3]));
+}
+__device__ __forceinline__ float load1(const float* p) { return *p; }
+__device__ __forceinline__ float load1(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ void store1(float* p, float v) { *p = v; }
+__device__ __forceinline__ void store1(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+
+// ---------------------------------------------------------------- reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Sum over the CTA (result valid in thread 0).  Fixed tree: deterministic.
+__device__ double block_sum(double v) {
+  __shared__ double ws[kThreads / 32];
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) ws[warp] = v;
+  __syncthreads();
+  v = 0.0;
+  if (warp == 0) {
+    v = lane < (kThreads / 32) ? ws[lane] : 0.0;
+    v = warp_sum(v);
+  }
+  __syncthreads();
+  return v;
+}
+
+// Writes this CTA's partial; the last CTA to finish adds all partials in index order
+// (fp64) and stores the total in *out, then re-arms the ticket counter.
+__device__ void finish_partials(double cta_total, double* cta_parts, uint32_t* counter, double* out) {
+  __shared__ bool is_last;
+  if (threadIdx.x == 0) {
+    cta_parts[blockIdx.x] = cta_total;
+    __threadfence();
+    is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  double v = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) v += __ldcg(cta_parts + i);
+  v = block_sum(v);
+  if (threadIdx.x == 0) {
+    *out = v;
+    *counter = 0u;
+  }
+}
+
+// ---------------------------------------------------------------- K1
+// Alg. 2 l.442-443: Delta = anchor - local; partial ||Delta||^2 of this shard.
+template <typename T, bool kWriteS>
+__global__ void __launch_bounds__(kThreads) pg_norm_kernel(const T* __restrict__ local,
+                                                           const float* __restrict__ anchor,
+                                                           float* __restrict__ S, int64_t n,
+                                                           LayerScratch* __restrict__ scr) {
+  const int64_t n8 = n >> 3;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n8; i += stride) {
+    float l[8], a[8], d[8];
+    load8(local + 8 * i, l);
+    load8(anchor + 8 * i, a);
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      d[j] = a[j] - l[j];
+      s = fmaf(d[j], d[j], s);
+    }
+    acc += (double)s;
+    if (kWriteS) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) d[j] = isfinite(d[j]) ? d[j] : 0.f;  // R9: w = 0 must give 0
+      store8(S + 8 * i, d);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 7)) {  // ragged tail (< 8 elements)
+    const int64_t k = 8 * n8 + threadIdx.x;
+    const float d = anchor[k] - load1(local + k);
+    acc += (double)(d * d);
+    if (kWriteS) S[k] = isfinite(d) ? d : 0.f;
+  }
+  acc = block_sum(acc);
+  finish_partials(acc, scr->cta1, &scr->counter1, &scr->send1);
+}
+
+// ---------------------------------------------------------------- K3
+// Eq. 4: partial ||Dbar||^2 of this shard of the all-reduced pseudo-gradient.
+__global__ void __launch_bounds__(kThreads) sumsq_kernel(const float* __restrict__ x, int64_t n,
+                                                         LayerScratch* __restrict__ scr) {
+  const int64_t n8 = n >> 3;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n8; i += stride) {
+    float v[8];
+    load8(x + 8 * i, v);
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s = fmaf(v[j], v[j], s);
+    acc += (double)s;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 7)) {
+    const float v = x[8 * n8 + threadIdx.x];
+    acc += (double)(v * v);
+  }
+  acc = block_sum(acc);
+  finish_partials(acc, scr->cta2, &scr->counter2, &scr->send2);
+}
+
+// ---------------------------------------------------------------- K2
+// Alg. 2 l.443-451 on the gathered scalars, identically on every rank (R6): all N
+// replicas' norms, z-tests, EMA updates (Eq. 1) and weights (Eq. 2).  One thread:
+// N <= 8 scalars, fp64, fixed order.
+__global__ void decide_kernel(DecideArgs p) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double G[EDIT_MAX_SYNC];
+  const int M = p.M, N = p.N;
+  edit_layer_stats_t* rec = p.rec;
+  for (int n = 0; n < N; ++n) {
+    double s = 0.0;
+    for (int m = 0; m < M; ++m) s += p.parts[n * M + m];  // module-level norm (R5)
+    G[n] = sqrt(s);
+  }
+  // IsAnomaly (R7-R10) with the pre-update EMA, then Eq. 1 for finite G.
+  for (int n = 0; n < N; ++n) {
+    edit_ema_t e = p.ema[n];
+    double z = nan("");
+    bool flagged = !isfinite(G[n]);  // R9: always excluded
+    if (!flagged && !(p.flags & EDIT_NO_AE) && e.count >= p.warmup && e.sigma > 0.0) {
+      z = (G[n] - e.mu) / e.sigma;
+      flagged = z > p.delta;
+    }
+    rec->z[n] = z;
+    rec->anomalous[n] = flagged ? 1 : 0;
+    if (flagged) {
+      G[n] = INFINITY;  // Alg. 2 l.445; Eq. 1 skipped
+    } else {
+      const double mu_new = p.alpha * G[n] + (1.0 - p.alpha) * e.mu;
+      const double dev = G[n] - mu_new;
+      e.sigma = sqrt((1.0 - p.alpha) * e.sigma * e.sigma + p.alpha * dev * dev);
+      e.mu = mu_new;
+      e.count += 1;
+      p.ema[n] = e;
+    }
+    rec->G[n] = G[n];
+    rec->ema_mu[n] = e.mu;
+    rec->ema_sigma[n] = e.sigma;
+    rec->ema_count[n] = e.count;
+  }
+  // gamma == 0 <=> no finite G (R11); Eq. 2 with exp(G_min) cancelled.
+  int nfinite = 0;
+  double gmin = INFINITY;
+  for (int n = 0; n < N; ++n)
+    if (isfinite(G[n])) {
+      ++nfinite;
+      gmin = fmin(gmin, G[n]);
+    }
+  double w[EDIT_MAX_SYNC];
+  double gamma = 0.0;
+  for (int n = 0; n < N; ++n) {
+    if (!isfinite(G[n])) w[n] = 0.0;
+    else w[n] = (p.flags & EDIT_NO_WA) ? 1.0 : exp(-(G[n] - gmin));
+    gamma += w[n];
+  }
+  const int rollback = nfinite == 0;
+  for (int n = 0; n < N; ++n) {
+    w[n] = rollback ? 0.0 : w[n] / gamma;
+    rec->w[n] = w[n];
+  }
+  for (int n = N; n < EDIT_MAX_SYNC; ++n) {
+    rec->G[n] = 0.0; rec->z[n] = 0.0; rec->w[n] = 0.0; rec->anomalous[n] = 0;
+  }
+  rec->num_sync = N;
+  *p.w_out = (float)w[p.my_n];
+  *p.rollback_out = rollback;
+  *p.gsq_out = rollback ? 0.0 : G[p.my_n] * G[p.my_n];  // N == 1: G_bar = G
+}
+
+// ---------------------------------------------------------------- K4
+// beta (Eq. 4), then OuterOpt = Nesterov (R2) on (anchor, momentum) and the
+// write-back local = rne(anchor) (Alg. 2 l.454-455).  Rollback: local = rne(anchor).
+template <typename T, bool kFromS>
+__global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
+  T* __restrict__ local = static_cast<T*>(p.local);
+  float* __restrict__ anchor = p.anchor;
+  float* __restrict__ mom = p.momentum;
+  const float* __restrict__ dbar = p.dbar;
+  double gsq = 0.0;
+  for (int i = 0; i < p.n_gparts; ++i) gsq += p.gparts[i];  // module level, m order
+  const double gbar = sqrt(gsq);
+  double beta_d = p.phi / (gbar + p.eps);
+  beta_d = beta_d < 1.0 ? beta_d : 1.0;
+  if (p.flags & EDIT_NO_GC) beta_d = 1.0;
+  const int rollback = *p.rollback;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.rec->G_bar = rollback ? 0.0 : gbar;
+    p.rec->beta = rollback ? 1.0 : beta_d;
+    p.rec->rollback = rollback;
+    p.rec->round += 1;
+  }
+  const float beta = (float)beta_d, mu = p.mu, nu = p.nu;
+  const int64_t n8 = p.n >> 3;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  const int64_t first = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const int tail = (blockIdx.x == 0 && threadIdx.x < (p.n & 7)) ? 1 : 0;
+  if (rollback) {  // Alg. 2 l.449: theta_{t+1,0} = theta_t (R14)
+    for (int64_t i = first; i < n8; i += stride) {
+      float a[8];
+      load8(anchor + 8 * i, a);
+      store8(local + 8 * i, a);
+    }
+    if (tail) {
+      const int64_t k = 8 * n8 + threadIdx.x;
+      store1(local + k, anchor[k]);
+    }
+    return;
+  }
+  for (int64_t i = first; i < n8; i += stride) {
+    float a[8], m[8], d[8];
+    if (kFromS) {
+      load8(dbar + 8 * i, d);
+    } else {
+      float l[8];
+      load8(local + 8 * i, l);
+      load8(anchor + 8 * i, a);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) d[j] = a[j] - l[j];  // N == 1: Dbar = Delta
+    }
+    if (kFromS) load8(anchor + 8 * i, a);
+    load8(mom + 8 * i, m);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float g = beta * d[j];          // Eq. 5
+      m[j] = fmaf(mu, m[j], g);             // m' = mu m + g
+      a[j] = a[j] - nu * fmaf(mu, m[j], g); // a' = a - nu (g + mu m')
+    }
+    store8(mom + 8 * i, m);
+    store8(anchor + 8 * i, a);
+    store8(local + 8 * i, a);
+  }
+  if (tail) {
+    const int64_t k = 8 * n8 + threadIdx.x;
+    const float d = kFromS ? dbar[k] : anchor[k] - load1(local + k);
+    const float g = beta * d;
+    const float m = fmaf(mu, mom[k], g);
+    const float a = anchor[k] - nu * fmaf(mu, m, g);
+    mom[k] = m;
+    anchor[k] = a;
+    store1(local + k, a);
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- launchers
+int launch_pg_norm(int dtype, const void* local, const float* anchor, float* S, int64_t n,
+                   LayerScratch* scr, int grid, cudaStream_t st) {
+  if (dtype == EDIT_BF16) {
+    if (S) pg_norm_kernel<__nv_bfloat16, true><<<grid, kThreads, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(local), anchor, S, n, scr);
+    else pg_norm_kernel<__nv_bfloat16, false><<<grid, kThreads, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(local), anchor, S, n, scr);
+  } else {
+    if (S) pg_norm_kernel<float, true><<<grid, kThreads, 0, st>>>(
+        static_cast<const float*>(local), anchor, S, n, scr);
+    else pg_norm_kernel<float, false><<<grid, kThreads, 0, st>>>(
+        static_cast<const float*>(local), anchor, S, n, scr);
+  }
+  return 1;
+}
+
+int launch_sumsq(const float* x, int64_t n, LayerScratch* scr, int grid, cudaStream_t st) {
+  sumsq_kernel<<<grid, kThreads, 0, st>>>(x, n, scr);
+  return 1;
+}
+
+int launch_decide(const DecideArgs& a, cudaStream_t st) {
+  decide_kernel<<<1, 32, 0, st>>>(a);
+  return 1;
+}
+
+int launch_update(int dtype, const UpdateArgs& a, int grid, cudaStream_t st) {
+  if (dtype == EDIT_BF16) {
+    if (a.dbar) outer_update_kernel<__nv_bfloat16, true><<<grid, kThreads, 0, st>>>(a);
+    else outer_update_kernel<__nv_bfloat16, false><<<grid, kThreads, 0, st>>>(a);
+  } else {
+    if (a.dbar) outer_update_kernel<float, true><<<grid, kThreads, 0, st>>>(a);
+    else outer_update_kernel<float, false><<<grid, kThreads, 0, st>>>(a);
+  }
+  return 1;
+}
+
+cudaError_t query_occupancy(Occupancy* occ) {
+  cudaError_t e = cudaSuccess;
+#define OCC(dst, fn) \
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&(dst), fn, kThreads, 0)
+  OCC(occ->pg_norm[EDIT_BF16][0], (pg_norm_kernel<__nv_bfloat16, false>));
+  OCC(occ->pg_norm[EDIT_BF16][1], (pg_norm_kernel<__nv_bfloat16, true>));
+  OCC(occ->pg_norm[EDIT_F32][0], (pg_norm_kernel<float, false>));
+  OCC(occ->pg_norm[EDIT_F32][1], (pg_norm_kernel<float, true>));
+  OCC(occ->sumsq, sumsq_kernel);
+  OCC(occ->update[EDIT_BF16][0], (outer_update_kernel<__nv_bfloat16, false>));
+  OCC(occ->update[EDIT_BF16][1], (outer_update_kernel<__nv_bfloat16, true>));
+  OCC(occ->update[EDIT_F32][0], (outer_update_kernel<float, false>));
+  OCC(occ->update[EDIT_F32][1], (outer_update_kernel<float, true>));
+#undef OCC
+  return e;
+}
+
+}  // namespace edit

@@ -1,0 +1,198 @@
+"""Single-GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, on
+seeded synthetic inputs (synth/), mesh 1 x 1 (N = 1: the two-pass path).
+
+Multi-rank parity lives in tests/test_gpu_multirank.py."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests import parity
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU boxes too; every test here is -m gpu
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2412_07210_b200 import EditSync  # noqa: E402
+from paper_2412_07210_b200.build import build  # noqa: E402
+
+build()
+DEV = torch.device("cuda", 0)
+DTYPES = {"bf16": torch.bfloat16, "f32": torch.float32}
+
+
+def _cfg_kwargs(cfg: oracle.Config):
+    return dict(outer_lr=cfg.outer_lr, outer_momentum=cfg.outer_momentum, clip_threshold=cfg.clip_threshold,
+                clip_eps=cfg.clip_eps, anomaly_threshold=cfg.anomaly_threshold, ema_alpha=cfg.ema_alpha,
+                ema_warmup_rounds=cfg.ema_warmup_rounds, flags=cfg.flags)
+
+
+class Case:
+    """One rank (1 x 1 mesh) holding L units, with the oracle's mirror of its state."""
+
+    def __init__(self, units, dtype, cfg=oracle.Config(), recipe=synth.Recipe(), plant=None):
+        self.units, self.dtype, self.cfg, self.recipe = units, dtype, cfg, recipe
+        self.sync = EditSync([u.numel for u in units], param_dtype=dtype, device=DEV, **_cfg_kwargs(cfg))
+        self.anchor = [synth.shard_anchor(u, i, 1, 0, DEV, recipe) for i, u in enumerate(units)]
+        self.mom = [synth.shard_momentum(u, i, 1, 0, DEV, recipe) for i, u in enumerate(units)]
+        plant = plant or {}
+        self.local = [synth.shard_local(u, i, 1, 0, 0, self.anchor[i], dtype, DEV, recipe, plant.get(i, 1.0))
+                      for i, u in enumerate(units)]
+        # oracle mirror (CPU, fp32 storage as the GPU)
+        self.o_anchor = [a.cpu().numpy().copy() for a in self.anchor]
+        self.o_mom = [m.cpu().numpy().copy() for m in self.mom]
+        self.o_local = [parity.to_oracle_local(l) for l in self.local]
+        self.o_ema = [[oracle.Ema()] for _ in units]
+
+    def seed_ema(self, mu, sigma, count):
+        self.sync.set_ema(np.asarray(mu)[:, None], np.asarray(sigma)[:, None], count)
+        self.o_ema = [[oracle.Ema(float(mu[i]), float(sigma[i]), int(count))] for i in range(len(self.units))]
+
+    def new_round(self, salt, plant=None):
+        """Both sides draw fresh locals from their OWN anchors (tau more inner steps)."""
+        plant = plant or {}
+        for i, u in enumerate(self.units):
+            p = plant.get(i, 1.0)
+            self.local[i] = synth.shard_local(u, i, 1, 0, 0, self.anchor[i], self.dtype, DEV, self.recipe, p, salt)
+            oa = torch.from_numpy(self.o_anchor[i]).to(DEV)
+            self.o_local[i] = parity.to_oracle_local(
+                synth.shard_local(u, i, 1, 0, 0, oa, self.dtype, DEV, self.recipe, p, salt))
+
+    def run_and_check(self, what=""):
+        for i in range(len(self.units)):
+            self.sync.layer_sync(i, self.local[i], self.anchor[i], self.mom[i])
+        torch.cuda.synchronize()
+        for i in range(len(self.units)):
+            loc, anc, mom, ema, out = oracle.sync_unit(self.cfg, self.o_local[i][None, None], self.o_anchor[i][None],
+                                                       self.o_mom[i][None], self.o_ema[i])
+            self.o_anchor[i], self.o_mom[i], self.o_local[i], self.o_ema[i] = anc[0], mom[0], loc[0, 0], ema
+            tag = f"{what} unit {i} ({self.units[i].numel})"
+            st = self.sync.stats(i)
+            parity.assert_outcome(st, out, ema, tag)
+            parity.assert_f32_close(self.anchor[i].cpu().numpy(), anc[0], tag + " anchor")
+            parity.assert_f32_close(self.mom[i].cpu().numpy(), mom[0], tag + " momentum")
+            parity.assert_local_close(parity.to_oracle_local(self.local[i]), loc[0, 0], tag + " local")
+            # invariant: local == rne(anchor) bitwise on the GPU side (R16)
+            assert torch.equal(self.local[i], self.anchor[i].to(self.dtype)), tag
+        return out
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("numel", [1, 7, 8, 1000, 3 * 65536 + 5, 3_000_017])
+def test_parity_single_unit_two_rounds(dtype, numel):
+    units = [synth.Unit("u", numel, ())]
+    c = Case(units, DTYPES[dtype], cfg=oracle.Config(clip_threshold=0.05))
+    c.run_and_check("round1")
+    c.new_round(1)
+    c.run_and_check("round2")
+    assert c.sync.stats(0).round == 2
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_parity_multi_unit_with_norm_segments_and_empty_unit(dtype):
+    units = [synth.Unit("a", 70_001, ((69_000, 1001),)), synth.Unit("empty", 0, ()),
+             synth.Unit("b", 1_048_576, ((0, 512),)), synth.Unit("c", 13, ())]
+    c = Case(units, DTYPES[dtype])
+    c.run_and_check()
+
+
+@pytest.mark.parametrize("flags", [oracle.NO_AE, oracle.NO_WA, oracle.NO_GC,
+                                   oracle.NO_AE | oracle.NO_WA | oracle.NO_GC])
+def test_parity_ablation_flags(flags):
+    units = [synth.Unit("u", 200_003, ())]
+    c = Case(units, torch.bfloat16, cfg=oracle.Config(flags=flags, clip_threshold=0.1))
+    out = c.run_and_check(f"flags={flags}")
+    if flags & oracle.NO_GC:
+        assert out.beta == 1.0
+
+
+def test_decisions_bit_exact_seeded_ema():
+    # z drawn in U[-2, 2.95] u U[3.05, 10] through the seeded (mu, sigma): N = 1, so a
+    # flagged unit takes the rollback branch, an unflagged one the full update.
+    rng = np.random.default_rng(42)
+    units = [synth.Unit(f"u{i}", int(n), ()) for i, n in enumerate(rng.integers(1000, 300_000, 16))]
+    c = Case(units, torch.bfloat16)
+    G = np.array([oracle.l2_norm(c.o_anchor[i].astype(np.float64) - parity.local_as_f32(c.o_local[i]))
+                  for i in range(len(units))])
+    z = np.where(rng.random(len(units)) < 0.5, rng.uniform(-2, 2.95, len(units)), rng.uniform(3.05, 10, len(units)))
+    sigma = 0.1 * G
+    c.seed_ema(G - z * sigma, sigma, 10)
+    c.run_and_check("seeded")
+    flagged = [bool(c.sync.stats(i).anomalous[0]) for i in range(len(units))]
+    assert flagged == list(z > 3.0)
+    assert any(flagged) and not all(flagged)
+
+
+def test_rollback_is_exact_and_nan_is_excluded():
+    units = [synth.Unit("u", 100_000, ()), synth.Unit("v", 4097, ())]
+    c = Case(units, torch.bfloat16)
+    c.local[0][12345] = float("nan")       # non-finite params: always excluded (R9)
+    c.o_local[0] = parity.to_oracle_local(c.local[0])
+    anchor0, mom0 = c.anchor[0].clone(), c.mom[0].clone()
+    c.run_and_check("nan")
+    st = c.sync.stats(0)
+    assert st.rollback and st.anomalous[0] and math.isinf(st.G[0])
+    assert torch.equal(c.anchor[0], anchor0) and torch.equal(c.mom[0], mom0)
+    assert torch.equal(c.local[0], anchor0.to(torch.bfloat16))
+    assert not c.sync.stats(1).rollback
+
+
+def test_deterministic_bitwise():
+    units = [synth.Unit("u", 2_000_003, ())]
+    outs = []
+    for _ in range(2):
+        c = Case(units, torch.bfloat16)
+        c.sync.layer_sync(0, c.local[0], c.anchor[0], c.mom[0])
+        torch.cuda.synchronize()
+        outs.append((c.local[0].clone(), c.anchor[0].clone(), c.mom[0].clone(), c.sync.stats(0)))
+    for x, y in zip(outs[0][:3], outs[1][:3]):
+        assert torch.equal(x, y)
+    assert (outs[0][3].G == outs[1][3].G).all() and outs[0][3].beta == outs[1][3].beta
+
+
+def test_argument_errors():
+    s = EditSync([16], device=DEV)
+    t = torch.zeros(16, device=DEV)
+    with pytest.raises(ValueError):
+        s.layer_sync(0, t, t, t)                         # local must be bf16
+    with pytest.raises(ValueError):
+        s.layer_sync(1, t.bfloat16(), t, t.clone())      # layer out of range
+    # misaligned pointer straight through the C ABI -> EDIT_ERR_INVALID_ARG
+    assert s._lib.edit_layer_sync(s._h, 0, t.data_ptr() + 2, t.data_ptr(), t.data_ptr(), None) == 1
+
+
+@pytest.mark.parametrize("unit_index", [0, 1, 33])
+def test_full_size_7b_units_bench_launch_config(unit_index):
+    # BASELINE.json's N = 1 bench workload: 7B-shaped shards, 1 x 1 mesh, bf16 locals,
+    # steady-state momentum, seeded EMA (clip active: G ~ 28 > phi = 10).
+    units = synth.llama_units("7B")
+    u = units[unit_index]
+    c = Case([u], torch.bfloat16, recipe=synth.Recipe())
+    mu, sigma, cnt = synth.ema_seed(u, 0)
+    c.seed_ema([mu], [sigma], cnt)
+    out = c.run_and_check(f"7B {u.name}")
+    assert out.beta < 1.0 and not out.rollback
+
+
+def test_host_buffer_variant_matches_oracle():
+    # edit_layer_sync_host: pinned host shards in, results copied back (CPU offload)
+    units = [synth.Unit("a", 300_001, ()), synth.Unit("b", 65_536, ()), synth.Unit("c", 1_000_003, ())]
+    c = Case(units, torch.bfloat16)
+    h_loc = [l.cpu().pin_memory() for l in c.local]
+    h_anc = [a.cpu().pin_memory() for a in c.anchor]
+    h_mom = [m.cpu().pin_memory() for m in c.mom]
+    for i in range(len(units)):
+        c.sync.layer_sync_host(i, h_loc[i], h_anc[i], h_mom[i])
+    c.sync.host_wait()
+    torch.cuda.synchronize()
+    for i in range(len(units)):
+        loc, anc, mom, ema, out = oracle.sync_unit(c.cfg, c.o_local[i][None, None], c.o_anchor[i][None],
+                                                   c.o_mom[i][None], c.o_ema[i])
+        parity.assert_outcome(c.sync.stats(i), out, ema, f"host unit {i}")
+        parity.assert_f32_close(h_anc[i].numpy(), anc[0], "host anchor")
+        parity.assert_f32_close(h_mom[i].numpy(), mom[0], "host momentum")
+        parity.assert_local_close(parity.to_oracle_local(h_loc[i]), loc[0, 0], "host local")
