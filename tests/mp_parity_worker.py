@@ -1,0 +1,133 @@
+"""Multi-rank parity worker (launched by tests/test_gpu_multirank.py under torchrun).
+
+Every rank syncs its shards of L units through the C ABI (NCCL comms of the M x N mesh).
+Rank 0 regenerates every rank's seeded inputs (synth/, same Philox streams), runs the fp64
+oracle for the whole mesh, gathers all ranks' outputs and compares; all ranks check the
+cross-rank invariants (identical anchors along a sync row, local == rne(anchor) bitwise).
+
+usage: torchrun --nproc-per-node K tests/mp_parity_worker.py MxN dtype config
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from paper_2412_07210_b200 import EditSync, broadcast_unique_id  # noqa: E402
+from tests import parity  # noqa: E402
+
+
+def inputs_of(units, M, m, n, dtype, dev, plant, recipe, salt=0):
+    anc = [synth.shard_anchor(u, i, M, m, dev, recipe) for i, u in enumerate(units)]
+    mom = [synth.shard_momentum(u, i, M, m, dev, recipe) for i, u in enumerate(units)]
+    loc = [synth.shard_local(u, i, M, m, n, anc[i], dtype, dev, recipe, plant.get((i, n), 1.0), salt)
+           for i, u in enumerate(units)]
+    return loc, anc, mom
+
+
+def main():
+    mesh, dtype_s, config = sys.argv[1], sys.argv[2], sys.argv[3]
+    M, N = (int(x) for x in mesh.split("x"))
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    assert world == M * N
+    local_rank = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist.init_process_group("nccl", device_id=dev)
+    m_idx, n_idx = rank % M, rank // M
+    dtype = torch.bfloat16 if dtype_s == "bf16" else torch.float32
+    recipe = synth.Recipe()
+    cfg = oracle.Config()
+    plant = {}
+    seed_ema = True
+    if config == "toy":
+        # BASELINE configs[0]: 4 layers x 64K fp32 params, replica 1 planted (x4) in every unit
+        units = synth.toy_units(4, 65536)
+        plant = {(i, 1): 4.0 for i in range(4)} if N > 1 else {}
+    elif config == "toy_clip":
+        units = synth.toy_units(4, 65536)
+        cfg = oracle.Config(clip_threshold=0.3)
+    elif config == "ragged":
+        units = [synth.Unit("a", 1_000_003, ((999_000, 1003),)), synth.Unit("b", 7, ()),
+                 synth.Unit("c", 3 * 65536 + 5, ())]
+        seed_ema = False
+    elif config == "rollback":
+        units = synth.toy_units(2, 40_000)
+        plant = {(i, n): 4.0 for i in range(2) for n in range(N)}       # every replica anomalous
+    elif config == "llama350m_sample":
+        all_units = synth.llama_units("350M")
+        units = [all_units[0], all_units[1], all_units[33]]
+    else:
+        raise SystemExit(f"unknown config {config}")
+    numel = [synth.shard_numel(u.numel, M) for u in units]
+    uid = broadcast_unique_id()
+    s = EditSync(numel, shard_dim=M, sync_dim=N, rank=rank, device=dev, param_dtype=dtype,
+                 outer_lr=cfg.outer_lr, outer_momentum=cfg.outer_momentum, clip_threshold=cfg.clip_threshold,
+                 clip_eps=cfg.clip_eps, anomaly_threshold=cfg.anomaly_threshold, ema_alpha=cfg.ema_alpha,
+                 ema_warmup_rounds=cfg.ema_warmup_rounds, flags=cfg.flags, unique_id=uid)
+    ema0 = [[oracle.Ema() for _ in range(N)] for _ in units]
+    if seed_ema:
+        mu = np.array([[synth.ema_seed(u, n, recipe)[0] for n in range(N)] for u in units])
+        s.set_ema(mu, 0.1 * mu, recipe.ema_warmup_rounds)
+        ema0 = [[oracle.Ema(mu[i, n], 0.1 * mu[i, n], recipe.ema_warmup_rounds) for n in range(N)]
+                for i in range(len(units))]
+
+    loc, anc, mom = inputs_of(units, M, m_idx, n_idx, dtype, dev, plant, recipe)
+    for i in range(len(units)):
+        s.layer_sync(i, loc[i], anc[i], mom[i])
+    torch.cuda.synchronize()
+    mine = {"rank": rank, "loc": [parity.to_oracle_local(x) for x in loc],
+            "anc": [x.cpu().numpy() for x in anc], "mom": [x.cpu().numpy() for x in mom],
+            "stats": [s.stats(i) for i in range(len(units))]}
+    # invariant: local == rne(anchor) bitwise on every rank (R16)
+    for i in range(len(units)):
+        assert torch.equal(loc[i], anc[i].to(dtype)), f"rank {rank} unit {i}: local != rne(anchor)"
+    gathered = [None] * world if rank == 0 else None
+    dist.gather_object(mine, gathered, dst=0)
+    ok = True
+    if rank == 0:
+        by_rank = {g["rank"]: g for g in gathered}
+        for i, u in enumerate(units):
+            # regenerate every rank's inputs for unit i (seeded, rank-independent)
+            locs, ancs, moms = [], [], []
+            for m in range(M):
+                a = synth.shard_anchor(u, i, M, m, dev, recipe)
+                ancs.append(a.cpu().numpy())
+                moms.append(synth.shard_momentum(u, i, M, m, dev, recipe).cpu().numpy())
+                locs.append([parity.to_oracle_local(synth.shard_local(u, i, M, m, n, a, dtype, dev, recipe,
+                                                                      plant.get((i, n), 1.0)))
+                             for n in range(N)])
+            o_loc, o_anc, o_mom, o_ema, out = oracle.sync_unit(cfg, np.array(locs), np.stack(ancs), np.stack(moms),
+                                                               ema0[i])
+            for r in range(world):
+                m, n = r % M, r // M
+                g = by_rank[r]
+                tag = f"{config} {mesh} unit {i} rank {r} (m={m}, n={n})"
+                parity.assert_outcome(g["stats"][i], out, o_ema, tag)
+                parity.assert_f32_close(g["anc"][i], o_anc[m], tag + " anchor")
+                parity.assert_f32_close(g["mom"][i], o_mom[m], tag + " momentum")
+                parity.assert_local_close(g["loc"][i], o_loc[m, n], tag + " local")
+                # sync-row identity: bitwise identical anchors across the N replicas of shard m
+                g0 = by_rank[m]
+                assert np.array_equal(g["anc"][i], g0["anc"][i]), tag + " anchors differ across the sync row"
+            if config == "toy" and N > 1:
+                assert out.anomalous[1] and not out.rollback
+            if config == "rollback":
+                assert out.rollback
+            if config == "toy_clip":
+                assert out.beta < 1.0
+        print(f"PARITY OK {config} {mesh} {dtype_s}: {len(units)} units", flush=True)
+    s.close()
+    dist.barrier(device_ids=[local_rank])
+    dist.destroy_process_group()
+    return 0 if ok else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -53,14 +53,17 @@ class Case:
         self.o_ema = [[oracle.Ema(float(mu[i]), float(sigma[i]), int(count))] for i in range(len(self.units))]
 
     def new_round(self, salt, plant=None):
-        """Both sides draw fresh locals from their OWN anchors (tau more inner steps)."""
+        """Next round from the ORACLE's state (oracle -> GPU only): both sides get identical
+        anchor/momentum and the same fresh locals cast(anchor - D).  (Drawing each side's
+        locals from its own anchor would let a 1-ulp fp32 anchor difference flip the bf16
+        rounding of the input and test the input, not the sync.)  The GPU keeps its own EMA."""
         plant = plant or {}
         for i, u in enumerate(self.units):
             p = plant.get(i, 1.0)
+            self.anchor[i].copy_(torch.from_numpy(self.o_anchor[i]))
+            self.mom[i].copy_(torch.from_numpy(self.o_mom[i]))
             self.local[i] = synth.shard_local(u, i, 1, 0, 0, self.anchor[i], self.dtype, DEV, self.recipe, p, salt)
-            oa = torch.from_numpy(self.o_anchor[i]).to(DEV)
-            self.o_local[i] = parity.to_oracle_local(
-                synth.shard_local(u, i, 1, 0, 0, oa, self.dtype, DEV, self.recipe, p, salt))
+            self.o_local[i] = parity.to_oracle_local(self.local[i])
 
     def run_and_check(self, what=""):
         for i in range(len(self.units)):
