@@ -38,7 +38,8 @@ edit_status_t fail(edit_status_t st, const std::string& msg) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t s_off, s_bytes, scratch_off, ema_off, rec_off, total;
+  size_t s_off, s_bytes, scratch_off, ema_off, rec_off, parts_off, total;
+  std::vector<size_t> part1, part2;  // per unit: offsets (bytes, from parts_off) of the per-CTA partials
 };
 
 Layout layout_of(const edit_sync_config_t& c) {
@@ -55,6 +56,18 @@ Layout layout_of(const edit_sync_config_t& c) {
   off += align_up(sizeof(edit_ema_t) * (size_t)c.num_layers * c.sync_dim, 256);
   L.rec_off = off;
   off += align_up(sizeof(edit_layer_stats_t) * (size_t)c.num_layers, 256);
+  // per-CTA fp64 partials of K1 and K3, one region per unit (so units on different
+  // streams never share slots): grid_of(numel, kVecReduce) each
+  L.parts_off = off;
+  size_t p = 0;
+  for (int i = 0; i < c.num_layers; ++i) {
+    const size_t g = (size_t)grid_of(c.layer_numel[i], kVecReduce);
+    L.part1.push_back(p);
+    p += align_up(g * sizeof(double), 256);
+    L.part2.push_back(p);
+    if (c.sync_dim > 1) p += align_up(g * sizeof(double), 256);
+  }
+  off += p;
   L.total = off;
   return L;
 }
@@ -93,7 +106,7 @@ struct edit_sync {
   std::vector<int64_t> numel;
   int M = 1, N = 1, K = 1, sync_idx = 0, shard_idx = 0;
   int num_sms = 0;
-  Occupancy occ{};
+  std::vector<double*> part1, part2;  // per-unit per-CTA partial slots (workspace)
   ncclComm_t global = nullptr, sync = nullptr, shard = nullptr;
   std::vector<ncclRedOp_t> ops;  // per unit: PreMulSum with that unit's device weight
   char* ws = nullptr;
@@ -137,11 +150,6 @@ namespace {
     }                                                                                       \
   } while (0)
 
-int grid_for(int64_t n, int blocks_per_sm, int num_sms) {
-  const int64_t want = (n / 8 + kThreads - 1) / kThreads;
-  const int64_t cap = std::min<int64_t>((int64_t)std::max(blocks_per_sm, 1) * num_sms, kMaxCtas);
-  return (int)std::max<int64_t>(1, std::min(want, cap));
-}
 
 }  // namespace
 
@@ -212,13 +220,16 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
 
   INIT_CUDA(cudaSetDevice(cfg->device));
   INIT_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
-  INIT_CUDA(query_occupancy(&h->occ));
 
   h->ws = static_cast<char*>(workspace);
   h->S = L.s_bytes ? reinterpret_cast<float*>(h->ws + L.s_off) : nullptr;
   h->scratch = reinterpret_cast<LayerScratch*>(h->ws + L.scratch_off);
   h->ema = reinterpret_cast<edit_ema_t*>(h->ws + L.ema_off);
   h->rec = reinterpret_cast<edit_layer_stats_t*>(h->ws + L.rec_off);
+  for (int i = 0; i < cfg->num_layers; ++i) {
+    h->part1.push_back(reinterpret_cast<double*>(h->ws + L.parts_off + L.part1[i]));
+    h->part2.push_back(reinterpret_cast<double*>(h->ws + L.parts_off + L.part2[i]));
+  }
   // zero scratch (ticket counters), EMA (mu = sigma = 0, count = 0: R8) and records
   INIT_CUDA(cudaMemset(h->ws + L.scratch_off, 0, L.total - L.scratch_off));
   INIT_CUDA(cudaDeviceSynchronize());
@@ -266,8 +277,7 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
   if (ev) CUDA_TRY(h, cudaEventRecord(ev[0], st));
   // K1: Delta and its shard norm (Alg. 2 l.442-443)
   float* S = N > 1 ? h->S : nullptr;
-  launched += launch_pg_norm(dt, local, anchor, S, n, scr,
-                             grid_for(n, h->occ.pg_norm[dt][S ? 1 : 0], h->num_sms), st);
+  launched += launch_pg_norm(dt, local, anchor, S, n, scr, h->part1[layer], st);
   CUDA_TRY(h, cudaGetLastError());
   if (ev) CUDA_TRY(h, cudaEventRecord(ev[1], st));
   // module norms of every replica on every rank: one K-scalar gather (R6)
@@ -310,7 +320,7 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
     // Eq. 3: Dbar = sum_n w_n Delta_n, the weight applied inside NCCL (PreMulSum)
     NCCL_TRY(h, ncclAllReduce(S, S, (size_t)n, ncclFloat32, h->ops[layer], h->sync, st));
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
-    launched += launch_sumsq(S, n, scr, grid_for(n, h->occ.sumsq, h->num_sms), st);
+    launched += launch_sumsq(S, n, scr, h->part2[layer], st);
     CUDA_TRY(h, cudaGetLastError());
     if (M > 1) {
       NCCL_TRY(h, ncclAllGather(&scr->send2, scr->recv2, 1, ncclFloat64, h->shard, st));
@@ -329,7 +339,7 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
     u.gparts = &scr->gsq;
     u.n_gparts = 1;
   }
-  launched += launch_update(dt, u, grid_for(n, h->occ.update[dt][N > 1 ? 1 : 0], h->num_sms), st);
+  launched += launch_update(dt, u, st);
   CUDA_TRY(h, cudaGetLastError());
   if (ev) {
     CUDA_TRY(h, cudaEventRecord(ev[5], st));

@@ -8,8 +8,21 @@
 namespace edit {
 
 constexpr int kThreads = 256;   // threads per CTA of the streaming kernels
-constexpr int kMaxCtas = 2048;  // upper bound of a streaming grid (per-CTA partial slots)
+// 8-element vectors per thread.  Grids are NOT persistent: one CTA per kThreads*U vectors
+// (measured on B200: a full grid streams at 6.9-7.4 TB/s where a grid-stride persistent
+// grid of occupancy x 148 CTAs stalls at 5.3-5.5 TB/s; profiles/r1_k4_variants_microbench.txt).
+// {U, I}: a thread handles I steps of U vectors (loads of the U vectors issued together).
+constexpr int kReduceShape[2] = {2, 2};  // K1, K3 (read-only streams)
+constexpr int kUpdateShape[2] = {1, 1};  // K4 (3 read + 3 write streams)
+constexpr int kVecReduce = kReduceShape[0] * kReduceShape[1];
+constexpr int kVecUpdate = kUpdateShape[0] * kUpdateShape[1];
 constexpr int kMaxRanks = EDIT_MAX_SYNC * EDIT_MAX_SHARD;
+
+inline int64_t grid_of(int64_t n, int vec_per_thread) {
+  const int64_t per_cta = (int64_t)kThreads * vec_per_thread * 8;
+  const int64_t g = (n + per_cta - 1) / per_cta;
+  return g < 1 ? 1 : g;
+}
 
 // Per-unit device scratch: partial sums, gathered scalars, the PreMulSum weight and
 // the rollback decision of the unit's last sync.  One per unit so that the scalar
@@ -25,8 +38,6 @@ struct alignas(256) LayerScratch {
   int32_t rollback;           // Alg. 2 l.448
   uint32_t counter1;          // last-CTA tickets
   uint32_t counter2;
-  double cta1[kMaxCtas];      // per-CTA partials of K1
-  double cta2[kMaxCtas];      // per-CTA partials of K3
 };
 
 struct DecideArgs {
@@ -58,18 +69,11 @@ struct UpdateArgs {
 };
 
 // Launchers (kernels.cu).  Each returns the number of kernels launched.
+// cta_parts: grid_of(n, kVecReduce) fp64 slots for the per-CTA partials.
 int launch_pg_norm(int dtype, const void* local, const float* anchor, float* S, int64_t n,
-                   LayerScratch* scr, int grid, cudaStream_t st);
-int launch_sumsq(const float* x, int64_t n, LayerScratch* scr, int grid, cudaStream_t st);
+                   LayerScratch* scr, double* cta_parts, cudaStream_t st);
+int launch_sumsq(const float* x, int64_t n, LayerScratch* scr, double* cta_parts, cudaStream_t st);
 int launch_decide(const DecideArgs& a, cudaStream_t st);
-int launch_update(int dtype, const UpdateArgs& a, int grid, cudaStream_t st);
-
-// Max co-resident CTAs of each streaming kernel (for grid sizing).
-struct Occupancy {
-  int pg_norm[2][2];  // [dtype][write_S]
-  int sumsq;
-  int update[2][2];   // [dtype][from_S]
-};
-cudaError_t query_occupancy(Occupancy* occ);
+int launch_update(int dtype, const UpdateArgs& a, cudaStream_t st);
 
 }  // namespace edit

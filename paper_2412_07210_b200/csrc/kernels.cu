@@ -11,8 +11,8 @@
 //                    rollback branch local = rne(a) (l.449).  N == 1 recomputes
 //                    Dbar = Delta = a - local from the inputs (2-pass sync).
 // Every reduction is deterministic: a fixed grid for a given length, fixed per-thread
-// element sets, warp-shuffle/CTA trees, and the last CTA adding the per-CTA partials in
-// index order in fp64.
+// element sets (fp32 sum of a thread's 8*U squares), warp-shuffle/CTA trees in fp64, and
+// the last CTA adding the per-CTA partials in index order in fp64.
 #include <cuda_bf16.h>
 #include <math.h>
 
@@ -22,15 +22,16 @@ namespace edit {
 namespace {
 
 // ---------------------------------------------------------------- vector IO
-// 8 elements per thread-iteration: one 16-byte load of bf16 or two of fp32.
+// 8 elements per vector: one 16-byte access of bf16 or two of fp32.  Plain ld/st: the
+// streaming cache hints (.cs / L1::no_allocate / .lu) measured 2-10% slower on K4.
 __device__ __forceinline__ void load8(const float* __restrict__ p, float (&v)[8]) {
-  const float4 a = __ldcs(reinterpret_cast<const float4*>(p));
-  const float4 b = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  const float4 b = *(reinterpret_cast<const float4*>(p) + 1);
   v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
   v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
 }
 __device__ __forceinline__ void load8(const __nv_bfloat16* __restrict__ p, float (&v)[8]) {
-  const uint4 r = __ldcs(reinterpret_cast<const uint4*>(p));
+  const uint4 r = *reinterpret_cast<const uint4*>(p);
   const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -39,8 +40,8 @@ __device__ __forceinline__ void load8(const __nv_bfloat16* __restrict__ p, float
   }
 }
 __device__ __forceinline__ void store8(float* __restrict__ p, const float (&v)[8]) {
-  __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
-  __stcs(reinterpret_cast<float4*>(p) + 1, make_float4(v[4], v[5], v[6], v[7]));
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  *(reinterpret_cast<float4*>(p) + 1) = make_float4(v[4], v[5], v[6], v[7]);
 }
 __device__ __forceinline__ void store8(__nv_bfloat16* __restrict__ p, const float (&v)[8]) {
   uint32_t w[4];
@@ -49,7 +50,7 @@ __device__ __forceinline__ void store8(__nv_bfloat16* __restrict__ p, const floa
     __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);  // RNE (R16)
     w[i] = *reinterpret_cast<uint32_t*>(&h);
   }
-  __stcs(reinterpret_cast<uint4*>(p), make_uint4(w[0], w[1], w[2], w[3]));
+  *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 __device__ __forceinline__ float load1(const float* p) { return *p; }
 __device__ __forceinline__ float load1(const __nv_bfloat16* p) { return __bfloat162float(*p); }
@@ -91,8 +92,18 @@ __device__ void finish_partials(double cta_total, double* cta_parts, uint32_t* c
   __syncthreads();
   if (!is_last) return;
   __threadfence();
+  // thread t adds partials t, t+T, t+2T, ... in that order; 8 loads in flight per step
+  const int G = (int)gridDim.x;
   double v = 0.0;
-  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) v += __ldcg(cta_parts + i);
+  int i = threadIdx.x;
+  for (; i + 7 * kThreads < G; i += 8 * kThreads) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = __ldcg(cta_parts + i + k * kThreads);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v += x[k];
+  }
+  for (; i < G; i += kThreads) v += __ldcg(cta_parts + i);
   v = block_sum(v);
   if (threadIdx.x == 0) {
     *out = v;
@@ -102,62 +113,92 @@ __device__ void finish_partials(double cta_total, double* cta_parts, uint32_t* c
 
 // ---------------------------------------------------------------- K1
 // Alg. 2 l.442-443: Delta = anchor - local; partial ||Delta||^2 of this shard.
-template <typename T, bool kWriteS>
+// Shape: CTA b owns vectors [b*T*U*I, (b+1)*T*U*I); a thread walks I steps of U vectors
+// (stride T), issuing the U vectors' loads before any arithmetic.
+template <typename T, bool kWriteS, int U, int I>
 __global__ void __launch_bounds__(kThreads) pg_norm_kernel(const T* __restrict__ local,
                                                            const float* __restrict__ anchor,
                                                            float* __restrict__ S, int64_t n,
-                                                           LayerScratch* __restrict__ scr) {
+                                                           LayerScratch* __restrict__ scr,
+                                                           double* __restrict__ cta_parts) {
   const int64_t n8 = n >> 3;
-  const int64_t stride = (int64_t)gridDim.x * kThreads;
-  double acc = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n8; i += stride) {
-    float l[8], a[8], d[8];
-    load8(local + 8 * i, l);
-    load8(anchor + 8 * i, a);
-    float s = 0.f;
+  const int64_t cta0 = (int64_t)blockIdx.x * kThreads * U * I + threadIdx.x;
+  float acc = 0.f;
+#pragma unroll 1
+  for (int it = 0; it < I; ++it) {
+    const int64_t base = cta0 + (int64_t)it * kThreads * U;
+    float l[U][8], a[U][8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      d[j] = a[j] - l[j];
-      s = fmaf(d[j], d[j], s);
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (int64_t)u * kThreads;
+      if (i < n8) {
+        load8(local + 8 * i, l[u]);
+        load8(anchor + 8 * i, a[u]);
+      }
     }
-    acc += (double)s;
-    if (kWriteS) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) d[j] = isfinite(d[j]) ? d[j] : 0.f;  // R9: w = 0 must give 0
-      store8(S + 8 * i, d);
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (int64_t)u * kThreads;
+      if (i < n8) {
+        float d[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          d[j] = a[u][j] - l[u][j];
+          acc = fmaf(d[j], d[j], acc);
+        }
+        if (kWriteS) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) d[j] = isfinite(d[j]) ? d[j] : 0.f;  // R9: w = 0 must give 0
+          store8(S + 8 * i, d);
+        }
+      }
     }
   }
+  double accd = (double)acc;
   if (blockIdx.x == 0 && threadIdx.x < (n & 7)) {  // ragged tail (< 8 elements)
     const int64_t k = 8 * n8 + threadIdx.x;
     const float d = anchor[k] - load1(local + k);
-    acc += (double)(d * d);
+    accd += (double)(d * d);
     if (kWriteS) S[k] = isfinite(d) ? d : 0.f;
   }
-  acc = block_sum(acc);
-  finish_partials(acc, scr->cta1, &scr->counter1, &scr->send1);
+  accd = block_sum(accd);
+  finish_partials(accd, cta_parts, &scr->counter1, &scr->send1);
 }
 
 // ---------------------------------------------------------------- K3
 // Eq. 4: partial ||Dbar||^2 of this shard of the all-reduced pseudo-gradient.
+template <int U, int I>
 __global__ void __launch_bounds__(kThreads) sumsq_kernel(const float* __restrict__ x, int64_t n,
-                                                         LayerScratch* __restrict__ scr) {
+                                                         LayerScratch* __restrict__ scr,
+                                                         double* __restrict__ cta_parts) {
   const int64_t n8 = n >> 3;
-  const int64_t stride = (int64_t)gridDim.x * kThreads;
-  double acc = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n8; i += stride) {
-    float v[8];
-    load8(x + 8 * i, v);
-    float s = 0.f;
+  const int64_t cta0 = (int64_t)blockIdx.x * kThreads * U * I + threadIdx.x;
+  float acc = 0.f;
+#pragma unroll 1
+  for (int it = 0; it < I; ++it) {
+    const int64_t base = cta0 + (int64_t)it * kThreads * U;
+    float v[U][8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) s = fmaf(v[j], v[j], s);
-    acc += (double)s;
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (int64_t)u * kThreads;
+      if (i < n8) load8(x + 8 * i, v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (int64_t)u * kThreads;
+      if (i < n8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc = fmaf(v[u][j], v[u][j], acc);
+      }
+    }
   }
+  double accd = (double)acc;
   if (blockIdx.x == 0 && threadIdx.x < (n & 7)) {
-    const float v = x[8 * n8 + threadIdx.x];
-    acc += (double)(v * v);
+    const float t = x[8 * n8 + threadIdx.x];
+    accd += (double)(t * t);
   }
-  acc = block_sum(acc);
-  finish_partials(acc, scr->cta2, &scr->counter2, &scr->send2);
+  accd = block_sum(accd);
+  finish_partials(accd, cta_parts, &scr->counter2, &scr->send2);
 }
 
 // ---------------------------------------------------------------- K2
@@ -232,98 +273,126 @@ __global__ void decide_kernel(DecideArgs p) {
 // ---------------------------------------------------------------- K4
 // beta (Eq. 4), then OuterOpt = Nesterov (R2) on (anchor, momentum) and the
 // write-back local = rne(anchor) (Alg. 2 l.454-455).  Rollback: local = rne(anchor).
-template <typename T, bool kFromS>
+template <typename T, bool kFromS, int U, int I>
 __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
   T* __restrict__ local = static_cast<T*>(p.local);
   float* __restrict__ anchor = p.anchor;
   float* __restrict__ mom = p.momentum;
   const float* __restrict__ dbar = p.dbar;
-  double gsq = 0.0;
-  for (int i = 0; i < p.n_gparts; ++i) gsq += p.gparts[i];  // module level, m order
-  const double gbar = sqrt(gsq);
-  double beta_d = p.phi / (gbar + p.eps);
-  beta_d = beta_d < 1.0 ? beta_d : 1.0;
-  if (p.flags & EDIT_NO_GC) beta_d = 1.0;
-  const int rollback = *p.rollback;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    p.rec->G_bar = rollback ? 0.0 : gbar;
-    p.rec->beta = rollback ? 1.0 : beta_d;
-    p.rec->rollback = rollback;
-    p.rec->round += 1;
-  }
-  const float beta = (float)beta_d, mu = p.mu, nu = p.nu;
-  const int64_t n8 = p.n >> 3;
-  const int64_t stride = (int64_t)gridDim.x * kThreads;
-  const int64_t first = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  const int tail = (blockIdx.x == 0 && threadIdx.x < (p.n & 7)) ? 1 : 0;
-  if (rollback) {  // Alg. 2 l.449: theta_{t+1,0} = theta_t (R14)
-    for (int64_t i = first; i < n8; i += stride) {
-      float a[8];
-      load8(anchor + 8 * i, a);
-      store8(local + 8 * i, a);
+  __shared__ float s_beta;
+  __shared__ int s_rollback;
+  if (threadIdx.x == 0) {  // Eq. 4 once per CTA (fp64), broadcast through shared memory
+    double gsq = 0.0;
+    for (int i = 0; i < p.n_gparts; ++i) gsq += p.gparts[i];  // module level, m order
+    const double gbar = sqrt(gsq);
+    double beta_d = p.phi / (gbar + p.eps);
+    beta_d = beta_d < 1.0 ? beta_d : 1.0;
+    if (p.flags & EDIT_NO_GC) beta_d = 1.0;
+    const int rb = *p.rollback;
+    if (blockIdx.x == 0) {
+      p.rec->G_bar = rb ? 0.0 : gbar;
+      p.rec->beta = rb ? 1.0 : beta_d;
+      p.rec->rollback = rb;
+      p.rec->round += 1;
     }
+    s_beta = (float)beta_d;
+    s_rollback = rb;
+  }
+  __syncthreads();
+  const float beta = s_beta, mu = p.mu, nu = p.nu;
+  const int64_t n8 = p.n >> 3;
+  const int64_t cta0 = (int64_t)blockIdx.x * kThreads * U * I + threadIdx.x;
+  const bool tail = blockIdx.x == 0 && threadIdx.x < (p.n & 7);
+  if (s_rollback) {  // Alg. 2 l.449: theta_{t+1,0} = theta_t (R14)
+#pragma unroll 1
+    for (int it = 0; it < I; ++it)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = cta0 + (int64_t)(it * U + u) * kThreads;
+        if (i < n8) {
+          float a[8];
+          load8(anchor + 8 * i, a);
+          store8(local + 8 * i, a);
+        }
+      }
     if (tail) {
       const int64_t k = 8 * n8 + threadIdx.x;
       store1(local + k, anchor[k]);
     }
     return;
   }
-  for (int64_t i = first; i < n8; i += stride) {
-    float a[8], m[8], d[8];
-    if (kFromS) {
-      load8(dbar + 8 * i, d);
-    } else {
-      float l[8];
-      load8(local + 8 * i, l);
-      load8(anchor + 8 * i, a);
+#pragma unroll 1
+  for (int it = 0; it < I; ++it) {
+    const int64_t base = cta0 + (int64_t)it * kThreads * U;
+    float a[U][8], m[U][8], d[U][8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) d[j] = a[j] - l[j];  // N == 1: Dbar = Delta
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (int64_t)u * kThreads;
+      if (i < n8) {
+        if (kFromS) {
+          load8(dbar + 8 * i, d[u]);
+        } else {
+          load8(local + 8 * i, d[u]);  // the local; Delta formed below
+        }
+        load8(anchor + 8 * i, a[u]);
+        load8(mom + 8 * i, m[u]);
+      }
     }
-    if (kFromS) load8(anchor + 8 * i, a);
-    load8(mom + 8 * i, m);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float g = beta * d[j];          // Eq. 5
-      m[j] = fmaf(mu, m[j], g);             // m' = mu m + g
-      a[j] = a[j] - nu * fmaf(mu, m[j], g); // a' = a - nu (g + mu m')
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (int64_t)u * kThreads;
+      if (i < n8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float dj = kFromS ? d[u][j] : a[u][j] - d[u][j];  // N == 1: Dbar = Delta
+          const float g = beta * dj;                    // Eq. 5
+          m[u][j] = fmaf(mu, m[u][j], g);               // m' = mu m + g
+          a[u][j] = a[u][j] - nu * fmaf(mu, m[u][j], g);  // a' = a - nu (g + mu m')
+        }
+        store8(mom + 8 * i, m[u]);
+        store8(anchor + 8 * i, a[u]);
+        store8(local + 8 * i, a[u]);
+      }
     }
-    store8(mom + 8 * i, m);
-    store8(anchor + 8 * i, a);
-    store8(local + 8 * i, a);
   }
   if (tail) {
     const int64_t k = 8 * n8 + threadIdx.x;
     const float d = kFromS ? dbar[k] : anchor[k] - load1(local + k);
     const float g = beta * d;
-    const float m = fmaf(mu, mom[k], g);
-    const float a = anchor[k] - nu * fmaf(mu, m, g);
-    mom[k] = m;
-    anchor[k] = a;
-    store1(local + k, a);
+    const float m1 = fmaf(mu, mom[k], g);
+    const float a1 = anchor[k] - nu * fmaf(mu, m1, g);
+    mom[k] = m1;
+    anchor[k] = a1;
+    store1(local + k, a1);
   }
 }
 
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
+// Production shapes (profiles/r1_k4_variants_microbench.txt, tools/kbench.cu).
+constexpr int kRedU = kReduceShape[0], kRedI = kReduceShape[1];
+constexpr int kUpdU = kUpdateShape[0], kUpdI = kUpdateShape[1];
+
 int launch_pg_norm(int dtype, const void* local, const float* anchor, float* S, int64_t n,
-                   LayerScratch* scr, int grid, cudaStream_t st) {
+                   LayerScratch* scr, double* cta_parts, cudaStream_t st) {
+  const unsigned grid = (unsigned)grid_of(n, kRedU * kRedI);
   if (dtype == EDIT_BF16) {
-    if (S) pg_norm_kernel<__nv_bfloat16, true><<<grid, kThreads, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(local), anchor, S, n, scr);
-    else pg_norm_kernel<__nv_bfloat16, false><<<grid, kThreads, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(local), anchor, S, n, scr);
+    if (S) pg_norm_kernel<__nv_bfloat16, true, kRedU, kRedI><<<grid, kThreads, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(local), anchor, S, n, scr, cta_parts);
+    else pg_norm_kernel<__nv_bfloat16, false, kRedU, kRedI><<<grid, kThreads, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(local), anchor, S, n, scr, cta_parts);
   } else {
-    if (S) pg_norm_kernel<float, true><<<grid, kThreads, 0, st>>>(
-        static_cast<const float*>(local), anchor, S, n, scr);
-    else pg_norm_kernel<float, false><<<grid, kThreads, 0, st>>>(
-        static_cast<const float*>(local), anchor, S, n, scr);
+    if (S) pg_norm_kernel<float, true, kRedU, kRedI><<<grid, kThreads, 0, st>>>(
+        static_cast<const float*>(local), anchor, S, n, scr, cta_parts);
+    else pg_norm_kernel<float, false, kRedU, kRedI><<<grid, kThreads, 0, st>>>(
+        static_cast<const float*>(local), anchor, S, n, scr, cta_parts);
   }
   return 1;
 }
 
-int launch_sumsq(const float* x, int64_t n, LayerScratch* scr, int grid, cudaStream_t st) {
-  sumsq_kernel<<<grid, kThreads, 0, st>>>(x, n, scr);
+int launch_sumsq(const float* x, int64_t n, LayerScratch* scr, double* cta_parts, cudaStream_t st) {
+  sumsq_kernel<kRedU, kRedI><<<(unsigned)grid_of(n, kRedU * kRedI), kThreads, 0, st>>>(x, n, scr, cta_parts);
   return 1;
 }
 
@@ -332,32 +401,16 @@ int launch_decide(const DecideArgs& a, cudaStream_t st) {
   return 1;
 }
 
-int launch_update(int dtype, const UpdateArgs& a, int grid, cudaStream_t st) {
+int launch_update(int dtype, const UpdateArgs& a, cudaStream_t st) {
+  const unsigned grid = (unsigned)grid_of(a.n, kUpdU * kUpdI);
   if (dtype == EDIT_BF16) {
-    if (a.dbar) outer_update_kernel<__nv_bfloat16, true><<<grid, kThreads, 0, st>>>(a);
-    else outer_update_kernel<__nv_bfloat16, false><<<grid, kThreads, 0, st>>>(a);
+    if (a.dbar) outer_update_kernel<__nv_bfloat16, true, kUpdU, kUpdI><<<grid, kThreads, 0, st>>>(a);
+    else outer_update_kernel<__nv_bfloat16, false, kUpdU, kUpdI><<<grid, kThreads, 0, st>>>(a);
   } else {
-    if (a.dbar) outer_update_kernel<float, true><<<grid, kThreads, 0, st>>>(a);
-    else outer_update_kernel<float, false><<<grid, kThreads, 0, st>>>(a);
+    if (a.dbar) outer_update_kernel<float, true, kUpdU, kUpdI><<<grid, kThreads, 0, st>>>(a);
+    else outer_update_kernel<float, false, kUpdU, kUpdI><<<grid, kThreads, 0, st>>>(a);
   }
   return 1;
-}
-
-cudaError_t query_occupancy(Occupancy* occ) {
-  cudaError_t e = cudaSuccess;
-#define OCC(dst, fn) \
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&(dst), fn, kThreads, 0)
-  OCC(occ->pg_norm[EDIT_BF16][0], (pg_norm_kernel<__nv_bfloat16, false>));
-  OCC(occ->pg_norm[EDIT_BF16][1], (pg_norm_kernel<__nv_bfloat16, true>));
-  OCC(occ->pg_norm[EDIT_F32][0], (pg_norm_kernel<float, false>));
-  OCC(occ->pg_norm[EDIT_F32][1], (pg_norm_kernel<float, true>));
-  OCC(occ->sumsq, sumsq_kernel);
-  OCC(occ->update[EDIT_BF16][0], (outer_update_kernel<__nv_bfloat16, false>));
-  OCC(occ->update[EDIT_BF16][1], (outer_update_kernel<__nv_bfloat16, true>));
-  OCC(occ->update[EDIT_F32][0], (outer_update_kernel<float, false>));
-  OCC(occ->update[EDIT_F32][1], (outer_update_kernel<float, true>));
-#undef OCC
-  return e;
 }
 
 }  // namespace edit
