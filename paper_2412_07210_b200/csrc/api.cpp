@@ -333,8 +333,6 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
     u.dbar = S;
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[4], st));
   } else {
-    if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
-    if (ev) CUDA_TRY(h, cudaEventRecord(ev[4], st));
     u.dbar = nullptr;  // Dbar = Delta, G_bar = G (module level)
     u.gparts = &scr->gsq;
     u.n_gparts = 1;
@@ -477,10 +475,14 @@ edit_status_t edit_sync_profile_collect(edit_sync_t h, double phase_ms[EDIT_NUM_
   for (int32_t layer : h->pending) {
     cudaEvent_t* ev = &h->prof[(size_t)layer * (EDIT_NUM_PHASES + 1)];
     CUDA_TRY(h, cudaEventSynchronize(ev[EDIT_NUM_PHASES]));
-    for (int p = 0; p < EDIT_NUM_PHASES; ++p) {
+    // N == 1 records no events for the empty phases 2 and 3 (no all-reduce, no K3)
+    const int seq[6] = {0, 1, 2, 3, 4, 5}, seq1[4] = {0, 1, 2, 5};
+    const int* q = h->N > 1 ? seq : seq1;
+    const int nq = h->N > 1 ? 6 : 4;
+    for (int k = 0; k + 1 < nq; ++k) {
       float ms = 0.f;
-      CUDA_TRY(h, cudaEventElapsedTime(&ms, ev[p], ev[p + 1]));
-      phase_ms[p] += ms;
+      CUDA_TRY(h, cudaEventElapsedTime(&ms, ev[q[k]], ev[q[k + 1]]));
+      phase_ms[q[k + 1] == 5 ? 4 : q[k]] += ms;
     }
     elems += h->numel[layer];
   }

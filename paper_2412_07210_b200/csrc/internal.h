@@ -12,7 +12,7 @@ constexpr int kThreads = 256;   // threads per CTA of the streaming kernels
 // (measured on B200: a full grid streams at 6.9-7.4 TB/s where a grid-stride persistent
 // grid of occupancy x 148 CTAs stalls at 5.3-5.5 TB/s; profiles/r1_k4_variants_microbench.txt).
 // {U, I}: a thread handles I steps of U vectors (loads of the U vectors issued together).
-constexpr int kReduceShape[2] = {2, 2};  // K1, K3 (read-only streams)
+constexpr int kReduceShape[2] = {2, 4};  // K1, K3 (read-only streams): 6.8 TB/s incl. the fp64 combine
 constexpr int kUpdateShape[2] = {1, 1};  // K4 (3 read + 3 write streams)
 constexpr int kVecReduce = kReduceShape[0] * kReduceShape[1];
 constexpr int kVecUpdate = kUpdateShape[0] * kUpdateShape[1];

@@ -301,8 +301,11 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
   __syncthreads();
   const float beta = s_beta, mu = p.mu, nu = p.nu;
   const int64_t n8 = p.n >> 3;
-  const int64_t cta0 = (int64_t)blockIdx.x * kThreads * U * I + threadIdx.x;
-  const bool tail = blockIdx.x == 0 && threadIdx.x < (p.n & 7);
+  // CTAs walk the unit from its END: the producer pass right before (K1 at N == 1, K3 at
+  // N > 1) streamed it forward, so its last ~100 MB are still in the 126 MB L2.
+  const int64_t chunk = (int64_t)gridDim.x - 1 - blockIdx.x;
+  const int64_t cta0 = chunk * kThreads * U * I + threadIdx.x;
+  const bool tail = chunk == (int64_t)gridDim.x - 1 && threadIdx.x < (p.n & 7);
   if (s_rollback) {  // Alg. 2 l.449: theta_{t+1,0} = theta_t (R14)
 #pragma unroll 1
     for (int it = 0; it < I; ++it)
