@@ -194,6 +194,9 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=4_000_000)
+    ap.add_argument("--overlap-tokens", type=int, default=8192,
+                    help="tokens/GPU of the synthetic forward for the prefetch-overlap measurement (0 = skip)")
+    ap.add_argument("--overlap-steps", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: W >= 3
@@ -311,6 +314,56 @@ def main() -> None:
         if key in tinfo:
             traffic = tinfo[key]["dram_bytes_per_elem"] * k4_elems / k4_launches
 
+    # a8: layer-wise prefetch -- hidden fraction h = 1 - (t_fwd+sync - t_fwd) / t_sync
+    overlap = None
+    if args.overlap_tokens > 0:
+        from synth.forward import SyntheticForward
+        fwd = SyntheticForward(args.model, units, args.overlap_tokens, dev)
+
+        def timed(fn, nsteps, redraw_first=True):
+            ts = []
+            for s in range(nsteps + 1):          # first one untimed (warm-up)
+                if redraw_first:
+                    redraw(1000 + s)
+                barrier()
+                torch.cuda.synchronize()
+                ev0.record(stream)
+                fn()
+                ev1.record(stream)
+                torch.cuda.synchronize()
+                t = ev0.elapsed_time(ev1)
+                if world > 1:
+                    tt = torch.tensor([t], device=dev, dtype=torch.float64)
+                    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                    t = float(tt.item())
+                if s > 0:
+                    ts.append(t)
+            return sum(ts) / len(ts)
+
+        def forward_only():
+            for u in range(len(units)):
+                fwd.unit(u, locs[u])
+
+        def fwd_and_sync(depth):
+            def run():
+                sync.begin_round(locs, anchors, moms, depth, stream)
+                for u in range(len(units)):
+                    sync.acquire(u, stream)
+                    fwd.unit(u, locs[u])
+                sync.end_round(stream)
+            return run
+
+        t_fwd = timed(forward_only, args.overlap_steps, redraw_first=False)
+        t_sync_alone = timed(run_round, args.overlap_steps)
+        overlap = {"tokens_per_gpu": args.overlap_tokens, "t_fwd_ms": t_fwd, "t_sync_ms": t_sync_alone,
+                   "fwd_tflops": fwd.flops_per_round() / (t_fwd * 1e-3) / 1e12, "by_depth": {}}
+        for depth in (1, 2):
+            t_both = timed(fwd_and_sync(depth), args.overlap_steps)
+            overlap["by_depth"][str(depth)] = {"t_fwd_plus_sync_ms": t_both,
+                                               "hidden_fraction": 1.0 - (t_both - t_fwd) / t_sync_alone}
+        overlap["note"] = ("synthetic forward (bf16 GEMMs of each unit, weights = the synced local) on the "
+                           "compute stream; syncs on the library's side stream; acquire(u) before forward(u)")
+
     # e2e: same metric through the host-buffer C-ABI call (pinned host buffers; H2D of
     # local/anchor/momentum and D2H of the three results inside the timed region)
     e2e = None
@@ -370,7 +423,7 @@ def main() -> None:
             "phases_ms_per_step": {k: v / args.steps for k, v in phase_ms.items()},
             "per_gpu_GBps": bytes_per_rank_round / (ms_per_step * 1e-3) / 1e9,
             "rollbacks_last_round": rollbacks, "beta_sample": betas,
-            "gpu_launches": launches, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+            "gpu_launches": launches, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "overlap": overlap,
         }
         print(json.dumps(line), flush=True)
     sync.close()

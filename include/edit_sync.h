@@ -146,6 +146,23 @@ edit_status_t edit_layer_sync_host(edit_sync_t h, int32_t layer, void* local_hos
 /* Makes `stream` wait until every outstanding host-variant copy-out has landed. */
 edit_status_t edit_sync_host_wait(edit_sync_t h, void* stream);
 
+/* Layer-wise prefetch scheduler (Alg. 1 l.408-412): "sync parameters for the
+ * upcoming module concurrently with ongoing computations".  The syncs run in unit order on
+ * a library-owned side stream; the caller's forward (on `compute_stream`) acquires each unit
+ * before using its params.
+ *   begin_round: registers the round's L buffers (arrays of L device pointers, copied),
+ *     makes the side stream wait for everything already enqueued on compute_stream (the
+ *     inner steps that produced the locals), and enqueues the syncs of units 0..depth-1.
+ *   acquire(layer): makes compute_stream wait until unit `layer` is synced and enqueues the
+ *     sync of unit layer+depth.  Call for layer = 0, 1, ..., L-1 in order.
+ *   end_round: enqueues any unit not yet synced and makes compute_stream wait for all.
+ * depth >= 1 (the paper prefetches "the upcoming module": depth 1).
+ * EDIT_ERR_INVALID_ARG: null arrays, depth < 1, acquire out of order / outside a round. */
+edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* const* anchors,
+                                     float* const* momenta, int32_t depth, void* compute_stream);
+edit_status_t edit_sched_acquire(edit_sync_t h, int32_t layer, void* compute_stream);
+edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream);
+
 /* Blocks until this unit's last enqueued sync has completed, then copies its
  * outcome record to *out. */
 edit_status_t edit_sync_stats(edit_sync_t h, int32_t layer, edit_layer_stats_t* out);

@@ -126,6 +126,13 @@ struct edit_sync {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t slot_in[2] = {nullptr, nullptr}, slot_done[2] = {nullptr, nullptr},
               slot_free[2] = {nullptr, nullptr};
+  // prefetch scheduler state
+  cudaStream_t sched_stream = nullptr;
+  cudaEvent_t sched_start = nullptr;
+  std::vector<void*> sched_local;
+  std::vector<float*> sched_anchor, sched_mom;
+  int sched_depth = 0, sched_next_sync = 0, sched_next_acquire = 0;
+  bool sched_active = false;
   bool poisoned = false;
   int64_t launches = 0;
 };
@@ -408,6 +415,80 @@ edit_status_t edit_sync_host_wait(edit_sync_t h, void* stream) {
   return EDIT_OK;
 }
 
+static edit_status_t sched_enqueue_next(edit_sync_t h) {
+  const int u = h->sched_next_sync++;
+  return edit_layer_sync(h, u, h->sched_local[u], h->sched_anchor[u], h->sched_mom[u], h->sched_stream);
+}
+
+edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* const* anchors,
+                                     float* const* momenta, int32_t depth, void* compute_stream) {
+  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
+  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  if (!locals || !anchors || !momenta) return fail(EDIT_ERR_INVALID_ARG, "null buffer arrays");
+  if (depth < 1) return fail(EDIT_ERR_INVALID_ARG, "depth must be >= 1");
+  if (h->sched_active) return fail(EDIT_ERR_INVALID_ARG, "a round is already active");
+  const int L = h->cfg.num_layers;
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  if (!h->sched_stream) {
+    int lo = 0, hi = 0;
+    CUDA_TRY(h, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    // the side stream gets the highest priority: its CTAs are scheduled ahead of the
+    // forward's GEMM tiles, so a unit's sync is never starved by the compute it hides behind
+    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->sched_stream, cudaStreamNonBlocking, hi));
+    CUDA_TRY(h, cudaEventCreateWithFlags(&h->sched_start, cudaEventDisableTiming));
+  }
+  h->sched_local.assign(locals, locals + L);
+  h->sched_anchor.assign(anchors, anchors + L);
+  h->sched_mom.assign(momenta, momenta + L);
+  h->sched_depth = depth;
+  h->sched_next_sync = 0;
+  h->sched_next_acquire = 0;
+  h->sched_active = true;
+  cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
+  CUDA_TRY(h, cudaEventRecord(h->sched_start, cs));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->sched_stream, h->sched_start, 0));
+  while (h->sched_next_sync < std::min(depth, L)) {
+    edit_status_t rc = sched_enqueue_next(h);
+    if (rc != EDIT_OK) return rc;
+  }
+  return EDIT_OK;
+}
+
+edit_status_t edit_sched_acquire(edit_sync_t h, int32_t layer, void* compute_stream) {
+  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
+  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  if (!h->sched_active) return fail(EDIT_ERR_INVALID_ARG, "no active round");
+  if (layer != h->sched_next_acquire) return fail(EDIT_ERR_INVALID_ARG, "acquire units in order 0..L-1");
+  const int L = h->cfg.num_layers;
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  while (h->sched_next_sync <= layer) {  // (depth can only lag if acquire skipped ahead)
+    edit_status_t rc = sched_enqueue_next(h);
+    if (rc != EDIT_OK) return rc;
+  }
+  CUDA_TRY(h, cudaStreamWaitEvent(static_cast<cudaStream_t>(compute_stream), h->done[layer], 0));
+  h->sched_next_acquire = layer + 1;
+  if (h->sched_next_sync < L && h->sched_next_sync <= layer + h->sched_depth) {
+    edit_status_t rc = sched_enqueue_next(h);
+    if (rc != EDIT_OK) return rc;
+  }
+  return EDIT_OK;
+}
+
+edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream) {
+  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
+  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  if (!h->sched_active) return fail(EDIT_ERR_INVALID_ARG, "no active round");
+  const int L = h->cfg.num_layers;
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  while (h->sched_next_sync < L) {
+    edit_status_t rc = sched_enqueue_next(h);
+    if (rc != EDIT_OK) return rc;
+  }
+  CUDA_TRY(h, cudaStreamWaitEvent(static_cast<cudaStream_t>(compute_stream), h->done[L - 1], 0));
+  h->sched_active = false;
+  return EDIT_OK;
+}
+
 edit_status_t edit_sync_stats(edit_sync_t h, int32_t layer, edit_layer_stats_t* out) {
   if (!h || !out) return fail(EDIT_ERR_INVALID_ARG, "null argument");
   if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
@@ -516,6 +597,8 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
   if (h->h2d) cudaStreamDestroy(h->h2d);
   if (h->d2h) cudaStreamDestroy(h->d2h);
   if (h->staging) cudaFree(h->staging);
+  if (h->sched_start) cudaEventDestroy(h->sched_start);
+  if (h->sched_stream) cudaStreamDestroy(h->sched_stream);
   delete h;
   return st;
 }

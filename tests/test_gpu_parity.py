@@ -199,3 +199,45 @@ def test_host_buffer_variant_matches_oracle():
         parity.assert_f32_close(h_anc[i].numpy(), anc[0], "host anchor")
         parity.assert_f32_close(h_mom[i].numpy(), mom[0], "host momentum")
         parity.assert_local_close(parity.to_oracle_local(h_loc[i]), loc[0, 0], "host local")
+
+
+@pytest.mark.parametrize("depth", [1, 2, 5])
+def test_prefetch_scheduler_round_matches_oracle_and_orders_forward(depth):
+    # a8: syncs on the library side stream, the "forward" of unit u (on the caller's
+    # stream) must see unit u's SYNCED params; results identical to direct layer_sync.
+    units = [synth.Unit(f"u{i}", n, ()) for i, n in enumerate([3_000_017, 65_536, 1_000_000, 7, 2_500_000])]
+    c = Case(units, torch.bfloat16)
+    stream = torch.cuda.current_stream(DEV)
+    seen = []
+    c.sync.begin_round(c.local, c.anchor, c.mom, depth, stream)
+    for i in range(len(units)):
+        c.sync.acquire(i, stream)
+        seen.append(c.local[i].float().sum())          # the forward reads unit i
+        torch.cuda._sleep(200_000)                      # ~0.1 ms of "compute" per unit
+    c.sync.end_round(stream)
+    torch.cuda.synchronize()
+    for i in range(len(units)):
+        assert torch.equal(seen[i], c.local[i].float().sum()), f"forward of unit {i} did not see the synced params"
+    # outputs vs oracle
+    for i in range(len(units)):
+        loc, anc, mom, ema, out = oracle.sync_unit(c.cfg, c.o_local[i][None, None], c.o_anchor[i][None],
+                                                   c.o_mom[i][None], c.o_ema[i])
+        parity.assert_outcome(c.sync.stats(i), out, ema, f"sched unit {i}")
+        parity.assert_f32_close(c.anchor[i].cpu().numpy(), anc[0], "sched anchor")
+        parity.assert_f32_close(c.mom[i].cpu().numpy(), mom[0], "sched momentum")
+        parity.assert_local_close(parity.to_oracle_local(c.local[i]), loc[0, 0], "sched local")
+
+
+def test_prefetch_scheduler_argument_errors():
+    from paper_2412_07210_b200 import EditSyncError
+    units = [synth.Unit("a", 1000, ()), synth.Unit("b", 2000, ())]
+    c = Case(units, torch.bfloat16)
+    with pytest.raises(EditSyncError):
+        c.sync.acquire(0)                                # no active round
+    c.sync.begin_round(c.local, c.anchor, c.mom, 1)
+    with pytest.raises(EditSyncError):
+        c.sync.acquire(1)                                # out of order
+    c.sync.acquire(0)
+    c.sync.end_round()
+    torch.cuda.synchronize()
+    assert c.sync.stats(1).round == 1
