@@ -190,6 +190,7 @@ def main() -> None:
     ap.add_argument("--model", default="7B", choices=list(synth.LLAMA))
     ap.add_argument("--mesh", default=None, help="MxN shard x sync mesh (default 1xN)")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--algo", default="peer", choices=["peer", "nccl"], help="N > 1 exchange of Eq. 3")
     ap.add_argument("--e2e-units", default="1,2,3", help="unit indices timed through the host-buffer API")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -223,7 +224,8 @@ def main() -> None:
     numel = [synth.shard_numel(u.numel, M) for u in units]
     P_r = sum(numel)
     uid = broadcast_unique_id() if world > 1 else None
-    sync = EditSync(numel, shard_dim=M, sync_dim=N, rank=rank, device=dev, param_dtype=dtype, unique_id=uid)
+    sync = EditSync(numel, shard_dim=M, sync_dim=N, rank=rank, device=dev, param_dtype=dtype, unique_id=uid,
+                    algo=args.algo)
     # EMA seeded at the expected module norm of each replica (synth recipe, R8)
     import numpy as np
     mu = np.array([[synth.ema_seed(u, n)[0] for n in range(N)] for u in units])
@@ -302,9 +304,24 @@ def main() -> None:
     b_nvl = 8.0 * (N - 1) / N                   # NCCL bus bytes per direction per param
     k4_ms = phase_ms["outer_update"]
     k4_launches = args.steps * len(units)
-    k4_achieved = b_hbm * k4_elems / (k4_ms * 1e-3) / 1e9 if k4_ms > 0 else None
-    t_roof_nom = max(P_r * b_hbm / (NOMINAL_HBM_GBS * 1e9), P_r * b_nvl / (NOMINAL_NVL_GBS * 1e9)) * 1e3
-    t_roof_meas = max(P_r * b_hbm / (hbm_peak * 1e9), P_r * b_nvl / (MEASURED_NVL_GBS * 1e9)) * 1e3
+    # dominant kernel: K4 (outer_update; N == 1 or NCCL exchange) or, on the peer-memory path,
+    # ag_update (pulls Dbar over NVLink while applying K4's update).  Its algorithmic bytes:
+    # HBM 16 + 2 b_l (20 B bf16) and, on the peer path, NVLink 4 (N-1)/N B/param in.
+    peer = N > 1 and args.algo == "peer"
+    k4_name = "ag_update (RS'd Dbar pull + Nesterov + write-back)" if peer else "outer_update (K4)"
+    k4_hbm_B = b_hbm
+    k4_nvl_B = 4.0 * (N - 1) / N if peer else 0.0
+    t_hbm = k4_hbm_B / hbm_peak
+    t_nvl = k4_nvl_B / MEASURED_NVL_GBS
+    if k4_ms > 0 and t_nvl > t_hbm:
+        k4_bound, k4_peak, k4_B = "nvlink", MEASURED_NVL_GBS, k4_nvl_B
+    else:
+        k4_bound, k4_peak, k4_B = "hbm", hbm_peak, k4_hbm_B
+    k4_achieved = k4_B * k4_elems / (k4_ms * 1e-3) / 1e9 if k4_ms > 0 else None
+    if peer:
+        b_nvl = 6.0 * (N - 1) / N if b_l == 2 else 8.0 * (N - 1) / N  # bytes the peer path moves
+    t_roof_nom = max(P_r * b_hbm / (NOMINAL_HBM_GBS * 1e9), P_r * (8.0 * (N - 1) / N) / (NOMINAL_NVL_GBS * 1e9)) * 1e3
+    t_roof_meas = max(P_r * b_hbm / (hbm_peak * 1e9), P_r * (8.0 * (N - 1) / N) / (MEASURED_NVL_GBS * 1e9)) * 1e3
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -409,17 +426,24 @@ def main() -> None:
                                    f"of {len(units)} units ({P_r} params/rank), {args.dtype} local + f32 "
                                    "anchor/momentum",
                        "mesh": f"{M}x{N}", "params_per_rank": P_r, "param_dtype": args.dtype,
+                       "exchange": (args.algo if N > 1 else "none (N = 1)"),
                        "l2": "inputs (%.1f GB/rank) larger than L2" % (P_r * (b_l + 8) / 1e9),
                        "inner_steps": "locals redrawn as cast(anchor - D) between steps, outside the timed region"},
-            "roofline": {"bound": "hbm", "kernel": "outer_update (K4)", "achieved": k4_achieved, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": (k4_achieved / hbm_peak) if k4_achieved else None,
-                         "traffic": traffic, "algorithmic_bytes_per_param": b_hbm,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "_fallback" not in peaks
-                         else "fallback 6650 GB/s"},
+            "roofline": {"bound": k4_bound, "kernel": k4_name, "achieved": k4_achieved, "peak": k4_peak,
+                         "unit": "GB/s", "frac": (k4_achieved / k4_peak) if k4_achieved else None,
+                         "traffic": traffic if k4_bound == "hbm" else None,
+                         "algorithmic_bytes_per_param": k4_B,
+                         "peak_source": ("MEASURED_PEAKS.json hbm_gbs (measured)" if "_fallback" not in peaks
+                                         else "fallback 6650 GB/s") if k4_bound == "hbm" else
+                         "B200_PROFILING.md measured peer copy 770 GB/s per direction",
+                         "hbm_achieved_GBps": (k4_hbm_B * k4_elems / (k4_ms * 1e-3) / 1e9) if k4_ms > 0 else None},
             "sync_roofline": {"t_roof_ms_nominal": t_roof_nom, "frac_nominal": t_roof_nom / ms_per_step,
                               "t_roof_ms_measured": t_roof_meas, "frac_measured": t_roof_meas / ms_per_step,
                               "bound": "hbm" if N == 1 else "nvlink", "hbm_B_per_param": b_hbm,
-                              "nvlink_B_per_param_per_dir": b_nvl},
+                              "nvlink_B_per_param_per_dir_bus_convention": 8.0 * (N - 1) / N,
+                              "nvlink_B_per_param_per_dir_moved": b_nvl,
+                              "note": "T_roof per BASELINE.md: max(P_r*(16+2b_l)/HBM, P_r*8(N-1)/N/NVLink); "
+                                      "the peer path moves (b_l+4)(N-1)/N B/param, below the fp32 bus convention"},
             "phases_ms_per_step": {k: v / args.steps for k, v in phase_ms.items()},
             "per_gpu_GBps": bytes_per_rank_round / (ms_per_step * 1e-3) / 1e9,
             "rollbacks_last_round": rollbacks, "beta_sample": betas,

@@ -74,7 +74,18 @@ typedef struct {
   float ema_alpha;               /* alpha (0.02)                                     */
   int32_t ema_warmup_rounds;     /* EMA warm-up length (unstated -> 10, R8)          */
   uint32_t flags;                /* EDIT_NO_AE | EDIT_NO_WA | EDIT_NO_GC                   */
+  int32_t algo;                  /* N > 1 exchange (Eq. 3): EDIT_ALGO_PEER (default) or EDIT_ALGO_NCCL */
 } edit_sync_config_t;
+
+/* How Eq. 3's weighted sum crosses the sync group when N > 1:
+ *  EDIT_ALGO_PEER: fused peer-memory kernels over NVLink (CUDA IPC within one node): each
+ *    member reduces one 1/N slice straight from the peers' bf16/fp32 params
+ *    (Dbar = sum_j w_j (anchor - local_j)) and every member then pulls the reduced slices
+ *    while applying the update -- (b_l + 4)(N-1)/N bytes per param per direction.
+ *  EDIT_ALGO_NCCL: Delta in an fp32 buffer, ncclAllReduce with PreMulSum(w on device),
+ *    then the update -- 8(N-1)/N bytes per param per direction plus NCCL's HBM traffic. */
+#define EDIT_ALGO_PEER 0
+#define EDIT_ALGO_NCCL 1
 
 /* Outcome of the last completed sync of one unit (device-written, D5). */
 typedef struct {

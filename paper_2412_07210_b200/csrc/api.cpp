@@ -48,7 +48,8 @@ Layout layout_of(const edit_sync_config_t& c) {
   for (int i = 0; i < c.num_layers; ++i) max_numel = std::max<int64_t>(max_numel, c.layer_numel[i]);
   size_t off = 0;
   L.s_off = off;
-  L.s_bytes = c.sync_dim > 1 ? align_up((size_t)max_numel * sizeof(float), 256) : 0;
+  const bool nccl = c.sync_dim > 1 && c.algo == EDIT_ALGO_NCCL;
+  L.s_bytes = nccl ? align_up((size_t)max_numel * sizeof(float), 256) : 0;
   off += L.s_bytes;
   L.scratch_off = off;
   off += align_up(sizeof(LayerScratch) * (size_t)c.num_layers, 256);
@@ -65,7 +66,10 @@ Layout layout_of(const edit_sync_config_t& c) {
     L.part1.push_back(p);
     p += align_up(g * sizeof(double), 256);
     L.part2.push_back(p);
-    if (c.sync_dim > 1) p += align_up(g * sizeof(double), 256);
+    if (c.sync_dim > 1) {
+      const size_t g2 = nccl ? g : (size_t)rs_partial_slots(c.layer_numel[i], c.sync_dim);
+      p += align_up(g2 * sizeof(double), 256);
+    }
   }
   off += p;
   L.total = off;
@@ -96,6 +100,8 @@ edit_status_t validate(const edit_sync_config_t* c) {
   if (!(c->anomaly_threshold > 0.f)) return fail(EDIT_ERR_INVALID_ARG, "anomaly_threshold (delta) must be > 0");
   if (c->ema_warmup_rounds < 0) return fail(EDIT_ERR_INVALID_ARG, "ema_warmup_rounds must be >= 0");
   if (c->flags & ~(EDIT_NO_AE | EDIT_NO_WA | EDIT_NO_GC)) return fail(EDIT_ERR_INVALID_ARG, "unknown flags");
+  if (c->algo != EDIT_ALGO_PEER && c->algo != EDIT_ALGO_NCCL)
+    return fail(EDIT_ERR_INVALID_ARG, "algo must be EDIT_ALGO_PEER or EDIT_ALGO_NCCL");
   return EDIT_OK;
 }
 
@@ -108,7 +114,15 @@ struct edit_sync {
   int num_sms = 0;
   std::vector<double*> part1, part2;  // per-unit per-CTA partial slots (workspace)
   ncclComm_t global = nullptr, sync = nullptr, shard = nullptr;
-  std::vector<ncclRedOp_t> ops;  // per unit: PreMulSum with that unit's device weight
+  std::vector<ncclRedOp_t> ops;  // per unit: PreMulSum with that unit's device weight (NCCL algo)
+  // peer-memory algo: own staging copy of the local (L) and own Dbar slice (D), cudaMalloc'd
+  // and exported by CUDA IPC to the sync row; pp holds every member's mapped pointers
+  bool peer = false;
+  void* Lown = nullptr;
+  float* Down = nullptr;
+  PeerPtrs pp{};
+  std::vector<void*> opened;  // IPC mappings to close
+  bool ready = false;         // init completed (destroy may then barrier with the peers)
   char* ws = nullptr;
   float* S = nullptr;
   LayerScratch* scratch = nullptr;
@@ -251,7 +265,45 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
     // sync group (row): same shard index m, ordered by n; shard group (column): same n.
     INIT_NCCL(ncclCommSplit(h->global, h->shard_idx, h->sync_idx, &h->sync, nullptr));
     INIT_NCCL(ncclCommSplit(h->global, h->sync_idx, h->shard_idx, &h->shard, nullptr));
-    if (h->N > 1) {
+    if (h->N > 1 && cfg->algo == EDIT_ALGO_PEER) {
+      h->peer = true;
+      int64_t max_numel = 0;
+      for (int64_t x : h->numel) max_numel = std::max(max_numel, x);
+      const size_t esz = cfg->param_dtype == EDIT_BF16 ? 2 : 4;
+      const Slicing sl = slicing_of(max_numel, h->N, 0);
+      INIT_CUDA(cudaMalloc(&h->Lown, align_up((size_t)std::max<int64_t>(max_numel, 8) * esz, 256)));
+      INIT_CUDA(cudaMalloc(reinterpret_cast<void**>(&h->Down), align_up((size_t)sl.slice * 8 * sizeof(float), 256)));
+      // exchange the IPC handles over the sync comm (row): [N][2] cudaIpcMemHandle_t
+      cudaIpcMemHandle_t mine[2];
+      INIT_CUDA(cudaIpcGetMemHandle(&mine[0], h->Lown));
+      INIT_CUDA(cudaIpcGetMemHandle(&mine[1], h->Down));
+      const size_t hb = sizeof(mine);
+      char* dev = nullptr;
+      INIT_CUDA(cudaMalloc(&dev, hb * (h->N + 1)));
+      INIT_CUDA(cudaMemcpy(dev, mine, hb, cudaMemcpyHostToDevice));
+      cudaStream_t tmp;
+      INIT_CUDA(cudaStreamCreateWithFlags(&tmp, cudaStreamNonBlocking));
+      INIT_NCCL(ncclAllGather(dev, dev + hb, hb, ncclChar, h->sync, tmp));
+      INIT_CUDA(cudaStreamSynchronize(tmp));
+      INIT_CUDA(cudaStreamDestroy(tmp));
+      std::vector<cudaIpcMemHandle_t> all(2 * h->N);
+      INIT_CUDA(cudaMemcpy(all.data(), dev + hb, hb * h->N, cudaMemcpyDeviceToHost));
+      INIT_CUDA(cudaFree(dev));
+      for (int j = 0; j < h->N; ++j) {
+        if (j == h->sync_idx) {
+          h->pp.L[j] = h->Lown;
+          h->pp.D[j] = h->Down;
+          continue;
+        }
+        void *pl = nullptr, *pd = nullptr;
+        INIT_CUDA(cudaIpcOpenMemHandle(&pl, all[2 * j], cudaIpcMemLazyEnablePeerAccess));
+        h->opened.push_back(pl);
+        INIT_CUDA(cudaIpcOpenMemHandle(&pd, all[2 * j + 1], cudaIpcMemLazyEnablePeerAccess));
+        h->opened.push_back(pd);
+        h->pp.L[j] = pl;
+        h->pp.D[j] = static_cast<float*>(pd);
+      }
+    } else if (h->N > 1) {
       h->ops.assign(cfg->num_layers, ncclRedOp_t{});
       for (int l = 0; l < cfg->num_layers; ++l)
         INIT_NCCL(ncclRedOpCreatePreMulSum(&h->ops[l], &h->scratch[l].w, ncclFloat32,
@@ -260,6 +312,7 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
   }
 #undef INIT_CUDA
 #undef INIT_NCCL
+  h->ready = true;
   *out = h;
   return EDIT_OK;
 }
@@ -283,8 +336,11 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
   cudaEvent_t* ev = h->profiling ? &h->prof[(size_t)layer * (EDIT_NUM_PHASES + 1)] : nullptr;
   if (ev) CUDA_TRY(h, cudaEventRecord(ev[0], st));
   // K1: Delta and its shard norm (Alg. 2 l.442-443)
-  float* S = N > 1 ? h->S : nullptr;
-  launched += launch_pg_norm(dt, local, anchor, S, n, scr, h->part1[layer], st);
+  float* S = (N > 1 && !h->peer) ? h->S : nullptr;
+  if (h->peer)
+    launched += launch_pg_norm_copy(dt, local, anchor, h->Lown, n, scr, h->part1[layer], st);
+  else
+    launched += launch_pg_norm(dt, local, anchor, S, n, scr, h->part1[layer], st);
   CUDA_TRY(h, cudaGetLastError());
   if (ev) CUDA_TRY(h, cudaEventRecord(ev[1], st));
   // module norms of every replica on every rank: one K-scalar gather (R6)
@@ -301,6 +357,7 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
   d.ema = h->ema + (size_t)layer * N;
   d.rec = h->rec + layer;
   d.w_out = &scr->w;
+  d.w_all_out = scr->w_all;
   d.rollback_out = &scr->rollback;
   d.gsq_out = &scr->gsq;
   d.alpha = h->cfg.ema_alpha;
@@ -323,7 +380,20 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
   u.eps = h->cfg.clip_eps;
   u.flags = h->cfg.flags;
   u.rec = h->rec + layer;
-  if (N > 1) {
+  if (h->peer) {
+    // Eq. 3 as a reduce-scatter over NVLink peer memory: this rank's slice of Dbar
+    const Slicing sl = slicing_of(n, N, h->sync_idx);
+    launched += launch_rs(dt, h->pp, sl, anchor, h->Down, scr, h->part2[layer], st);
+    CUDA_TRY(h, cudaGetLastError());
+    if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
+    // ||Dbar||^2 of the module = sum over every slice of every shard: one K-scalar gather
+    // (also the barrier after which every member's D slice is complete)
+    NCCL_TRY(h, ncclAllGather(&scr->send2, scr->recv2, 1, ncclFloat64, h->global, st));
+    if (ev) CUDA_TRY(h, cudaEventRecord(ev[4], st));
+    u.gparts = scr->recv2;
+    u.n_gparts = h->K;
+    launched += launch_ag_update(dt, u, h->pp, sl, st);
+  } else if (N > 1) {
     // Eq. 3: Dbar = sum_n w_n Delta_n, the weight applied inside NCCL (PreMulSum)
     NCCL_TRY(h, ncclAllReduce(S, S, (size_t)n, ncclFloat32, h->ops[layer], h->sync, st));
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
@@ -344,7 +414,7 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
     u.gparts = &scr->gsq;
     u.n_gparts = 1;
   }
-  launched += launch_update(dt, u, st);
+  if (!h->peer) launched += launch_update(dt, u, st);
   CUDA_TRY(h, cudaGetLastError());
   if (ev) {
     CUDA_TRY(h, cudaEventRecord(ev[5], st));
@@ -580,8 +650,23 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
   edit_status_t st = EDIT_OK;
   cudaSetDevice(h->cfg.device);
   if (!h->poisoned) cudaDeviceSynchronize();
+  if (h->peer && h->ready && !h->poisoned && h->global) {
+    // barrier: no member may free its IPC-exported buffers while a peer still reads them
+    double* tmpd = nullptr;
+    cudaStream_t tmp = nullptr;
+    if (cudaMalloc(&tmpd, sizeof(double) * (h->K + 1)) == cudaSuccess &&
+        cudaStreamCreateWithFlags(&tmp, cudaStreamNonBlocking) == cudaSuccess) {
+      if (ncclAllGather(tmpd, tmpd + 1, 1, ncclFloat64, h->global, tmp) != ncclSuccess) st = EDIT_ERR_NCCL;
+      cudaStreamSynchronize(tmp);
+    }
+    if (tmp) cudaStreamDestroy(tmp);
+    if (tmpd) cudaFree(tmpd);
+  }
   for (size_t l = 0; l < h->ops.size(); ++l)
     if (h->sync) ncclRedOpDestroy(h->ops[l], h->sync);
+  for (void* p : h->opened) cudaIpcCloseMemHandle(p);
+  if (h->Lown) cudaFree(h->Lown);
+  if (h->Down) cudaFree(h->Down);
   if (h->shard) ncclCommDestroy(h->shard);
   if (h->sync) ncclCommDestroy(h->sync);
   if (h->global) ncclCommDestroy(h->global);

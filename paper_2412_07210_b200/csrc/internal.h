@@ -33,9 +33,10 @@ struct alignas(256) LayerScratch {
   double send2;               // this rank's ||Dbar_shard||^2             (K3 output)
   double pad0;
   double recv1[kMaxRanks];    // gathered send1 of all K ranks, index n*M + m
-  double recv2[EDIT_MAX_SHARD];  // gathered send2 of the M shard ranks
+  double recv2[kMaxRanks];    // gathered send2 (M shard ranks; all K ranks on the peer path)
   float w;                    // own Eq. 2 weight: the PreMulSum scalar
   int32_t rollback;           // Alg. 2 l.448
+  float w_all[EDIT_MAX_SYNC]; // every replica's Eq. 2 weight (peer-memory reduce-scatter)
   uint32_t counter1;          // last-CTA tickets
   uint32_t counter2;
 };
@@ -46,6 +47,7 @@ struct DecideArgs {
   edit_ema_t* ema;            // [N] EMA of this unit
   edit_layer_stats_t* rec;    // outcome record of this unit
   float* w_out;
+  float* w_all_out;
   int32_t* rollback_out;
   double* gsq_out;
   double alpha, delta;
@@ -68,12 +70,50 @@ struct UpdateArgs {
   edit_layer_stats_t* rec;
 };
 
+// Peer-memory view of a sync row (the N members sharing shard index m): every member's
+// staging copy of its local (L) and its slice of Dbar (D), mapped through CUDA IPC.
+struct PeerPtrs {
+  const void* L[EDIT_MAX_SYNC];
+  const float* D[EDIT_MAX_SYNC];
+};
+
+// Slicing of a unit's shard for the peer-memory reduce-scatter: nv = ceil(n/8) vectors,
+// owner j of vectors [j*slice, min((j+1)*slice, nv)); the last vector may be partial.
+struct Slicing {
+  int64_t n, nv, slice;
+  int32_t N, me;
+};
+inline Slicing slicing_of(int64_t n, int N, int me) {
+  Slicing s;
+  s.n = n;
+  s.nv = (n + 7) / 8;
+  s.slice = (s.nv + N - 1) / N;
+  if (s.slice < 1) s.slice = 1;
+  s.N = N;
+  s.me = me;
+  return s;
+}
+
 // Launchers (kernels.cu).  Each returns the number of kernels launched.
 // cta_parts: grid_of(n, kVecReduce) fp64 slots for the per-CTA partials.
 int launch_pg_norm(int dtype, const void* local, const float* anchor, float* S, int64_t n,
                    LayerScratch* scr, double* cta_parts, cudaStream_t st);
 int launch_sumsq(const float* x, int64_t n, LayerScratch* scr, double* cta_parts, cudaStream_t st);
 int launch_decide(const DecideArgs& a, cudaStream_t st);
+// K1 variant for the peer-memory path: also copies the local into this rank's staging L.
+int launch_pg_norm_copy(int dtype, const void* local, const float* anchor, void* Lcopy, int64_t n,
+                        LayerScratch* scr, double* cta_parts, cudaStream_t st);
+// RS: Dbar = sum_j w_j (anchor - L_j) over this rank's slice, written to its D; ||Dbar_slice||^2
+// -> scr->send2 (per-CTA partials in cta_parts, grid_of(slice*8, ...) slots).
+int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anchor, float* Dmine,
+              LayerScratch* scr, double* cta_parts, cudaStream_t st);
+// AG + update: Dbar pulled from each slice's owner, then the K4 math on the whole shard.
+int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl, cudaStream_t st);
+constexpr int kRsShape[2] = {1, 2};  // RS: N peer loads per vector already in flight per thread
+inline int64_t rs_partial_slots(int64_t n, int N) {
+  const Slicing s = slicing_of(n, N, 0);
+  return grid_of(s.slice * 8, kRsShape[0] * kRsShape[1]);
+}
 int launch_update(int dtype, const UpdateArgs& a, cudaStream_t st);
 
 }  // namespace edit

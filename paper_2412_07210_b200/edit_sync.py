@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_PKG, "libedit_sync.so")
 MAX_SYNC = 8
 UNIQUE_ID_BYTES = 128
 EDIT_BF16, EDIT_F32 = 0, 1
+ALGOS = {"peer": 0, "nccl": 1}
 NO_AE, NO_WA, NO_GC = 1, 2, 4
 
 EXPORTED = ("edit_sync_get_unique_id", "edit_sync_workspace_bytes", "edit_sync_init", "edit_layer_sync",
@@ -45,7 +46,7 @@ class Config(ctypes.Structure):
                 ("outer_momentum", ctypes.c_float), ("clip_threshold", ctypes.c_float),
                 ("clip_eps", ctypes.c_float), ("anomaly_threshold", ctypes.c_float),
                 ("ema_alpha", ctypes.c_float), ("ema_warmup_rounds", ctypes.c_int32),
-                ("flags", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("algo", ctypes.c_int32)]
 
 
 class LayerStatsC(ctypes.Structure):
@@ -148,7 +149,7 @@ class EditSync:
                  device=None, param_dtype=torch.bfloat16, outer_lr: float = 0.8,
                  outer_momentum: float = 0.85, clip_threshold: float = 10.0, clip_eps: float = 1e-6,
                  anomaly_threshold: float = 3.0, ema_alpha: float = 0.02, ema_warmup_rounds: int = 10,
-                 flags: int = 0, unique_id: bytes | None = None):
+                 flags: int = 0, unique_id: bytes | None = None, algo: str = "peer"):
         self._lib = load_library()
         self._h = None
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
@@ -164,7 +165,9 @@ class EditSync:
         self._numel_arr = (ctypes.c_int64 * max(1, self.num_layers))(*self.layer_numel)
         self._cfg = Config(self.shard_dim, self.sync_dim, self.rank, dev.index or 0, self.num_layers,
                            _DTYPES[param_dtype], self._numel_arr, outer_lr, outer_momentum, clip_threshold,
-                           clip_eps, anomaly_threshold, ema_alpha, int(ema_warmup_rounds), int(flags))
+                           clip_eps, anomaly_threshold, ema_alpha, int(ema_warmup_rounds), int(flags),
+                           ALGOS[algo])
+        self.algo = algo
         nbytes = ctypes.c_size_t()
         _check(self._lib.edit_sync_workspace_bytes(ctypes.byref(self._cfg), ctypes.byref(nbytes)))
         # workspace from torch's allocator (256-byte aligned by the caching allocator)

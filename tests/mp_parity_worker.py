@@ -5,7 +5,7 @@ Rank 0 regenerates every rank's seeded inputs (synth/, same Philox streams), run
 oracle for the whole mesh, gathers all ranks' outputs and compares; all ranks check the
 cross-rank invariants (identical anchors along a sync row, local == rne(anchor) bitwise).
 
-usage: torchrun --nproc-per-node K tests/mp_parity_worker.py MxN dtype config
+usage: torchrun --nproc-per-node K tests/mp_parity_worker.py MxN dtype config [peer|nccl]
 """
 import os
 import sys
@@ -33,6 +33,7 @@ def inputs_of(units, M, m, n, dtype, dev, plant, recipe, salt=0):
 
 def main():
     mesh, dtype_s, config = sys.argv[1], sys.argv[2], sys.argv[3]
+    algo = sys.argv[4] if len(sys.argv) > 4 else "peer"
     M, N = (int(x) for x in mesh.split("x"))
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     assert world == M * N
@@ -60,6 +61,9 @@ def main():
     elif config == "rollback":
         units = synth.toy_units(2, 40_000)
         plant = {(i, n): 4.0 for i in range(2) for n in range(N)}       # every replica anomalous
+    elif config == "nan":
+        units = [synth.Unit("a", 300_001, ()), synth.Unit("b", 9, ())]
+        seed_ema = False
     elif config == "llama350m_sample":
         all_units = synth.llama_units("350M")
         units = [all_units[0], all_units[1], all_units[33]]
@@ -70,7 +74,7 @@ def main():
     s = EditSync(numel, shard_dim=M, sync_dim=N, rank=rank, device=dev, param_dtype=dtype,
                  outer_lr=cfg.outer_lr, outer_momentum=cfg.outer_momentum, clip_threshold=cfg.clip_threshold,
                  clip_eps=cfg.clip_eps, anomaly_threshold=cfg.anomaly_threshold, ema_alpha=cfg.ema_alpha,
-                 ema_warmup_rounds=cfg.ema_warmup_rounds, flags=cfg.flags, unique_id=uid)
+                 ema_warmup_rounds=cfg.ema_warmup_rounds, flags=cfg.flags, unique_id=uid, algo=algo)
     ema0 = [[oracle.Ema() for _ in range(N)] for _ in units]
     if seed_ema:
         mu = np.array([[synth.ema_seed(u, n, recipe)[0] for n in range(N)] for u in units])
@@ -79,6 +83,8 @@ def main():
                 for i in range(len(units))]
 
     loc, anc, mom = inputs_of(units, M, m_idx, n_idx, dtype, dev, plant, recipe)
+    if config == "nan" and n_idx == N - 1:
+        loc[0][1234 % loc[0].numel()] = float("nan")   # replica N-1 has a NaN param (R9)
     for i in range(len(units)):
         s.layer_sync(i, loc[i], anc[i], mom[i])
     torch.cuda.synchronize()
@@ -100,9 +106,13 @@ def main():
                 a = synth.shard_anchor(u, i, M, m, dev, recipe)
                 ancs.append(a.cpu().numpy())
                 moms.append(synth.shard_momentum(u, i, M, m, dev, recipe).cpu().numpy())
-                locs.append([parity.to_oracle_local(synth.shard_local(u, i, M, m, n, a, dtype, dev, recipe,
-                                                                      plant.get((i, n), 1.0)))
-                             for n in range(N)])
+                row = []
+                for n in range(N):
+                    l = synth.shard_local(u, i, M, m, n, a, dtype, dev, recipe, plant.get((i, n), 1.0))
+                    if config == "nan" and n == N - 1 and i == 0:
+                        l[1234 % l.numel()] = float("nan")
+                    row.append(parity.to_oracle_local(l))
+                locs.append(row)
             o_loc, o_anc, o_mom, o_ema, out = oracle.sync_unit(cfg, np.array(locs), np.stack(ancs), np.stack(moms),
                                                                ema0[i])
             for r in range(world):
@@ -122,7 +132,9 @@ def main():
                 assert out.rollback
             if config == "toy_clip":
                 assert out.beta < 1.0
-        print(f"PARITY OK {config} {mesh} {dtype_s}: {len(units)} units", flush=True)
+            if config == "nan" and i == 0:
+                assert out.anomalous[N - 1] and not out.rollback
+        print(f"PARITY OK {config} {mesh} {dtype_s} {algo}: {len(units)} units", flush=True)
     s.close()
     dist.barrier(device_ids=[local_rank])
     dist.destroy_process_group()

@@ -86,10 +86,10 @@ def test_validation_without_gpu(lib_path):
     numel = (ctypes.c_int64 * 2)(10, 20)
     bad = [dict(shard_dim=0), dict(sync_dim=9), dict(rank=4), dict(outer_lr=0.0), dict(outer_momentum=1.0),
            dict(clip_threshold=-1.0), dict(clip_eps=0.0), dict(ema_alpha=0.0), dict(anomaly_threshold=0.0),
-           dict(param_dtype=7), dict(flags=8), dict(num_layers=0)]
+           dict(param_dtype=7), dict(flags=8), dict(num_layers=0), dict(algo=2)]
     base = dict(shard_dim=2, sync_dim=2, rank=0, device=0, num_layers=2, param_dtype=0, layer_numel=numel,
                 outer_lr=0.8, outer_momentum=0.85, clip_threshold=10.0, clip_eps=1e-6, anomaly_threshold=3.0,
-                ema_alpha=0.02, ema_warmup_rounds=10, flags=0)
+                ema_alpha=0.02, ema_warmup_rounds=10, flags=0, algo=0)
     nb = ctypes.c_size_t()
     assert lib.edit_sync_workspace_bytes(ctypes.byref(es.Config(**base)), ctypes.byref(nb)) == 0
     assert nb.value > 20 * 4
