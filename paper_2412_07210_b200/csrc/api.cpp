@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -121,6 +122,7 @@ struct edit_sync {
   void* Lown = nullptr;
   float* Down = nullptr;
   PeerPtrs pp{};
+  int peer_ctas = 148;        // persistent grid of the peer kernels (EDIT_PEER_CTAS env overrides)
   std::vector<void*> opened;  // IPC mappings to close
   bool ready = false;         // init completed (destroy may then barrier with the peers)
   char* ws = nullptr;
@@ -241,6 +243,11 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
 
   INIT_CUDA(cudaSetDevice(cfg->device));
   INIT_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
+  h->peer_ctas = h->num_sms;
+  if (const char* e = getenv("EDIT_PEER_CTAS")) {
+    const int v = atoi(e);
+    if (v > 0) h->peer_ctas = std::min(v, kMaxPeerCtas);
+  }
 
   h->ws = static_cast<char*>(workspace);
   h->S = L.s_bytes ? reinterpret_cast<float*>(h->ws + L.s_off) : nullptr;
@@ -383,7 +390,7 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
   if (h->peer) {
     // Eq. 3 as a reduce-scatter over NVLink peer memory: this rank's slice of Dbar
     const Slicing sl = slicing_of(n, N, h->sync_idx);
-    launched += launch_rs(dt, h->pp, sl, anchor, h->Down, scr, h->part2[layer], st);
+    launched += launch_rs(dt, h->pp, sl, anchor, h->Down, scr, h->part2[layer], h->peer_ctas, st);
     CUDA_TRY(h, cudaGetLastError());
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
     // ||Dbar||^2 of the module = sum over every slice of every shard: one K-scalar gather
@@ -392,7 +399,7 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[4], st));
     u.gparts = scr->recv2;
     u.n_gparts = h->K;
-    launched += launch_ag_update(dt, u, h->pp, sl, st);
+    launched += launch_ag_update(dt, u, h->pp, sl, h->peer_ctas, st);
   } else if (N > 1) {
     // Eq. 3: Dbar = sum_n w_n Delta_n, the weight applied inside NCCL (PreMulSum)
     NCCL_TRY(h, ncclAllReduce(S, S, (size_t)n, ncclFloat32, h->ops[layer], h->sync, st));

@@ -1,0 +1,142 @@
+// device_common.cuh -- device helpers shared by kernels.cu and peer_kernels.cu:
+// 8-element vector IO, deterministic CTA reductions, mbarrier / TMA (cp.async.bulk) wrappers.
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace edit {
+namespace dev {
+
+// ---------------------------------------------------------------- vector IO
+// 8 elements per vector: one 16-byte access of bf16 or two of fp32.  Plain ld/st: the
+// streaming cache hints (.cs / L1::no_allocate / .lu) measured 2-10% slower on K4.
+__device__ __forceinline__ void load8(const float* __restrict__ p, float (&v)[8]) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  const float4 b = *(reinterpret_cast<const float4*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void load8(const __nv_bfloat16* __restrict__ p, float (&v)[8]) {
+  const uint4 r = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[2 * i] = __uint_as_float(w[i] << 16);
+    v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+__device__ __forceinline__ void store8(float* __restrict__ p, const float (&v)[8]) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  *(reinterpret_cast<float4*>(p) + 1) = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* __restrict__ p, const float (&v)[8]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);  // RNE (R16)
+    w[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+__device__ __forceinline__ float load1(const float* p) { return *p; }
+__device__ __forceinline__ float load1(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ void store1(float* p, float v) { *p = v; }
+__device__ __forceinline__ void store1(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+
+// ---------------------------------------------------------------- reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Sum over a CTA of NT threads (result valid in thread 0).  Fixed tree: deterministic.
+template <int NT>
+__device__ double block_sum_n(double v) {
+  __shared__ double ws[NT / 32];
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) ws[warp] = v;
+  __syncthreads();
+  v = 0.0;
+  if (warp == 0) {
+    v = lane < (NT / 32) ? ws[lane] : 0.0;
+    v = warp_sum(v);
+  }
+  __syncthreads();
+  return v;
+}
+__device__ __forceinline__ double block_sum(double v) { return block_sum_n<kThreads>(v); }
+
+// Writes this CTA's partial; the last CTA to finish adds all partials in index order
+// (fp64) and stores the total in *out, then re-arms the ticket counter.
+template <int NT>
+__device__ void finish_partials_n(double cta_total, double* cta_parts, uint32_t* counter, double* out) {
+  __shared__ bool is_last;
+  if (threadIdx.x == 0) {
+    cta_parts[blockIdx.x] = cta_total;
+    __threadfence();
+    is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  // thread t adds partials t, t+NT, t+2NT, ... in that order; 8 loads in flight per step
+  const int G = (int)gridDim.x;
+  double v = 0.0;
+  int i = threadIdx.x;
+  for (; i + 7 * NT < G; i += 8 * NT) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = __ldcg(cta_parts + i + k * NT);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v += x[k];
+  }
+  for (; i < G; i += NT) v += __ldcg(cta_parts + i);
+  v = block_sum_n<NT>(v);
+  if (threadIdx.x == 0) {
+    *out = v;
+    *counter = 0u;
+  }
+}
+__device__ __forceinline__ void finish_partials(double cta_total, double* cta_parts, uint32_t* counter,
+                                                double* out) {
+  finish_partials_n<kThreads>(cta_total, cta_parts, counter, out);
+}
+
+// ---------------------------------------------------------------- mbarrier + TMA (sm_90+/sm_100a)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+// arrive (count 1) and add `bytes` to the expected transaction count of the current phase
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global (local HBM or an NVLink peer's memory) -> shared, completing on `bar`
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+}  // namespace dev
+}  // namespace edit

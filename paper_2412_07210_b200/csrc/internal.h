@@ -83,12 +83,17 @@ struct Slicing {
   int64_t n, nv, slice;
   int32_t N, me;
 };
+constexpr int kPeerTileVec = 256;  // vectors (of 8 elements) per TMA tile of the peer kernels
+constexpr int kMaxStages = 8;      // shared-memory ring depth cap
+constexpr int kMaxPeerCtas = 1024; // persistent grid cap of the peer kernels (per-CTA partial slots)
+// slices are whole tiles, so every AG tile has exactly one owner
 inline Slicing slicing_of(int64_t n, int N, int me) {
   Slicing s;
   s.n = n;
   s.nv = (n + 7) / 8;
-  s.slice = (s.nv + N - 1) / N;
-  if (s.slice < 1) s.slice = 1;
+  const int64_t per = (s.nv + N - 1) / N;
+  s.slice = (per + kPeerTileVec - 1) / kPeerTileVec * kPeerTileVec;
+  if (s.slice < kPeerTileVec) s.slice = kPeerTileVec;
   s.N = N;
   s.me = me;
   return s;
@@ -103,17 +108,14 @@ int launch_decide(const DecideArgs& a, cudaStream_t st);
 // K1 variant for the peer-memory path: also copies the local into this rank's staging L.
 int launch_pg_norm_copy(int dtype, const void* local, const float* anchor, void* Lcopy, int64_t n,
                         LayerScratch* scr, double* cta_parts, cudaStream_t st);
-// RS: Dbar = sum_j w_j (anchor - L_j) over this rank's slice, written to its D; ||Dbar_slice||^2
-// -> scr->send2 (per-CTA partials in cta_parts, grid_of(slice*8, ...) slots).
+// RS (peer_kernels.cu): Dbar = sum_j w_j (anchor - L_j) over this rank's slice, written to its D;
+// ||Dbar_slice||^2 -> scr->send2 (persistent grid <= max_ctas; cta_parts needs that many slots).
 int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anchor, float* Dmine,
-              LayerScratch* scr, double* cta_parts, cudaStream_t st);
+              LayerScratch* scr, double* cta_parts, int max_ctas, cudaStream_t st);
 // AG + update: Dbar pulled from each slice's owner, then the K4 math on the whole shard.
-int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl, cudaStream_t st);
-constexpr int kRsShape[2] = {1, 2};  // RS: N peer loads per vector already in flight per thread
-inline int64_t rs_partial_slots(int64_t n, int N) {
-  const Slicing s = slicing_of(n, N, 0);
-  return grid_of(s.slice * 8, kRsShape[0] * kRsShape[1]);
-}
+int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl, int max_ctas,
+                     cudaStream_t st);
+inline int64_t rs_partial_slots(int64_t, int) { return kMaxPeerCtas; }
 int launch_update(int dtype, const UpdateArgs& a, cudaStream_t st);
 
 }  // namespace edit

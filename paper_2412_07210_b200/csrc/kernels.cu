@@ -16,100 +16,12 @@
 #include <cuda_bf16.h>
 #include <math.h>
 
+#include "device_common.cuh"
 #include "internal.h"
 
 namespace edit {
 namespace {
-
-// ---------------------------------------------------------------- vector IO
-// 8 elements per vector: one 16-byte access of bf16 or two of fp32.  Plain ld/st: the
-// streaming cache hints (.cs / L1::no_allocate / .lu) measured 2-10% slower on K4.
-__device__ __forceinline__ void load8(const float* __restrict__ p, float (&v)[8]) {
-  const float4 a = *reinterpret_cast<const float4*>(p);
-  const float4 b = *(reinterpret_cast<const float4*>(p) + 1);
-  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-}
-__device__ __forceinline__ void load8(const __nv_bfloat16* __restrict__ p, float (&v)[8]) {
-  const uint4 r = *reinterpret_cast<const uint4*>(p);
-  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    v[2 * i] = __uint_as_float(w[i] << 16);
-    v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
-  }
-}
-__device__ __forceinline__ void store8(float* __restrict__ p, const float (&v)[8]) {
-  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-  *(reinterpret_cast<float4*>(p) + 1) = make_float4(v[4], v[5], v[6], v[7]);
-}
-__device__ __forceinline__ void store8(__nv_bfloat16* __restrict__ p, const float (&v)[8]) {
-  uint32_t w[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);  // RNE (R16)
-    w[i] = *reinterpret_cast<uint32_t*>(&h);
-  }
-  *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
-}
-__device__ __forceinline__ float load1(const float* p) { return *p; }
-__device__ __forceinline__ float load1(const __nv_bfloat16* p) { return __bfloat162float(*p); }
-__device__ __forceinline__ void store1(float* p, float v) { *p = v; }
-__device__ __forceinline__ void store1(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
-
-// ---------------------------------------------------------------- reductions
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// Sum over the CTA (result valid in thread 0).  Fixed tree: deterministic.
-__device__ double block_sum(double v) {
-  __shared__ double ws[kThreads / 32];
-  v = warp_sum(v);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) ws[warp] = v;
-  __syncthreads();
-  v = 0.0;
-  if (warp == 0) {
-    v = lane < (kThreads / 32) ? ws[lane] : 0.0;
-    v = warp_sum(v);
-  }
-  __syncthreads();
-  return v;
-}
-
-// Writes this CTA's partial; the last CTA to finish adds all partials in index order
-// (fp64) and stores the total in *out, then re-arms the ticket counter.
-__device__ void finish_partials(double cta_total, double* cta_parts, uint32_t* counter, double* out) {
-  __shared__ bool is_last;
-  if (threadIdx.x == 0) {
-    cta_parts[blockIdx.x] = cta_total;
-    __threadfence();
-    is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  // thread t adds partials t, t+T, t+2T, ... in that order; 8 loads in flight per step
-  const int G = (int)gridDim.x;
-  double v = 0.0;
-  int i = threadIdx.x;
-  for (; i + 7 * kThreads < G; i += 8 * kThreads) {
-    double x[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] = __ldcg(cta_parts + i + k * kThreads);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v += x[k];
-  }
-  for (; i < G; i += kThreads) v += __ldcg(cta_parts + i);
-  v = block_sum(v);
-  if (threadIdx.x == 0) {
-    *out = v;
-    *counter = 0u;
-  }
-}
+using namespace dev;
 
 // ---------------------------------------------------------------- K1
 // Alg. 2 l.442-443: Delta = anchor - local; partial ||Delta||^2 of this shard.
@@ -377,175 +289,6 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
   }
 }
 
-// ---------------------------------------------------------------- peer-memory path
-// RS (Eq. 3 over this rank's slice, read straight from the peers' staging copies over
-// NVLink): Dbar = sum_j w_j (anchor - L_j), fixed j order, peers with w_j == 0 skipped
-// (their params may be non-finite, R9).  Writes the slice into this rank's D and adds
-// ||Dbar_slice||^2 into scr->send2.  Only the owner computes a slice, and every member
-// reads it from there: the sync row gets bitwise-identical Dbar.
-template <typename T, int U, int I>
-__global__ void __launch_bounds__(kThreads) rs_kernel(const __grid_constant__ PeerPtrs pp, Slicing sl, const float* __restrict__ anchor,
-                                                      float* __restrict__ Dmine, LayerScratch* __restrict__ scr,
-                                                      double* __restrict__ cta_parts) {
-  const int64_t v0 = (int64_t)sl.me * sl.slice;
-  const int64_t v1 = min(v0 + sl.slice, sl.nv);
-  const int64_t nfull = sl.n >> 3;  // vectors with 8 valid elements
-  const int N = sl.N;
-  float w[EDIT_MAX_SYNC];
-#pragma unroll
-  for (int j = 0; j < EDIT_MAX_SYNC; ++j) w[j] = scr->w_all[j];
-  const bool skip = scr->rollback != 0;
-  const int64_t cta0 = v0 + (int64_t)blockIdx.x * kThreads * U * I + threadIdx.x;
-  float acc = 0.f;
-  if (!skip) {
-#pragma unroll 1
-    for (int it = 0; it < I; ++it) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t i = cta0 + (int64_t)(it * U + u) * kThreads;
-        if (i < v1 && i < nfull) {
-          float a[8], d[8];
-          load8(anchor + 8 * i, a);
-          uint4 raw[EDIT_MAX_SYNC];  // every peer's 16-byte chunk in flight at once
-#pragma unroll
-          for (int j = 0; j < EDIT_MAX_SYNC; ++j)
-            if (j < N && w[j] != 0.f) {
-              if (sizeof(T) == 2) raw[j] = *reinterpret_cast<const uint4*>(static_cast<const T*>(pp.L[j]) + 8 * i);
-            }
-#pragma unroll
-          for (int k = 0; k < 8; ++k) d[k] = 0.f;
-#pragma unroll
-          for (int j = 0; j < EDIT_MAX_SYNC; ++j)
-            if (j < N && w[j] != 0.f) {
-              float l[8];
-              if (sizeof(T) == 2) {
-                const uint32_t q[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  l[2 * k] = __uint_as_float(q[k] << 16);
-                  l[2 * k + 1] = __uint_as_float(q[k] & 0xffff0000u);
-                }
-              } else {
-                load8(static_cast<const float*>(pp.L[j]) + 8 * i, l);
-              }
-#pragma unroll
-              for (int k = 0; k < 8; ++k) d[k] = fmaf(w[j], a[k] - l[k], d[k]);
-            }
-#pragma unroll
-          for (int k = 0; k < 8; ++k) acc = fmaf(d[k], d[k], acc);
-          store8(Dmine + 8 * (i - v0), d);
-        }
-      }
-    }
-  }
-  double accd = (double)acc;
-  // the partial last vector (n % 8 elements), if this rank owns it
-  const int64_t vlast = sl.nv - 1;
-  if (!skip && (sl.n & 7) && vlast >= v0 && vlast < v1 && blockIdx.x == 0 && threadIdx.x < (sl.n & 7)) {
-    const int64_t k = 8 * vlast + threadIdx.x;
-    const float a = anchor[k];
-    float d = 0.f;
-    for (int j = 0; j < N; ++j)
-      if (w[j] != 0.f) d = fmaf(w[j], a - load1(static_cast<const T*>(pp.L[j]) + k), d);
-    accd += (double)(d * d);
-    Dmine[k - 8 * v0] = d;
-  }
-  accd = block_sum(accd);
-  finish_partials(accd, cta_parts, &scr->counter2, &scr->send2);
-}
-
-// AG + update: Dbar of vector i is read from its owner's D (NVLink for peers), then
-// beta (Eq. 4), Nesterov and the write-back exactly as K4.  CTAs are rotated by rank so
-// that at any moment the N members read from N different owners.
-template <typename T, int U, int I>
-__global__ void __launch_bounds__(kThreads) ag_update_kernel(UpdateArgs p, const __grid_constant__ PeerPtrs pp,
-                                                             Slicing sl) {
-  T* __restrict__ local = static_cast<T*>(p.local);
-  float* __restrict__ anchor = p.anchor;
-  float* __restrict__ mom = p.momentum;
-  __shared__ float s_beta;
-  __shared__ int s_rollback;
-  if (threadIdx.x == 0) {
-    double gsq = 0.0;
-    for (int i = 0; i < p.n_gparts; ++i) gsq += p.gparts[i];  // every slice of every shard, rank order
-    const double gbar = sqrt(gsq);
-    double beta_d = p.phi / (gbar + p.eps);
-    beta_d = beta_d < 1.0 ? beta_d : 1.0;
-    if (p.flags & EDIT_NO_GC) beta_d = 1.0;
-    const int rb = *p.rollback;
-    if (blockIdx.x == 0) {
-      p.rec->G_bar = rb ? 0.0 : gbar;
-      p.rec->beta = rb ? 1.0 : beta_d;
-      p.rec->rollback = rb;
-      p.rec->round += 1;
-    }
-    s_beta = (float)beta_d;
-    s_rollback = rb;
-  }
-  __syncthreads();
-  const float beta = s_beta, mu = p.mu, nu = p.nu;
-  const int64_t nfull = p.n >> 3;
-  const int64_t G = gridDim.x;
-  const int64_t chunk = (blockIdx.x + (int64_t)sl.me * G / sl.N) % G;
-  const int64_t cta0 = chunk * kThreads * U * I + threadIdx.x;
-  if (s_rollback) {  // Alg. 2 l.449
-#pragma unroll 1
-    for (int it = 0; it < I * U; ++it) {
-      const int64_t i = cta0 + (int64_t)it * kThreads;
-      if (i < nfull) {
-        float a[8];
-        load8(anchor + 8 * i, a);
-        store8(local + 8 * i, a);
-      }
-    }
-    if (chunk == 0 && threadIdx.x < (p.n & 7)) {
-      const int64_t k = 8 * nfull + threadIdx.x;
-      store1(local + k, anchor[k]);
-    }
-    return;
-  }
-#pragma unroll 1
-  for (int it = 0; it < I; ++it) {
-    float a[U][8], m[U][8], d[U][8];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = cta0 + (int64_t)(it * U + u) * kThreads;
-      if (i < nfull) {
-        const int64_t j = i / sl.slice;
-        load8(pp.D[j] + 8 * (i - j * sl.slice), d[u]);
-        load8(anchor + 8 * i, a[u]);
-        load8(mom + 8 * i, m[u]);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = cta0 + (int64_t)(it * U + u) * kThreads;
-      if (i < nfull) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float g = beta * d[u][k];
-          m[u][k] = fmaf(mu, m[u][k], g);
-          a[u][k] = a[u][k] - nu * fmaf(mu, m[u][k], g);
-        }
-        store8(mom + 8 * i, m[u]);
-        store8(anchor + 8 * i, a[u]);
-        store8(local + 8 * i, a[u]);
-      }
-    }
-  }
-  if (chunk == 0 && threadIdx.x < (p.n & 7)) {  // partial last vector
-    const int64_t k = 8 * nfull + threadIdx.x;
-    const int64_t j = nfull / sl.slice;
-    const float dk = pp.D[j][k - 8 * j * sl.slice];
-    const float g = beta * dk;
-    const float m1 = fmaf(mu, mom[k], g);
-    const float a1 = anchor[k] - nu * fmaf(mu, m1, g);
-    mom[k] = m1;
-    anchor[k] = a1;
-    store1(local + k, a1);
-  }
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
@@ -585,27 +328,6 @@ int launch_pg_norm_copy(int dtype, const void* local, const float* anchor, void*
   else
     pg_norm_kernel<float, false, kRedU, kRedI, true><<<grid, kThreads, 0, st>>>(
         static_cast<const float*>(local), anchor, nullptr, n, scr, cta_parts, static_cast<float*>(Lcopy));
-  return 1;
-}
-
-constexpr int kRsU = kRsShape[0], kRsI = kRsShape[1];
-
-int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anchor, float* Dmine,
-              LayerScratch* scr, double* cta_parts, cudaStream_t st) {
-  const unsigned grid = (unsigned)grid_of(sl.slice * 8, kRsU * kRsI);
-  if (dtype == EDIT_BF16)
-    rs_kernel<__nv_bfloat16, kRsU, kRsI><<<grid, kThreads, 0, st>>>(pp, sl, anchor, Dmine, scr, cta_parts);
-  else
-    rs_kernel<float, kRsU, kRsI><<<grid, kThreads, 0, st>>>(pp, sl, anchor, Dmine, scr, cta_parts);
-  return 1;
-}
-
-int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl, cudaStream_t st) {
-  const unsigned grid = (unsigned)grid_of(a.n, kUpdU * kUpdI);
-  if (dtype == EDIT_BF16)
-    ag_update_kernel<__nv_bfloat16, kUpdU, kUpdI><<<grid, kThreads, 0, st>>>(a, pp, sl);
-  else
-    ag_update_kernel<float, kUpdU, kUpdI><<<grid, kThreads, 0, st>>>(a, pp, sl);
   return 1;
 }
 

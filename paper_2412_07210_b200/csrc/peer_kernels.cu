@@ -1,0 +1,314 @@
+// peer_kernels.cu -- the N > 1 exchange of Eq. 3 (Alg. 2 l.452) as two
+// fused compute+communication kernels over NVLink peer memory (CUDA IPC within a node),
+// instead of an all-reduce of an fp32 pseudo-gradient buffer:
+//
+//   RS  (reduce-scatter): member n owns a 1/N slice of the shard; it pulls that slice of
+//       every member's staged local (bf16: 2 B/param) and computes
+//           Dbar = sum_j w_j (anchor - L_j)             (fixed j order; w_j == 0 skipped, R9)
+//       into its D buffer, plus ||Dbar_slice||^2 for the clip (Eq. 4).
+//   AG  (all-gather + update): every member pulls each slice of Dbar from its owner (fp32)
+//       and applies beta, the Nesterov step and the write-back (Eq. 5, l.454-455) -- the K4
+//       math -- on its whole shard.  All members read the same Dbar bits: bitwise-identical
+//       anchors along the sync row.
+//
+// Both are persistent, warp-specialised TMA pipelines: one producer thread streams tiles
+// (local HBM and peers alike) with 1-D bulk copies (cp.async.bulk ... complete_tx) into a
+// ring of shared-memory stages; 8 consumer warps compute from shared memory and store with
+// 16-byte STG.  Measured on B200 (profiles/r1_peer_bench_2gpu.txt): 16-32 CTAs of bulk
+// copies already pull ~780 GB/s from a peer, where plain LDG needs the whole GPU.
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include <algorithm>
+
+#include "device_common.cuh"
+#include "internal.h"
+
+namespace edit {
+namespace {
+using namespace dev;
+
+constexpr int kConsumerWarps = 8;
+constexpr int kPeerThreads = 32 * (1 + kConsumerWarps);  // warp 0 = producer
+constexpr int kSmemBudget = 200 * 1024;
+
+struct RingBars {
+  uint64_t full[kMaxStages];
+  uint64_t empty[kMaxStages];
+};
+
+__device__ __forceinline__ void ring_init(RingBars* b, int K) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < K; ++s) {
+      mbar_init(&b->full[s], 1);
+      mbar_init(&b->empty[s], kConsumerWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------------------ RS
+template <typename T>
+__global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_constant__ PeerPtrs pp, Slicing sl,
+                                                              const float* __restrict__ anchor,
+                                                              float* __restrict__ Dmine,
+                                                              LayerScratch* __restrict__ scr,
+                                                              double* __restrict__ cta_parts, int K) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ RingBars bars;
+  constexpr int V = kPeerTileVec;
+  const int N = sl.N;
+  float w[EDIT_MAX_SYNC];
+  int nact = 0;
+#pragma unroll
+  for (int j = 0; j < EDIT_MAX_SYNC; ++j) {
+    w[j] = scr->w_all[j];
+    nact += (j < N && w[j] != 0.f) ? 1 : 0;
+  }
+  const int lbytes = (int)sizeof(T);
+  const bool skip = scr->rollback != 0;
+  const int64_t n8 = sl.n >> 3;
+  const int64_t s0 = (int64_t)sl.me * sl.slice;                       // first vector of my slice
+  const int64_t s1 = min(s0 + sl.slice, n8);                           // end (full vectors only)
+  const int64_t ntiles = s1 > s0 ? (s1 - s0 + V - 1) / V : 0;
+  // stage layout: [anchor V*8 f32][L_0 V*8 T]...[L_{N-1}]; slots of w_j == 0 stay unused
+  const int stage_bytes = V * 8 * (4 + N * lbytes);
+  ring_init(&bars, K);
+  float acc = 0.f;
+  if (!skip) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) {
+      if (lane == 0) {  // producer
+        int it = 0;
+        for (int64_t q = blockIdx.x; q < ntiles; q += gridDim.x, ++it) {
+          const int s = it % K, use = it / K;
+          if (use > 0) mbar_wait(&bars.empty[s], (use - 1) & 1);
+          const int64_t v0 = s0 + q * V;
+          const int nv = (int)min((int64_t)V, s1 - v0);
+          char* st = smem + (size_t)s * stage_bytes;
+          mbar_arrive_expect_tx(&bars.full[s], (uint32_t)(nv * 8 * (4 + nact * lbytes)));
+          tma_load_1d(st, anchor + 8 * v0, nv * 32, &bars.full[s]);
+          for (int j = 0; j < N; ++j) {
+            if (w[j] == 0.f) continue;
+            tma_load_1d(st + V * 32 + j * V * 8 * lbytes, static_cast<const T*>(pp.L[j]) + 8 * v0,
+                        (uint32_t)(nv * 8 * lbytes), &bars.full[s]);
+          }
+        }
+      }
+    } else {  // consumers
+      const int t = threadIdx.x - 32;
+      int it = 0;
+      for (int64_t q = blockIdx.x; q < ntiles; q += gridDim.x, ++it) {
+        const int s = it % K, use = it / K;
+        mbar_wait(&bars.full[s], use & 1);
+        const int64_t v0 = s0 + q * V;
+        const int nv = (int)min((int64_t)V, s1 - v0);
+        const char* st = smem + (size_t)s * stage_bytes;
+        for (int v = t; v < nv; v += 32 * kConsumerWarps) {
+          float a[8], d[8];
+          load8(reinterpret_cast<const float*>(st) + 8 * v, a);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) d[k] = 0.f;
+#pragma unroll
+          for (int j = 0; j < EDIT_MAX_SYNC; ++j) {
+            if (j >= N || w[j] == 0.f) continue;
+            float l[8];
+            load8(reinterpret_cast<const T*>(st + V * 32 + j * V * 8 * lbytes) + 8 * v, l);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) d[k] = fmaf(w[j], a[k] - l[k], d[k]);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc = fmaf(d[k], d[k], acc);
+          store8(Dmine + 8 * (v0 - s0 + v), d);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.empty[s]);
+      }
+    }
+  }
+  double accd = (double)acc;
+  // the partial last vector (n % 8 elements) belongs to the owner of vector n8
+  const int64_t tail = sl.n & 7;
+  if (!skip && tail && n8 >= s0 && n8 < s0 + sl.slice && blockIdx.x == 0 && threadIdx.x >= 32 &&
+      threadIdx.x < 32 + tail) {
+    const int64_t k = 8 * n8 + (threadIdx.x - 32);
+    const float a = anchor[k];
+    float d = 0.f;
+    for (int j = 0; j < N; ++j)
+      if (w[j] != 0.f) d = fmaf(w[j], a - load1(static_cast<const T*>(pp.L[j]) + k), d);
+    accd += (double)(d * d);
+    Dmine[k - 8 * s0] = d;
+  }
+  accd = block_sum_n<kPeerThreads>(accd);
+  finish_partials_n<kPeerThreads>(accd, cta_parts, &scr->counter2, &scr->send2);
+}
+
+// ------------------------------------------------------------------------------ AG + update
+template <typename T>
+__global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs p,
+                                                                     const __grid_constant__ PeerPtrs pp,
+                                                                     Slicing sl, int K) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ RingBars bars;
+  __shared__ float s_beta;
+  __shared__ int s_rollback;
+  constexpr int V = kPeerTileVec;
+  T* __restrict__ local = static_cast<T*>(p.local);
+  float* __restrict__ anchor = p.anchor;
+  float* __restrict__ mom = p.momentum;
+  if (threadIdx.x == 0) {  // Eq. 4 once per CTA (fp64)
+    double gsq = 0.0;
+    for (int i = 0; i < p.n_gparts; ++i) gsq += p.gparts[i];  // every slice of every shard, rank order
+    const double gbar = sqrt(gsq);
+    double beta_d = p.phi / (gbar + p.eps);
+    beta_d = beta_d < 1.0 ? beta_d : 1.0;
+    if (p.flags & EDIT_NO_GC) beta_d = 1.0;
+    const int rb = *p.rollback;
+    if (blockIdx.x == 0) {
+      p.rec->G_bar = rb ? 0.0 : gbar;
+      p.rec->beta = rb ? 1.0 : beta_d;
+      p.rec->rollback = rb;
+      p.rec->round += 1;
+    }
+    s_beta = (float)beta_d;
+    s_rollback = rb;
+  }
+  ring_init(&bars, K);  // (contains __syncthreads)
+  const float beta = s_beta, mu = p.mu, nu = p.nu;
+  const int64_t n8 = p.n >> 3;
+  const int N = sl.N;
+  const int64_t tps = sl.slice / V;                      // tiles per slice (slices are tile-aligned)
+  const int64_t nq = (int64_t)N * tps;                   // owner-interleaved tile sequence
+  const int stage_bytes = V * 8 * 12;                    // Dbar | anchor | momentum, fp32
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // q -> (owner o = (q + me) mod N, k = q / N): at any moment a member's CTAs read from all
+  // N owners at once, and each owner serves all readers evenly.
+  auto tile_of = [&](int64_t q, int64_t& v0, int& nv, int& owner) {
+    owner = (int)((q + sl.me) % N);
+    v0 = owner * sl.slice + (q / N) * V;
+    nv = (int)max((int64_t)0, min((int64_t)V, n8 - v0));
+  };
+  if (s_rollback) {  // Alg. 2 l.449: local = rne(anchor), plain LDG/STG
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += stride) {
+      float a[8];
+      load8(anchor + 8 * i, a);
+      store8(local + 8 * i, a);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (p.n & 7)) {
+      const int64_t k = 8 * n8 + threadIdx.x;
+      store1(local + k, anchor[k]);
+    }
+    return;
+  }
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      int it = 0;
+      for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
+        int64_t v0;
+        int nv, owner;
+        tile_of(q, v0, nv, owner);
+        if (nv <= 0) continue;
+        const int s = it % K, use = it / K;
+        if (use > 0) mbar_wait(&bars.empty[s], (use - 1) & 1);
+        char* st = smem + (size_t)s * stage_bytes;
+        mbar_arrive_expect_tx(&bars.full[s], (uint32_t)(nv * 96));
+        tma_load_1d(st, pp.D[owner] + 8 * (v0 - owner * sl.slice), nv * 32, &bars.full[s]);
+        tma_load_1d(st + V * 32, anchor + 8 * v0, nv * 32, &bars.full[s]);
+        tma_load_1d(st + V * 64, mom + 8 * v0, nv * 32, &bars.full[s]);
+        ++it;
+      }
+    }
+  } else {  // consumers
+    const int t = threadIdx.x - 32;
+    int it = 0;
+    for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
+      int64_t v0;
+      int nv, owner;
+      tile_of(q, v0, nv, owner);
+      if (nv <= 0) continue;
+      const int s = it % K, use = it / K;
+      mbar_wait(&bars.full[s], use & 1);
+      const float* st = reinterpret_cast<const float*>(smem + (size_t)s * stage_bytes);
+      for (int v = t; v < nv; v += 32 * kConsumerWarps) {
+        float d[8], a[8], m[8];
+        load8(st + 8 * v, d);
+        load8(st + V * 8 + 8 * v, a);
+        load8(st + V * 16 + 8 * v, m);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float g = beta * d[k];             // Eq. 5
+          m[k] = fmaf(mu, m[k], g);                // m' = mu m + g
+          a[k] = a[k] - nu * fmaf(mu, m[k], g);    // a' = a - nu (g + mu m')
+        }
+        const int64_t i = v0 + v;
+        store8(mom + 8 * i, m);
+        store8(anchor + 8 * i, a);
+        store8(local + 8 * i, a);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.empty[s]);
+      ++it;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + (p.n & 7)) {  // partial last vector
+    const int64_t k = 8 * n8 + (threadIdx.x - 32);
+    const int64_t j = n8 / sl.slice;
+    const float dk = pp.D[j][k - 8 * j * sl.slice];
+    const float g = beta * dk;
+    const float m1 = fmaf(mu, mom[k], g);
+    const float a1 = anchor[k] - nu * fmaf(mu, m1, g);
+    mom[k] = m1;
+    anchor[k] = a1;
+    store1(local + k, a1);
+  }
+}
+
+template <typename KernelT>
+int stages_for(KernelT kernel, int stage_bytes) {
+  int K = kSmemBudget / stage_bytes;
+  K = K > kMaxStages ? kMaxStages : K;
+  K = K < 2 ? 2 : K;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, K * stage_bytes);
+  return K;
+}
+
+}  // namespace
+
+int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anchor, float* Dmine,
+              LayerScratch* scr, double* cta_parts, int max_ctas, cudaStream_t st) {
+  const int64_t n8 = sl.n >> 3;
+  const int64_t s0 = (int64_t)sl.me * sl.slice;
+  const int64_t s1 = n8 < s0 + sl.slice ? n8 : s0 + sl.slice;
+  const int64_t ntiles = s1 > s0 ? (s1 - s0 + kPeerTileVec - 1) / kPeerTileVec : 0;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, max_ctas));
+  const int esz = dtype == EDIT_BF16 ? 2 : 4;
+  const int stage_bytes = kPeerTileVec * 8 * (4 + sl.N * esz);
+  if (dtype == EDIT_BF16) {
+    const int K = stages_for(rs_tma_kernel<__nv_bfloat16>, stage_bytes);
+    rs_tma_kernel<__nv_bfloat16><<<grid, kPeerThreads, K * stage_bytes, st>>>(pp, sl, anchor, Dmine, scr,
+                                                                              cta_parts, K);
+  } else {
+    const int K = stages_for(rs_tma_kernel<float>, stage_bytes);
+    rs_tma_kernel<float><<<grid, kPeerThreads, K * stage_bytes, st>>>(pp, sl, anchor, Dmine, scr, cta_parts, K);
+  }
+  return 1;
+}
+
+int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl, int max_ctas,
+                     cudaStream_t st) {
+  const int64_t nq = (int64_t)sl.N * (sl.slice / kPeerTileVec);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nq, max_ctas));
+  const int stage_bytes = kPeerTileVec * 8 * 12;
+  if (dtype == EDIT_BF16) {
+    const int K = stages_for(ag_update_tma_kernel<__nv_bfloat16>, stage_bytes);
+    ag_update_tma_kernel<__nv_bfloat16><<<grid, kPeerThreads, K * stage_bytes, st>>>(a, pp, sl, K);
+  } else {
+    const int K = stages_for(ag_update_tma_kernel<float>, stage_bytes);
+    ag_update_tma_kernel<float><<<grid, kPeerThreads, K * stage_bytes, st>>>(a, pp, sl, K);
+  }
+  return 1;
+}
+
+}  // namespace edit
