@@ -509,9 +509,15 @@ edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* 
   if (!h->sched_stream) {
     int lo = 0, hi = 0;
     CUDA_TRY(h, cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    // the side stream gets the highest priority: its CTAs are scheduled ahead of the
-    // forward's GEMM tiles, so a unit's sync is never starved by the compute it hides behind
-    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->sched_stream, cudaStreamNonBlocking, hi));
+    // side-stream priority (EDIT_SCHED_PRIORITY=high|normal|low, default low): with the
+    // LOWEST priority the forward's GEMM CTAs are placed first and the sync's CTAs fill the
+    // threads/registers they leave free on each SM, instead of displacing them
+    int prio = lo;
+    if (const char* e = getenv("EDIT_SCHED_PRIORITY")) {
+      if (!strcmp(e, "high")) prio = hi;
+      else if (!strcmp(e, "normal")) prio = 0;
+    }
+    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->sched_stream, cudaStreamNonBlocking, prio));
     CUDA_TRY(h, cudaEventCreateWithFlags(&h->sched_start, cudaEventDisableTiming));
   }
   h->sched_local.assign(locals, locals + L);

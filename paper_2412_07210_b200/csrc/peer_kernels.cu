@@ -19,6 +19,8 @@
 #include <cuda_bf16.h>
 #include <math.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "device_common.cuh"
@@ -265,9 +267,18 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
   }
 }
 
+int smem_budget() {
+  static int b = [] {
+    const char* e = getenv("EDIT_PEER_SMEM_KB");  // shared-memory ring per CTA (default 200 KB)
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v * 1024 : kSmemBudget;
+  }();
+  return b;
+}
+
 template <typename KernelT>
 int stages_for(KernelT kernel, int stage_bytes) {
-  int K = kSmemBudget / stage_bytes;
+  int K = smem_budget() / stage_bytes;
   K = K > kMaxStages ? kMaxStages : K;
   K = K < 2 ? 2 : K;
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, K * stage_bytes);
