@@ -48,6 +48,20 @@ def measured_peaks() -> dict:
         return {"hbm_gbs": 6650.0, "_fallback": True}
 
 
+def max_over_ranks(t_ms: float, world: int, device) -> float:
+    """Multi-GPU timing rule: every number is the max over ranks (device-timed per rank)."""
+    if world <= 1:
+        return t_ms
+    tt = torch.tensor([t_ms], device=device, dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return float(tt.item())
+
+
+def rank_coords(rank: int, M: int) -> tuple[int, int]:
+    """(shard index m, sync index n) of a rank: rank = n*M + m (R20, include/edit_sync.h)."""
+    return rank % M, rank // M
+
+
 def parse_mesh(s: str | None, world: int) -> tuple[int, int]:
     if not s:
         return 1, world
@@ -198,6 +212,7 @@ def main() -> None:
     ap.add_argument("--overlap-tokens", type=int, default=8192,
                     help="tokens/GPU of the synthetic forward for the prefetch-overlap measurement (0 = skip)")
     ap.add_argument("--overlap-steps", type=int, default=3)
+    ap.add_argument("--lanes", type=int, default=1, help="experimental: pipeline units over k streams (N=M=1)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: W >= 3
@@ -217,7 +232,7 @@ def main() -> None:
     from paper_2412_07210_b200 import EditSync, broadcast_unique_id
 
     M, N = parse_mesh(args.mesh, world)
-    m_idx, n_idx = rank % M, rank // M
+    m_idx, n_idx = rank_coords(rank, M)
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     b_l = 2 if dtype == torch.bfloat16 else 4
     units = synth.llama_units(args.model)
@@ -250,9 +265,24 @@ def main() -> None:
         if world > 1:
             dist.barrier(device_ids=[local_rank])
 
+    lane_streams = [torch.cuda.Stream(dev) for _ in range(args.lanes)] if args.lanes > 1 else []
+
     def run_round():
+        if not lane_streams:
+            for i in range(len(units)):
+                sync.layer_sync(i, locs[i], anchors[i], moms[i], stream)
+            return
+        # experimental (N == M == 1 only: no collectives): units alternate between lanes
+        start = torch.cuda.Event()
+        start.record(stream)
+        for ls in lane_streams:
+            ls.wait_event(start)
         for i in range(len(units)):
-            sync.layer_sync(i, locs[i], anchors[i], moms[i], stream)
+            sync.layer_sync(i, locs[i], anchors[i], moms[i], lane_streams[i % len(lane_streams)])
+        for ls in lane_streams:
+            e = torch.cuda.Event()
+            e.record(ls)
+            stream.wait_event(e)
 
     for w in range(args.warmup):
         redraw(w + 1)
@@ -281,11 +311,7 @@ def main() -> None:
             for k, v in prof["ms"].items():
                 phase_ms[k] += v
             k4_elems += prof["elements"]
-            if world > 1:
-                tt = torch.tensor([t], device=dev, dtype=torch.float64)
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                t = float(tt.item())
-            step_ms.append(t)
+            step_ms.append(max_over_ranks(t, world, dev))
     launches = sync.kernel_launches - launches0
     sync.set_profiling(False)
     clk = clocks.summary()
@@ -349,10 +375,7 @@ def main() -> None:
                 ev1.record(stream)
                 torch.cuda.synchronize()
                 t = ev0.elapsed_time(ev1)
-                if world > 1:
-                    tt = torch.tensor([t], device=dev, dtype=torch.float64)
-                    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                    t = float(tt.item())
+                t = max_over_ranks(t, world, dev)
                 if s > 0:
                     ts.append(t)
             return sum(ts) / len(ts)
@@ -400,10 +423,7 @@ def main() -> None:
             ev1.record(stream)
             torch.cuda.synchronize()
             t = ev0.elapsed_time(ev1)
-            if world > 1:
-                tt = torch.tensor([t], device=dev, dtype=torch.float64)
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                t = float(tt.item())
+            t = max_over_ranks(t, world, dev)
             if s >= args.warmup:
                 e_ms.append(t)
         n_e = sum(numel[i] for i in idx)
