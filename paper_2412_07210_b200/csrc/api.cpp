@@ -123,6 +123,7 @@ struct edit_sync {
   float* Down = nullptr;
   PeerPtrs pp{};
   int peer_ctas = 148;        // persistent grid of the peer kernels (EDIT_PEER_CTAS env overrides)
+  int peer_tile = kPeerTileVec;  // vectors per TMA tile (EDIT_PEER_TILE env; must match on all ranks)
   std::vector<void*> opened;  // IPC mappings to close
   bool ready = false;         // init completed (destroy may then barrier with the peers)
   char* ws = nullptr;
@@ -244,6 +245,10 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
   INIT_CUDA(cudaSetDevice(cfg->device));
   INIT_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
   h->peer_ctas = h->num_sms;
+  if (const char* e = getenv("EDIT_PEER_TILE")) {
+    const int v = atoi(e);
+    if (v >= 32 && v <= 4096 && (v & 31) == 0) h->peer_tile = v;
+  }
   if (const char* e = getenv("EDIT_PEER_CTAS")) {
     const int v = atoi(e);
     if (v > 0) h->peer_ctas = std::min(v, kMaxPeerCtas);
@@ -277,7 +282,7 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
       int64_t max_numel = 0;
       for (int64_t x : h->numel) max_numel = std::max(max_numel, x);
       const size_t esz = cfg->param_dtype == EDIT_BF16 ? 2 : 4;
-      const Slicing sl = slicing_of(max_numel, h->N, 0);
+      const Slicing sl = slicing_of(max_numel, h->N, 0, h->peer_tile);
       INIT_CUDA(cudaMalloc(&h->Lown, align_up((size_t)std::max<int64_t>(max_numel, 8) * esz, 256)));
       INIT_CUDA(cudaMalloc(reinterpret_cast<void**>(&h->Down), align_up((size_t)sl.slice * 8 * sizeof(float), 256)));
       // exchange the IPC handles over the sync comm (row): [N][2] cudaIpcMemHandle_t
@@ -389,7 +394,7 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
   u.rec = h->rec + layer;
   if (h->peer) {
     // Eq. 3 as a reduce-scatter over NVLink peer memory: this rank's slice of Dbar
-    const Slicing sl = slicing_of(n, N, h->sync_idx);
+    const Slicing sl = slicing_of(n, N, h->sync_idx, h->peer_tile);
     launched += launch_rs(dt, h->pp, sl, anchor, h->Down, scr, h->part2[layer], h->peer_ctas, st);
     CUDA_TRY(h, cudaGetLastError());
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));

@@ -82,20 +82,22 @@ struct PeerPtrs {
 struct Slicing {
   int64_t n, nv, slice;
   int32_t N, me;
+  int32_t tile;  // vectors per TMA tile (slices are whole tiles)
 };
-constexpr int kPeerTileVec = 256;  // vectors (of 8 elements) per TMA tile of the peer kernels
+constexpr int kPeerTileVec = 512;  // default vectors (of 8 elements) per TMA tile of the peer kernels
 constexpr int kMaxStages = 8;      // shared-memory ring depth cap
 constexpr int kMaxPeerCtas = 1024; // persistent grid cap of the peer kernels (per-CTA partial slots)
 // slices are whole tiles, so every AG tile has exactly one owner
-inline Slicing slicing_of(int64_t n, int N, int me) {
+inline Slicing slicing_of(int64_t n, int N, int me, int tile = kPeerTileVec) {
   Slicing s;
   s.n = n;
   s.nv = (n + 7) / 8;
   const int64_t per = (s.nv + N - 1) / N;
-  s.slice = (per + kPeerTileVec - 1) / kPeerTileVec * kPeerTileVec;
-  if (s.slice < kPeerTileVec) s.slice = kPeerTileVec;
+  s.slice = (per + tile - 1) / tile * tile;
+  if (s.slice < tile) s.slice = tile;
   s.N = N;
   s.me = me;
+  s.tile = tile;
   return s;
 }
 

@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_const
                                                               double* __restrict__ cta_parts, int K) {
   extern __shared__ __align__(128) char smem[];
   __shared__ RingBars bars;
-  constexpr int V = kPeerTileVec;
+  const int V = sl.tile;
   const int N = sl.N;
   float w[EDIT_MAX_SYNC];
   int nact = 0;
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
   __shared__ RingBars bars;
   __shared__ float s_beta;
   __shared__ int s_rollback;
-  constexpr int V = kPeerTileVec;
+  const int V = sl.tile;
   T* __restrict__ local = static_cast<T*>(p.local);
   float* __restrict__ anchor = p.anchor;
   float* __restrict__ mom = p.momentum;
@@ -292,10 +292,10 @@ int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anc
   const int64_t n8 = sl.n >> 3;
   const int64_t s0 = (int64_t)sl.me * sl.slice;
   const int64_t s1 = n8 < s0 + sl.slice ? n8 : s0 + sl.slice;
-  const int64_t ntiles = s1 > s0 ? (s1 - s0 + kPeerTileVec - 1) / kPeerTileVec : 0;
+  const int64_t ntiles = s1 > s0 ? (s1 - s0 + sl.tile - 1) / sl.tile : 0;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, max_ctas));
   const int esz = dtype == EDIT_BF16 ? 2 : 4;
-  const int stage_bytes = kPeerTileVec * 8 * (4 + sl.N * esz);
+  const int stage_bytes = sl.tile * 8 * (4 + sl.N * esz);
   if (dtype == EDIT_BF16) {
     const int K = stages_for(rs_tma_kernel<__nv_bfloat16>, stage_bytes);
     rs_tma_kernel<__nv_bfloat16><<<grid, kPeerThreads, K * stage_bytes, st>>>(pp, sl, anchor, Dmine, scr,
@@ -309,9 +309,9 @@ int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anc
 
 int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl, int max_ctas,
                      cudaStream_t st) {
-  const int64_t nq = (int64_t)sl.N * (sl.slice / kPeerTileVec);
+  const int64_t nq = (int64_t)sl.N * (sl.slice / sl.tile);
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nq, max_ctas));
-  const int stage_bytes = kPeerTileVec * 8 * 12;
+  const int stage_bytes = sl.tile * 8 * 12;
   if (dtype == EDIT_BF16) {
     const int K = stages_for(ag_update_tma_kernel<__nv_bfloat16>, stage_bytes);
     ag_update_tma_kernel<__nv_bfloat16><<<grid, kPeerThreads, K * stage_bytes, st>>>(a, pp, sl, K);
