@@ -212,7 +212,8 @@ def main() -> None:
     ap.add_argument("--overlap-tokens", type=int, default=8192,
                     help="tokens/GPU of the synthetic forward for the prefetch-overlap measurement (0 = skip)")
     ap.add_argument("--overlap-steps", type=int, default=3)
-    ap.add_argument("--lanes", type=int, default=1, help="experimental: pipeline units over k streams (N=M=1)")
+    ap.add_argument("--sequential", action="store_true",
+                    help="time per-unit edit_layer_sync calls on one stream instead of edit_sync_round")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: W >= 3
@@ -265,24 +266,12 @@ def main() -> None:
         if world > 1:
             dist.barrier(device_ids=[local_rank])
 
-    lane_streams = [torch.cuda.Stream(dev) for _ in range(args.lanes)] if args.lanes > 1 else []
-
     def run_round():
-        if not lane_streams:
+        if args.sequential:
             for i in range(len(units)):
                 sync.layer_sync(i, locs[i], anchors[i], moms[i], stream)
-            return
-        # experimental (N == M == 1 only: no collectives): units alternate between lanes
-        start = torch.cuda.Event()
-        start.record(stream)
-        for ls in lane_streams:
-            ls.wait_event(start)
-        for i in range(len(units)):
-            sync.layer_sync(i, locs[i], anchors[i], moms[i], lane_streams[i % len(lane_streams)])
-        for ls in lane_streams:
-            e = torch.cuda.Event()
-            e.record(ls)
-            stream.wait_event(e)
+        else:  # edit_sync_round: units pipelined over the library's lanes
+            sync.sync_round(locs, anchors, moms, stream)
 
     for w in range(args.warmup):
         redraw(w + 1)
@@ -447,6 +436,8 @@ def main() -> None:
                                    "anchor/momentum",
                        "mesh": f"{M}x{N}", "params_per_rank": P_r, "param_dtype": args.dtype,
                        "exchange": (args.algo if N > 1 else "none (N = 1)"),
+                       "api": "edit_layer_sync x L (sequential)" if args.sequential else
+                       f"edit_sync_round ({os.environ.get('EDIT_LANES', '2')} lanes)",
                        "l2": "inputs (%.1f GB/rank) larger than L2" % (P_r * (b_l + 8) / 1e9),
                        "inner_steps": "locals redrawn as cast(anchor - D) between steps, outside the timed region"},
             "roofline": {"bound": k4_bound, "kernel": k4_name, "achieved": k4_achieved, "peak": k4_peak,

@@ -115,9 +115,11 @@ typedef struct {
  * (e.g. over a torch.distributed process group).  Not needed when M*N == 1. */
 edit_status_t edit_sync_get_unique_id(uint8_t id[EDIT_UNIQUE_ID_BYTES]);
 
-/* Device workspace the caller must provide to edit_sync_init (16-byte aligned,
- * on cfg->device).  Holds the fp32 exchange buffer (N > 1: max layer_numel * 4 B),
- * per-unit scratch, the EMA state [L][N] and the outcome records [L]. */
+/* Device workspace the caller must provide to edit_sync_init (256-byte aligned, on
+ * cfg->device): per-unit scratch and per-CTA partial slots, the EMA state [L][N] and the
+ * outcome records [L].  The exchange buffers of the N > 1 paths (peer: a staging copy of
+ * the local + a 1/N Dbar slice, exported by CUDA IPC; NCCL: an fp32 Delta buffer) are
+ * library-owned, one set per lane (see edit_sync_round), cudaMalloc'd by init. */
 edit_status_t edit_sync_workspace_bytes(const edit_sync_config_t* cfg, size_t* bytes);
 
 /* Collective over all M*N ranks (blocks until every rank has joined).
@@ -141,6 +143,16 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
  * data-dependent host branch (the rollback branch is taken on the device).
  * EDIT_ERR_INVALID_ARG: null handle/pointer, layer outside [0, L), misalignment. */
 edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* anchor, float* momentum,
+                              void* stream);
+
+/* One full sync round: every unit 0..L-1 (arrays of L device pointers), equivalent to
+ * calling edit_layer_sync for u = 0..L-1 in order but pipelined: units are dealt
+ * round-robin over the library's lanes (EDIT_LANES, default 2; each lane = an internal
+ * stream + its own NCCL communicators + exchange buffers), so unit u+1's norm pass and
+ * scalar gathers overlap unit u's exchange and update.  Starts after the work already on
+ * `stream`; `stream` waits for the whole round.  Same results, bit for bit, as the
+ * sequential calls (every unit's arithmetic and reduction order is unchanged). */
+edit_status_t edit_sync_round(edit_sync_t h, void* const* locals, float* const* anchors, float* const* momenta,
                               void* stream);
 
 /* Host-buffer variant (the paper's CPU offload of the extra parameters and outer

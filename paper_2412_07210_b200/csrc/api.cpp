@@ -39,7 +39,7 @@ edit_status_t fail(edit_status_t st, const std::string& msg) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t s_off, s_bytes, scratch_off, ema_off, rec_off, parts_off, total;
+  size_t scratch_off, ema_off, rec_off, parts_off, total;
   std::vector<size_t> part1, part2;  // per unit: offsets (bytes, from parts_off) of the per-CTA partials
 };
 
@@ -47,11 +47,9 @@ Layout layout_of(const edit_sync_config_t& c) {
   Layout L{};
   int64_t max_numel = 0;
   for (int i = 0; i < c.num_layers; ++i) max_numel = std::max<int64_t>(max_numel, c.layer_numel[i]);
+  (void)max_numel;
   size_t off = 0;
-  L.s_off = off;
   const bool nccl = c.sync_dim > 1 && c.algo == EDIT_ALGO_NCCL;
-  L.s_bytes = nccl ? align_up((size_t)max_numel * sizeof(float), 256) : 0;
-  off += L.s_bytes;
   L.scratch_off = off;
   off += align_up(sizeof(LayerScratch) * (size_t)c.num_layers, 256);
   L.ema_off = off;
@@ -108,30 +106,43 @@ edit_status_t validate(const edit_sync_config_t* c) {
 
 }  // namespace
 
+// A lane = one in-order pipeline of unit syncs: its stream (internal; the caller's stream for
+// edit_layer_sync), its own NCCL communicators (so two lanes' collectives never interleave on
+// one comm) and its own exchange buffers.  edit_sync_round / the prefetch scheduler deal
+// units round-robin over the lanes, so unit u+1's norm pass and scalar gathers run while unit
+// u's exchange and update run.  Every rank maps unit u to lane u % nlanes: the collective
+// order per communicator is identical on all ranks.
+struct Lane {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t tail = nullptr;  // join event
+  ncclComm_t global = nullptr, sync = nullptr, shard = nullptr;
+  std::vector<ncclRedOp_t> ops;  // NCCL algo: per unit PreMulSum with that unit's device weight
+  float* S = nullptr;            // NCCL algo: fp32 Delta exchange buffer
+  // peer algo: own staging copy of the local (L) and own Dbar slice (D), cudaMalloc'd and
+  // exported by CUDA IPC to the sync row; pp holds every member's mapped pointers
+  void* Lown = nullptr;
+  float* Down = nullptr;
+  PeerPtrs pp{};
+  std::vector<void*> opened;  // IPC mappings to close
+};
+
 struct edit_sync {
   edit_sync_config_t cfg{};
   std::vector<int64_t> numel;
   int M = 1, N = 1, K = 1, sync_idx = 0, shard_idx = 0;
   int num_sms = 0;
   std::vector<double*> part1, part2;  // per-unit per-CTA partial slots (workspace)
-  ncclComm_t global = nullptr, sync = nullptr, shard = nullptr;
-  std::vector<ncclRedOp_t> ops;  // per unit: PreMulSum with that unit's device weight (NCCL algo)
-  // peer-memory algo: own staging copy of the local (L) and own Dbar slice (D), cudaMalloc'd
-  // and exported by CUDA IPC to the sync row; pp holds every member's mapped pointers
-  bool peer = false;
-  void* Lown = nullptr;
-  float* Down = nullptr;
-  PeerPtrs pp{};
-  int peer_ctas = 148;        // persistent grid of the peer kernels (EDIT_PEER_CTAS env overrides)
+  std::vector<Lane> lanes;
+  bool peer = false;             // N > 1 and algo == EDIT_ALGO_PEER
+  int peer_ctas = 148;           // persistent grid of the peer kernels (EDIT_PEER_CTAS env overrides)
   int peer_tile = kPeerTileVec;  // vectors per TMA tile (EDIT_PEER_TILE env; must match on all ranks)
-  std::vector<void*> opened;  // IPC mappings to close
-  bool ready = false;         // init completed (destroy may then barrier with the peers)
+  bool ready = false;            // init completed (destroy may then barrier with the peers)
   char* ws = nullptr;
-  float* S = nullptr;
   LayerScratch* scratch = nullptr;
   edit_ema_t* ema = nullptr;
   edit_layer_stats_t* rec = nullptr;
   std::vector<cudaEvent_t> done;  // per unit: recorded after its last kernel
+  cudaEvent_t fork = nullptr;     // round API / scheduler: "the caller's inputs are ready"
   // profiling: EDIT_NUM_PHASES + 1 timing events per unit, and the units pending collection
   bool profiling = false;
   std::vector<cudaEvent_t> prof;
@@ -144,8 +155,6 @@ struct edit_sync {
   cudaEvent_t slot_in[2] = {nullptr, nullptr}, slot_done[2] = {nullptr, nullptr},
               slot_free[2] = {nullptr, nullptr};
   // prefetch scheduler state
-  cudaStream_t sched_stream = nullptr;
-  cudaEvent_t sched_start = nullptr;
   std::vector<void*> sched_local;
   std::vector<float*> sched_anchor, sched_mom;
   int sched_depth = 0, sched_next_sync = 0, sched_next_acquire = 0;
@@ -255,7 +264,6 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
   }
 
   h->ws = static_cast<char*>(workspace);
-  h->S = L.s_bytes ? reinterpret_cast<float*>(h->ws + L.s_off) : nullptr;
   h->scratch = reinterpret_cast<LayerScratch*>(h->ws + L.scratch_off);
   h->ema = reinterpret_cast<edit_ema_t*>(h->ws + L.ema_off);
   h->rec = reinterpret_cast<edit_layer_stats_t*>(h->ws + L.rec_off);
@@ -269,57 +277,79 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
 
   h->done.assign(cfg->num_layers, nullptr);
   for (auto& e : h->done) INIT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  INIT_CUDA(cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming));
 
-  if (K > 1) {
-    ncclUniqueId u;
-    memcpy(&u, id, sizeof u);
-    INIT_NCCL(ncclCommInitRank(&h->global, K, u, cfg->rank));
+  int nlanes = 2;  // EDIT_LANES (1..4) -- must be equal on every rank
+  if (const char* e = getenv("EDIT_LANES")) {
+    const int v = atoi(e);
+    if (v >= 1 && v <= 4) nlanes = v;
+  }
+  int prio_lo = 0, prio_hi = 0;
+  INIT_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  // lane-stream priority (EDIT_SCHED_PRIORITY=high|normal|low, default low): with the
+  // LOWEST priority a concurrent forward's GEMM CTAs are placed first and the sync's CTAs
+  // fill what they leave free on each SM, instead of displacing them
+  int prio = prio_lo;
+  if (const char* e = getenv("EDIT_SCHED_PRIORITY")) {
+    if (!strcmp(e, "high")) prio = prio_hi;
+    else if (!strcmp(e, "normal")) prio = 0;
+  }
+  h->lanes.resize(nlanes);
+  h->peer = h->N > 1 && cfg->algo == EDIT_ALGO_PEER;
+  int64_t max_numel = 0;
+  for (int64_t x : h->numel) max_numel = std::max(max_numel, x);
+  const size_t esz = cfg->param_dtype == EDIT_BF16 ? 2 : 4;
+  for (int li = 0; li < nlanes; ++li) {
+    Lane& ln = h->lanes[li];
+    INIT_CUDA(cudaStreamCreateWithPriority(&ln.stream, cudaStreamNonBlocking, prio));
+    INIT_CUDA(cudaEventCreateWithFlags(&ln.tail, cudaEventDisableTiming));
+    if (K == 1) continue;
+    if (li == 0) {
+      ncclUniqueId u;
+      memcpy(&u, id, sizeof u);
+      INIT_NCCL(ncclCommInitRank(&ln.global, K, u, cfg->rank));
+    } else {
+      INIT_NCCL(ncclCommSplit(h->lanes[0].global, 0, cfg->rank, &ln.global, nullptr));  // a dup
+    }
     // sync group (row): same shard index m, ordered by n; shard group (column): same n.
-    INIT_NCCL(ncclCommSplit(h->global, h->shard_idx, h->sync_idx, &h->sync, nullptr));
-    INIT_NCCL(ncclCommSplit(h->global, h->sync_idx, h->shard_idx, &h->shard, nullptr));
-    if (h->N > 1 && cfg->algo == EDIT_ALGO_PEER) {
-      h->peer = true;
-      int64_t max_numel = 0;
-      for (int64_t x : h->numel) max_numel = std::max(max_numel, x);
-      const size_t esz = cfg->param_dtype == EDIT_BF16 ? 2 : 4;
+    INIT_NCCL(ncclCommSplit(ln.global, h->shard_idx, h->sync_idx, &ln.sync, nullptr));
+    INIT_NCCL(ncclCommSplit(ln.global, h->sync_idx, h->shard_idx, &ln.shard, nullptr));
+    if (h->peer) {
       const Slicing sl = slicing_of(max_numel, h->N, 0, h->peer_tile);
-      INIT_CUDA(cudaMalloc(&h->Lown, align_up((size_t)std::max<int64_t>(max_numel, 8) * esz, 256)));
-      INIT_CUDA(cudaMalloc(reinterpret_cast<void**>(&h->Down), align_up((size_t)sl.slice * 8 * sizeof(float), 256)));
-      // exchange the IPC handles over the sync comm (row): [N][2] cudaIpcMemHandle_t
+      INIT_CUDA(cudaMalloc(&ln.Lown, align_up((size_t)std::max<int64_t>(max_numel, 8) * esz, 256)));
+      INIT_CUDA(cudaMalloc(reinterpret_cast<void**>(&ln.Down), align_up((size_t)sl.slice * 8 * sizeof(float), 256)));
+      // exchange the IPC handles over the lane's sync comm (row): [N][2] cudaIpcMemHandle_t
       cudaIpcMemHandle_t mine[2];
-      INIT_CUDA(cudaIpcGetMemHandle(&mine[0], h->Lown));
-      INIT_CUDA(cudaIpcGetMemHandle(&mine[1], h->Down));
+      INIT_CUDA(cudaIpcGetMemHandle(&mine[0], ln.Lown));
+      INIT_CUDA(cudaIpcGetMemHandle(&mine[1], ln.Down));
       const size_t hb = sizeof(mine);
       char* dev = nullptr;
       INIT_CUDA(cudaMalloc(&dev, hb * (h->N + 1)));
       INIT_CUDA(cudaMemcpy(dev, mine, hb, cudaMemcpyHostToDevice));
-      cudaStream_t tmp;
-      INIT_CUDA(cudaStreamCreateWithFlags(&tmp, cudaStreamNonBlocking));
-      INIT_NCCL(ncclAllGather(dev, dev + hb, hb, ncclChar, h->sync, tmp));
-      INIT_CUDA(cudaStreamSynchronize(tmp));
-      INIT_CUDA(cudaStreamDestroy(tmp));
+      INIT_NCCL(ncclAllGather(dev, dev + hb, hb, ncclChar, ln.sync, ln.stream));
+      INIT_CUDA(cudaStreamSynchronize(ln.stream));
       std::vector<cudaIpcMemHandle_t> all(2 * h->N);
       INIT_CUDA(cudaMemcpy(all.data(), dev + hb, hb * h->N, cudaMemcpyDeviceToHost));
       INIT_CUDA(cudaFree(dev));
       for (int j = 0; j < h->N; ++j) {
         if (j == h->sync_idx) {
-          h->pp.L[j] = h->Lown;
-          h->pp.D[j] = h->Down;
+          ln.pp.L[j] = ln.Lown;
+          ln.pp.D[j] = ln.Down;
           continue;
         }
         void *pl = nullptr, *pd = nullptr;
         INIT_CUDA(cudaIpcOpenMemHandle(&pl, all[2 * j], cudaIpcMemLazyEnablePeerAccess));
-        h->opened.push_back(pl);
+        ln.opened.push_back(pl);
         INIT_CUDA(cudaIpcOpenMemHandle(&pd, all[2 * j + 1], cudaIpcMemLazyEnablePeerAccess));
-        h->opened.push_back(pd);
-        h->pp.L[j] = pl;
-        h->pp.D[j] = static_cast<float*>(pd);
+        ln.opened.push_back(pd);
+        ln.pp.L[j] = pl;
+        ln.pp.D[j] = static_cast<float*>(pd);
       }
     } else if (h->N > 1) {
-      h->ops.assign(cfg->num_layers, ncclRedOp_t{});
+      INIT_CUDA(cudaMalloc(reinterpret_cast<void**>(&ln.S), align_up((size_t)std::max<int64_t>(max_numel, 8) * 4, 256)));
+      ln.ops.assign(cfg->num_layers, ncclRedOp_t{});
       for (int l = 0; l < cfg->num_layers; ++l)
-        INIT_NCCL(ncclRedOpCreatePreMulSum(&h->ops[l], &h->scratch[l].w, ncclFloat32,
-                                           ncclScalarDevice, h->sync));
+        INIT_NCCL(ncclRedOpCreatePreMulSum(&ln.ops[l], &h->scratch[l].w, ncclFloat32, ncclScalarDevice, ln.sync));
     }
   }
 #undef INIT_CUDA
@@ -329,16 +359,21 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
   return EDIT_OK;
 }
 
-edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* anchor, float* momentum,
-                              void* stream) {
+static edit_status_t check_unit_args(edit_sync_t h, int32_t layer, const void* local, const void* anchor,
+                                     const void* momentum) {
   if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
   if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
   if (layer < 0 || layer >= h->cfg.num_layers) return fail(EDIT_ERR_INVALID_ARG, "layer out of range");
-  const int64_t n = h->numel[layer];
-  if (n > 0 && (!local || !anchor || !momentum)) return fail(EDIT_ERR_INVALID_ARG, "null buffer");
+  if (h->numel[layer] > 0 && (!local || !anchor || !momentum)) return fail(EDIT_ERR_INVALID_ARG, "null buffer");
   if ((((uintptr_t)local) | ((uintptr_t)anchor) | ((uintptr_t)momentum)) & 15u)
     return fail(EDIT_ERR_INVALID_ARG, "buffers must be 16-byte aligned");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return EDIT_OK;
+}
+
+// Enqueue Sync() of one unit on stream `st` using lane `ln`'s communicators and buffers.
+static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* local, float* anchor, float* momentum,
+                               cudaStream_t st) {
+  const int64_t n = h->numel[layer];
   const int dt = h->cfg.param_dtype;
   LayerScratch* scr = &h->scratch[layer];
   const int M = h->M, N = h->N;
@@ -348,9 +383,9 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
   cudaEvent_t* ev = h->profiling ? &h->prof[(size_t)layer * (EDIT_NUM_PHASES + 1)] : nullptr;
   if (ev) CUDA_TRY(h, cudaEventRecord(ev[0], st));
   // K1: Delta and its shard norm (Alg. 2 l.442-443)
-  float* S = (N > 1 && !h->peer) ? h->S : nullptr;
+  float* S = (N > 1 && !h->peer) ? ln.S : nullptr;
   if (h->peer)
-    launched += launch_pg_norm_copy(dt, local, anchor, h->Lown, n, scr, h->part1[layer], st);
+    launched += launch_pg_norm_copy(dt, local, anchor, ln.Lown, n, scr, h->part1[layer], st);
   else
     launched += launch_pg_norm(dt, local, anchor, S, n, scr, h->part1[layer], st);
   CUDA_TRY(h, cudaGetLastError());
@@ -358,7 +393,7 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
   // module norms of every replica on every rank: one K-scalar gather (R6)
   const double* parts = &scr->send1;
   if (h->K > 1) {
-    NCCL_TRY(h, ncclAllGather(&scr->send1, scr->recv1, 1, ncclFloat64, h->global, st));
+    NCCL_TRY(h, ncclAllGather(&scr->send1, scr->recv1, 1, ncclFloat64, ln.global, st));
     parts = scr->recv1;
   }
   DecideArgs d{};
@@ -395,24 +430,24 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
   if (h->peer) {
     // Eq. 3 as a reduce-scatter over NVLink peer memory: this rank's slice of Dbar
     const Slicing sl = slicing_of(n, N, h->sync_idx, h->peer_tile);
-    launched += launch_rs(dt, h->pp, sl, anchor, h->Down, scr, h->part2[layer], h->peer_ctas, st);
+    launched += launch_rs(dt, ln.pp, sl, anchor, ln.Down, scr, h->part2[layer], h->peer_ctas, st);
     CUDA_TRY(h, cudaGetLastError());
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
     // ||Dbar||^2 of the module = sum over every slice of every shard: one K-scalar gather
     // (also the barrier after which every member's D slice is complete)
-    NCCL_TRY(h, ncclAllGather(&scr->send2, scr->recv2, 1, ncclFloat64, h->global, st));
+    NCCL_TRY(h, ncclAllGather(&scr->send2, scr->recv2, 1, ncclFloat64, ln.global, st));
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[4], st));
     u.gparts = scr->recv2;
     u.n_gparts = h->K;
-    launched += launch_ag_update(dt, u, h->pp, sl, h->peer_ctas, st);
+    launched += launch_ag_update(dt, u, ln.pp, sl, h->peer_ctas, st);
   } else if (N > 1) {
     // Eq. 3: Dbar = sum_n w_n Delta_n, the weight applied inside NCCL (PreMulSum)
-    NCCL_TRY(h, ncclAllReduce(S, S, (size_t)n, ncclFloat32, h->ops[layer], h->sync, st));
+    NCCL_TRY(h, ncclAllReduce(S, S, (size_t)n, ncclFloat32, ln.ops[layer], ln.sync, st));
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
     launched += launch_sumsq(S, n, scr, h->part2[layer], st);
     CUDA_TRY(h, cudaGetLastError());
     if (M > 1) {
-      NCCL_TRY(h, ncclAllGather(&scr->send2, scr->recv2, 1, ncclFloat64, h->shard, st));
+      NCCL_TRY(h, ncclAllGather(&scr->send2, scr->recv2, 1, ncclFloat64, ln.shard, st));
       u.gparts = scr->recv2;
       u.n_gparts = M;
     } else {
@@ -434,6 +469,41 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
   }
   CUDA_TRY(h, cudaEventRecord(h->done[layer], st));
   h->launches += launched;
+  return EDIT_OK;
+}
+
+edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* anchor, float* momentum,
+                              void* stream) {
+  edit_status_t rc = check_unit_args(h, layer, local, anchor, momentum);
+  if (rc != EDIT_OK) return rc;
+  return sync_unit(h, h->lanes[0], layer, local, anchor, momentum, static_cast<cudaStream_t>(stream));
+}
+
+edit_status_t edit_sync_round(edit_sync_t h, void* const* locals, float* const* anchors, float* const* momenta,
+                              void* stream) {
+  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
+  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  if (!locals || !anchors || !momenta) return fail(EDIT_ERR_INVALID_ARG, "null buffer arrays");
+  if (h->sched_active) return fail(EDIT_ERR_INVALID_ARG, "a scheduled round is active");
+  const int L = h->cfg.num_layers;
+  for (int u = 0; u < L; ++u) {
+    edit_status_t rc = check_unit_args(h, u, locals[u], anchors[u], momenta[u]);
+    if (rc != EDIT_OK) return rc;
+  }
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(h, cudaEventRecord(h->fork, cs));
+  const int nl = (int)h->lanes.size();
+  for (Lane& ln : h->lanes) CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->fork, 0));
+  for (int u = 0; u < L; ++u) {
+    Lane& ln = h->lanes[u % nl];
+    edit_status_t rc = sync_unit(h, ln, u, locals[u], anchors[u], momenta[u], ln.stream);
+    if (rc != EDIT_OK) return rc;
+  }
+  for (Lane& ln : h->lanes) {
+    CUDA_TRY(h, cudaEventRecord(ln.tail, ln.stream));
+    CUDA_TRY(h, cudaStreamWaitEvent(cs, ln.tail, 0));
+  }
   return EDIT_OK;
 }
 
@@ -499,7 +569,8 @@ edit_status_t edit_sync_host_wait(edit_sync_t h, void* stream) {
 
 static edit_status_t sched_enqueue_next(edit_sync_t h) {
   const int u = h->sched_next_sync++;
-  return edit_layer_sync(h, u, h->sched_local[u], h->sched_anchor[u], h->sched_mom[u], h->sched_stream);
+  Lane& ln = h->lanes[u % h->lanes.size()];
+  return sync_unit(h, ln, u, h->sched_local[u], h->sched_anchor[u], h->sched_mom[u], ln.stream);
 }
 
 edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* const* anchors,
@@ -510,21 +581,11 @@ edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* 
   if (depth < 1) return fail(EDIT_ERR_INVALID_ARG, "depth must be >= 1");
   if (h->sched_active) return fail(EDIT_ERR_INVALID_ARG, "a round is already active");
   const int L = h->cfg.num_layers;
-  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
-  if (!h->sched_stream) {
-    int lo = 0, hi = 0;
-    CUDA_TRY(h, cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    // side-stream priority (EDIT_SCHED_PRIORITY=high|normal|low, default low): with the
-    // LOWEST priority the forward's GEMM CTAs are placed first and the sync's CTAs fill the
-    // threads/registers they leave free on each SM, instead of displacing them
-    int prio = lo;
-    if (const char* e = getenv("EDIT_SCHED_PRIORITY")) {
-      if (!strcmp(e, "high")) prio = hi;
-      else if (!strcmp(e, "normal")) prio = 0;
-    }
-    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->sched_stream, cudaStreamNonBlocking, prio));
-    CUDA_TRY(h, cudaEventCreateWithFlags(&h->sched_start, cudaEventDisableTiming));
+  for (int u = 0; u < L; ++u) {
+    edit_status_t rc = check_unit_args(h, u, locals[u], anchors[u], momenta[u]);
+    if (rc != EDIT_OK) return rc;
   }
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   h->sched_local.assign(locals, locals + L);
   h->sched_anchor.assign(anchors, anchors + L);
   h->sched_mom.assign(momenta, momenta + L);
@@ -532,9 +593,10 @@ edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* 
   h->sched_next_sync = 0;
   h->sched_next_acquire = 0;
   h->sched_active = true;
-  cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
-  CUDA_TRY(h, cudaEventRecord(h->sched_start, cs));
-  CUDA_TRY(h, cudaStreamWaitEvent(h->sched_stream, h->sched_start, 0));
+  // the side streams (lanes) start after everything already on the compute stream (the
+  // inner steps that produced the locals)
+  CUDA_TRY(h, cudaEventRecord(h->fork, static_cast<cudaStream_t>(compute_stream)));
+  for (Lane& ln : h->lanes) CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->fork, 0));
   while (h->sched_next_sync < std::min(depth, L)) {
     edit_status_t rc = sched_enqueue_next(h);
     if (rc != EDIT_OK) return rc;
@@ -572,7 +634,11 @@ edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream) {
     edit_status_t rc = sched_enqueue_next(h);
     if (rc != EDIT_OK) return rc;
   }
-  CUDA_TRY(h, cudaStreamWaitEvent(static_cast<cudaStream_t>(compute_stream), h->done[L - 1], 0));
+  cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
+  for (Lane& ln : h->lanes) {
+    CUDA_TRY(h, cudaEventRecord(ln.tail, ln.stream));
+    CUDA_TRY(h, cudaStreamWaitEvent(cs, ln.tail, 0));
+  }
   h->sched_active = false;
   return EDIT_OK;
 }
@@ -583,9 +649,10 @@ edit_status_t edit_sync_stats(edit_sync_t h, int32_t layer, edit_layer_stats_t* 
   if (layer < 0 || layer >= h->cfg.num_layers) return fail(EDIT_ERR_INVALID_ARG, "layer out of range");
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   CUDA_TRY(h, cudaEventSynchronize(h->done[layer]));
-  if (h->global) {
+  for (Lane& ln : h->lanes) {
+    if (!ln.global) continue;
     ncclResult_t async_err = ncclSuccess;
-    NCCL_TRY(h, ncclCommGetAsyncError(h->global, &async_err));
+    NCCL_TRY(h, ncclCommGetAsyncError(ln.global, &async_err));
     if (async_err != ncclSuccess) {
       h->poisoned = true;
       return fail(EDIT_ERR_NCCL, std::string("async NCCL error: ") + ncclGetErrorString(async_err));
@@ -668,26 +735,30 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
   edit_status_t st = EDIT_OK;
   cudaSetDevice(h->cfg.device);
   if (!h->poisoned) cudaDeviceSynchronize();
-  if (h->peer && h->ready && !h->poisoned && h->global) {
+  if (h->peer && h->ready && !h->poisoned && !h->lanes.empty() && h->lanes[0].global) {
     // barrier: no member may free its IPC-exported buffers while a peer still reads them
     double* tmpd = nullptr;
-    cudaStream_t tmp = nullptr;
-    if (cudaMalloc(&tmpd, sizeof(double) * (h->K + 1)) == cudaSuccess &&
-        cudaStreamCreateWithFlags(&tmp, cudaStreamNonBlocking) == cudaSuccess) {
-      if (ncclAllGather(tmpd, tmpd + 1, 1, ncclFloat64, h->global, tmp) != ncclSuccess) st = EDIT_ERR_NCCL;
-      cudaStreamSynchronize(tmp);
+    if (cudaMalloc(&tmpd, sizeof(double) * (h->K + 1)) == cudaSuccess) {
+      if (ncclAllGather(tmpd, tmpd + 1, 1, ncclFloat64, h->lanes[0].global, h->lanes[0].stream) != ncclSuccess)
+        st = EDIT_ERR_NCCL;
+      cudaStreamSynchronize(h->lanes[0].stream);
+      cudaFree(tmpd);
     }
-    if (tmp) cudaStreamDestroy(tmp);
-    if (tmpd) cudaFree(tmpd);
   }
-  for (size_t l = 0; l < h->ops.size(); ++l)
-    if (h->sync) ncclRedOpDestroy(h->ops[l], h->sync);
-  for (void* p : h->opened) cudaIpcCloseMemHandle(p);
-  if (h->Lown) cudaFree(h->Lown);
-  if (h->Down) cudaFree(h->Down);
-  if (h->shard) ncclCommDestroy(h->shard);
-  if (h->sync) ncclCommDestroy(h->sync);
-  if (h->global) ncclCommDestroy(h->global);
+  for (Lane& ln : h->lanes) {
+    for (size_t l = 0; l < ln.ops.size(); ++l)
+      if (ln.sync) ncclRedOpDestroy(ln.ops[l], ln.sync);
+    for (void* p : ln.opened) cudaIpcCloseMemHandle(p);
+    if (ln.Lown) cudaFree(ln.Lown);
+    if (ln.Down) cudaFree(ln.Down);
+    if (ln.S) cudaFree(ln.S);
+    if (ln.shard) ncclCommDestroy(ln.shard);
+    if (ln.sync) ncclCommDestroy(ln.sync);
+    if (ln.global) ncclCommDestroy(ln.global);
+    if (ln.tail) cudaEventDestroy(ln.tail);
+    if (ln.stream) cudaStreamDestroy(ln.stream);
+  }
+  if (h->fork) cudaEventDestroy(h->fork);
   for (auto e : h->done)
     if (e) cudaEventDestroy(e);
   for (auto e : h->prof)
@@ -700,8 +771,6 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
   if (h->h2d) cudaStreamDestroy(h->h2d);
   if (h->d2h) cudaStreamDestroy(h->d2h);
   if (h->staging) cudaFree(h->staging);
-  if (h->sched_start) cudaEventDestroy(h->sched_start);
-  if (h->sched_stream) cudaStreamDestroy(h->sched_stream);
   delete h;
   return st;
 }

@@ -23,7 +23,7 @@ ALGOS = {"peer": 0, "nccl": 1}
 NO_AE, NO_WA, NO_GC = 1, 2, 4
 
 EXPORTED = ("edit_sync_get_unique_id", "edit_sync_workspace_bytes", "edit_sync_init", "edit_layer_sync",
-            "edit_layer_sync_host", "edit_sync_host_wait", "edit_sched_begin_round", "edit_sched_acquire",
+            "edit_layer_sync_host", "edit_sync_host_wait", "edit_sync_round", "edit_sched_begin_round", "edit_sched_acquire",
             "edit_sched_end_round",
             "edit_sync_stats", "edit_sync_get_state", "edit_sync_set_state", "edit_sync_kernel_launches",
             "edit_sync_set_profiling", "edit_sync_profile_collect",
@@ -80,6 +80,7 @@ def load_library() -> ctypes.CDLL:
     lib.edit_layer_sync.argtypes, lib.edit_layer_sync.restype = [P, I32, P, P, P, P], S
     lib.edit_layer_sync_host.argtypes, lib.edit_layer_sync_host.restype = [P, I32, P, P, P, P], S
     lib.edit_sync_host_wait.argtypes, lib.edit_sync_host_wait.restype = [P, P], S
+    lib.edit_sync_round.argtypes, lib.edit_sync_round.restype = [P, P, P, P, P], S
     lib.edit_sched_begin_round.argtypes, lib.edit_sched_begin_round.restype = [P, P, P, P, I32, P], S
     lib.edit_sched_acquire.argtypes, lib.edit_sched_acquire.restype = [P, I32, P], S
     lib.edit_sched_end_round.argtypes, lib.edit_sched_end_round.restype = [P, P], S
@@ -218,18 +219,10 @@ class EditSync:
     def begin_round(self, locals_, anchors, momenta, depth: int = 1, stream=None) -> None:
         """Start a layer-wise prefetched round: syncs run on a side stream, unit u+depth
         is enqueued when the forward acquires unit u."""
-        L = self.num_layers
-        for u in range(L):
-            for name, t, dt in (("local", locals_[u], self.param_dtype), ("anchor", anchors[u], torch.float32),
-                                ("momentum", momenta[u], torch.float32)):
-                if t.device != self.device or t.dtype != dt or not t.is_contiguous() or \
-                        t.numel() != self.layer_numel[u]:
-                    raise ValueError(f"unit {u} {name}: wrong device/dtype/shape")
-        arr = lambda ts: (ctypes.c_void_p * L)(*[t.data_ptr() for t in ts])
+        a, b, c = self._check_round(locals_, anchors, momenta)
         self._round_refs = (list(locals_), list(anchors), list(momenta))  # keep alive for the round
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
-        _check(self._lib.edit_sched_begin_round(self._h, arr(locals_), arr(anchors), arr(momenta), int(depth),
-                                                st.cuda_stream))
+        _check(self._lib.edit_sched_begin_round(self._h, a, b, c, int(depth), st.cuda_stream))
 
     def acquire(self, layer: int, stream=None) -> None:
         """The forward of unit `layer` may use its params after this (stream-ordered)."""
@@ -241,10 +234,24 @@ class EditSync:
         _check(self._lib.edit_sched_end_round(self._h, st.cuda_stream))
         self._round_refs = None
 
+    def _check_round(self, locals_, anchors, momenta):
+        L = self.num_layers
+        if not (len(locals_) == len(anchors) == len(momenta) == L):
+            raise ValueError(f"need {L} units")
+        for u in range(L):
+            for name, t, dt in (("local", locals_[u], self.param_dtype), ("anchor", anchors[u], torch.float32),
+                                ("momentum", momenta[u], torch.float32)):
+                if t.device != self.device or t.dtype != dt or not t.is_contiguous() or \
+                        t.numel() != self.layer_numel[u]:
+                    raise ValueError(f"unit {u} {name}: wrong device/dtype/shape")
+        arr = lambda ts: (ctypes.c_void_p * L)(*[t.data_ptr() for t in ts])
+        return arr(locals_), arr(anchors), arr(momenta)
+
     def sync_round(self, locals_, anchors, momenta, stream=None) -> None:
-        """All units in order (one full sync round)."""
-        for u in range(self.num_layers):
-            self.layer_sync(u, locals_[u], anchors[u], momenta[u], stream)
+        """One full round (all units), pipelined over the library's lanes (edit_sync_round)."""
+        a, b, c = self._check_round(locals_, anchors, momenta)
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _check(self._lib.edit_sync_round(self._h, a, b, c, st.cuda_stream))
 
     # ------------------------------------------------------------- queries
     def stats(self, layer: int) -> LayerStats:

@@ -34,6 +34,7 @@ def inputs_of(units, M, m, n, dtype, dev, plant, recipe, salt=0):
 def main():
     mesh, dtype_s, config = sys.argv[1], sys.argv[2], sys.argv[3]
     algo = sys.argv[4] if len(sys.argv) > 4 else "peer"
+    api = sys.argv[5] if len(sys.argv) > 5 else "unit"   # unit: edit_layer_sync x L; round: edit_sync_round
     M, N = (int(x) for x in mesh.split("x"))
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     assert world == M * N
@@ -85,8 +86,11 @@ def main():
     loc, anc, mom = inputs_of(units, M, m_idx, n_idx, dtype, dev, plant, recipe)
     if config == "nan" and n_idx == N - 1:
         loc[0][1234 % loc[0].numel()] = float("nan")   # replica N-1 has a NaN param (R9)
-    for i in range(len(units)):
-        s.layer_sync(i, loc[i], anc[i], mom[i])
+    if api == "round":
+        s.sync_round(loc, anc, mom)
+    else:
+        for i in range(len(units)):
+            s.layer_sync(i, loc[i], anc[i], mom[i])
     torch.cuda.synchronize()
     mine = {"rank": rank, "loc": [parity.to_oracle_local(x) for x in loc],
             "anc": [x.cpu().numpy() for x in anc], "mom": [x.cpu().numpy() for x in mom],
@@ -134,7 +138,7 @@ def main():
                 assert out.beta < 1.0
             if config == "nan" and i == 0:
                 assert out.anomalous[N - 1] and not out.rollback
-        print(f"PARITY OK {config} {mesh} {dtype_s} {algo}: {len(units)} units", flush=True)
+        print(f"PARITY OK {config} {mesh} {dtype_s} {algo} {api}: {len(units)} units", flush=True)
     s.close()
     dist.barrier(device_ids=[local_rank])
     dist.destroy_process_group()

@@ -19,21 +19,34 @@ CASES = [
     ("2x4", "bf16", "ragged"), ("4x2", "bf16", "toy"), ("4x2", "f32", "toy_clip"), ("1x8", "bf16", "nan"),
 ]
 ALGOS = ["peer", "nccl"]
+ROUND_CASES = [("1x2", "bf16", "ragged"), ("2x2", "f32", "toy"), ("1x4", "bf16", "nan"), ("2x1", "bf16", "ragged"),
+               ("2x4", "bf16", "toy"), ("1x8", "bf16", "ragged")]
 
 
 def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("algo", ALGOS)
-@pytest.mark.parametrize("mesh,dtype,config", CASES)
-def test_multirank_parity(mesh, dtype, config, algo):
+def _run(mesh, dtype, config, algo, api):
     M, N = (int(x) for x in mesh.split("x"))
     if _ngpus() < M * N:
         pytest.skip(f"needs {M * N} GPUs, have {_ngpus()}")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={M * N}",
            "--master-addr=127.0.0.1", "--master-port=29611", os.path.join(ROOT, "tests", "mp_parity_worker.py"),
-           mesh, dtype, config, algo]
+           mesh, dtype, config, algo, api]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
-    assert f"PARITY OK {config} {mesh} {dtype} {algo}" in r.stdout
+    assert f"PARITY OK {config} {mesh} {dtype} {algo} {api}" in r.stdout
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("mesh,dtype,config", CASES)
+def test_multirank_parity(mesh, dtype, config, algo):
+    _run(mesh, dtype, config, algo, "unit")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("mesh,dtype,config", ROUND_CASES)
+def test_multirank_parity_round_api(mesh, dtype, config, algo):
+    # edit_sync_round: units pipelined over two lanes (own comms / exchange buffers each)
+    _run(mesh, dtype, config, algo, "round")

@@ -241,3 +241,24 @@ def test_prefetch_scheduler_argument_errors():
     c.sync.end_round()
     torch.cuda.synchronize()
     assert c.sync.stats(1).round == 1
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_round_api_matches_oracle_and_sequential_bitwise(dtype):
+    # edit_sync_round (units over 2 lanes) == oracle, and == per-unit calls bit for bit
+    units = [synth.Unit(f"u{i}", n, ()) for i, n in enumerate([1_000_003, 65_536, 7, 2_000_000, 300_001])]
+    c = Case(units, DTYPES[dtype])
+    seq = Case(units, DTYPES[dtype])
+    c.sync.sync_round(c.local, c.anchor, c.mom)
+    for i in range(len(units)):
+        seq.sync.layer_sync(i, seq.local[i], seq.anchor[i], seq.mom[i])
+    torch.cuda.synchronize()
+    for i in range(len(units)):
+        assert torch.equal(c.local[i], seq.local[i]) and torch.equal(c.anchor[i], seq.anchor[i])
+        assert torch.equal(c.mom[i], seq.mom[i])
+        loc, anc, mom, ema, out = oracle.sync_unit(c.cfg, c.o_local[i][None, None], c.o_anchor[i][None],
+                                                   c.o_mom[i][None], c.o_ema[i])
+        parity.assert_outcome(c.sync.stats(i), out, ema, f"round unit {i}")
+        parity.assert_f32_close(c.anchor[i].cpu().numpy(), anc[0], "round anchor")
+        parity.assert_f32_close(c.mom[i].cpu().numpy(), mom[0], "round momentum")
+        parity.assert_local_close(parity.to_oracle_local(c.local[i]), loc[0, 0], "round local")
