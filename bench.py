@@ -302,8 +302,23 @@ def main() -> None:
             k4_elems += prof["elements"]
             step_ms.append(max_over_ranks(t, world, dev))
     launches = sync.kernel_launches - launches0
-    sync.set_profiling(False)
     clk = clocks.summary()
+    # the same kernels once more, isolated: per-unit calls on one stream (no lane overlap),
+    # outside the timed region -- each kernel's own duration for the isolated roofline
+    iso_ms = {k: 0.0 for k in sync.PHASES}
+    iso_elems = 0
+    for s in range(2):
+        redraw(5000 + s)
+        barrier()
+        torch.cuda.synchronize()
+        for i in range(len(units)):
+            sync.layer_sync(i, locs[i], anchors[i], moms[i], stream)
+        torch.cuda.synchronize()
+        prof = sync.profile_collect()
+        for k, v in prof["ms"].items():
+            iso_ms[k] += v
+        iso_elems += prof["elements"]
+    sync.set_profiling(False)
     # every unit's outcome of the last round (checks nothing rolled back unexpectedly)
     rollbacks = sum(int(sync.stats(i).rollback) for i in range(len(units)))
     betas = [sync.stats(i).beta for i in (0, 1, len(units) - 1)]
@@ -333,6 +348,9 @@ def main() -> None:
     else:
         k4_bound, k4_peak, k4_B = "hbm", hbm_peak, k4_hbm_B
     k4_achieved = k4_B * k4_elems / (k4_ms * 1e-3) / 1e9 if k4_ms > 0 else None
+    k4_iso = k4_B * iso_elems / (iso_ms["outer_update"] * 1e-3) / 1e9 if iso_ms["outer_update"] > 0 else None
+    k1_B = (2 * b_l + 4) if peer else (b_l + 4 + (4 if N > 1 else 0))   # K1 reads local+anchor (+ writes L copy / S)
+    k1_iso = k1_B * iso_elems / (iso_ms["pg_norm"] * 1e-3) / 1e9 if iso_ms["pg_norm"] > 0 else None
     if peer:
         b_nvl = 6.0 * (N - 1) / N if b_l == 2 else 8.0 * (N - 1) / N  # bytes the peer path moves
     t_roof_nom = max(P_r * b_hbm / (NOMINAL_HBM_GBS * 1e9), P_r * (8.0 * (N - 1) / N) / (NOMINAL_NVL_GBS * 1e9)) * 1e3
@@ -448,6 +466,14 @@ def main() -> None:
                                          else "fallback 6650 GB/s") if k4_bound == "hbm" else
                          "B200_PROFILING.md measured peer copy 770 GB/s per direction",
                          "hbm_achieved_GBps": (k4_hbm_B * k4_elems / (k4_ms * 1e-3) / 1e9) if k4_ms > 0 else None},
+            "roofline_isolated": {
+                "note": "same kernels, per-unit calls on one stream (no lane overlap), 2 rounds outside the timed "
+                        "region; achieved = algorithmic bytes / the kernel's own CUDA-event time",
+                "dominant": {"kernel": k4_name, "bound": k4_bound, "achieved": k4_iso, "peak": k4_peak,
+                             "frac": (k4_iso / k4_peak) if k4_iso else None},
+                "pg_norm": {"bytes_per_param": k1_B, "achieved": k1_iso, "peak": hbm_peak,
+                            "frac": (k1_iso / hbm_peak) if k1_iso else None},
+                "phases_ms_per_round": {k: v / 2 for k, v in iso_ms.items()}},
             "sync_roofline": {"t_roof_ms_nominal": t_roof_nom, "frac_nominal": t_roof_nom / ms_per_step,
                               "t_roof_ms_measured": t_roof_meas, "frac_measured": t_roof_meas / ms_per_step,
                               "bound": "hbm" if N == 1 else "nvlink", "hbm_B_per_param": b_hbm,
