@@ -136,6 +136,8 @@ struct edit_sync {
   bool peer = false;             // N > 1 and algo == EDIT_ALGO_PEER
   int peer_ctas = 148;           // persistent grid of the peer kernels (EDIT_PEER_CTAS env overrides)
   int peer_tile = kPeerTileVec;  // vectors per TMA tile (EDIT_PEER_TILE env; must match on all ranks)
+  bool ef_direct = false;        // L2 evict_first streaming for edit_layer_sync / edit_sync_round
+  bool ef_sched = true;          // ... for the prefetch scheduler (a forward runs concurrently)
   bool ready = false;            // init completed (destroy may then barrier with the peers)
   char* ws = nullptr;
   LayerScratch* scratch = nullptr;
@@ -258,6 +260,12 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
     const int v = atoi(e);
     if (v >= 32 && v <= 4096 && (v & 31) == 0) h->peer_tile = v;
   }
+  // L2 policy of the streaming passes: EDIT_L2_EVICT_FIRST = 0 | 1 | sched (default sched:
+  // only when a forward shares the GPU, i.e. scheduler rounds)
+  if (const char* e = getenv("EDIT_L2_EVICT_FIRST")) {
+    if (!strcmp(e, "1")) h->ef_direct = h->ef_sched = true;
+    else if (!strcmp(e, "0")) h->ef_direct = h->ef_sched = false;
+  }
   if (const char* e = getenv("EDIT_PEER_CTAS")) {
     const int v = atoi(e);
     if (v > 0) h->peer_ctas = std::min(v, kMaxPeerCtas);
@@ -372,7 +380,7 @@ static edit_status_t check_unit_args(edit_sync_t h, int32_t layer, const void* l
 
 // Enqueue Sync() of one unit on stream `st` using lane `ln`'s communicators and buffers.
 static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* local, float* anchor, float* momentum,
-                               cudaStream_t st) {
+                               cudaStream_t st, bool ef) {
   const int64_t n = h->numel[layer];
   const int dt = h->cfg.param_dtype;
   LayerScratch* scr = &h->scratch[layer];
@@ -385,9 +393,9 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
   // K1: Delta and its shard norm (Alg. 2 l.442-443)
   float* S = (N > 1 && !h->peer) ? ln.S : nullptr;
   if (h->peer)
-    launched += launch_pg_norm_copy(dt, local, anchor, ln.Lown, n, scr, h->part1[layer], st);
+    launched += launch_pg_norm_copy(dt, local, anchor, ln.Lown, n, scr, h->part1[layer], ef, st);
   else
-    launched += launch_pg_norm(dt, local, anchor, S, n, scr, h->part1[layer], st);
+    launched += launch_pg_norm(dt, local, anchor, S, n, scr, h->part1[layer], ef, st);
   CUDA_TRY(h, cudaGetLastError());
   if (ev) CUDA_TRY(h, cudaEventRecord(ev[1], st));
   // module norms of every replica on every rank: one K-scalar gather (R6)
@@ -430,7 +438,7 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
   if (h->peer) {
     // Eq. 3 as a reduce-scatter over NVLink peer memory: this rank's slice of Dbar
     const Slicing sl = slicing_of(n, N, h->sync_idx, h->peer_tile);
-    launched += launch_rs(dt, ln.pp, sl, anchor, ln.Down, scr, h->part2[layer], h->peer_ctas, st);
+    launched += launch_rs(dt, ln.pp, sl, anchor, ln.Down, scr, h->part2[layer], h->peer_ctas, ef, st);
     CUDA_TRY(h, cudaGetLastError());
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
     // ||Dbar||^2 of the module = sum over every slice of every shard: one K-scalar gather
@@ -439,12 +447,12 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[4], st));
     u.gparts = scr->recv2;
     u.n_gparts = h->K;
-    launched += launch_ag_update(dt, u, ln.pp, sl, h->peer_ctas, st);
+    launched += launch_ag_update(dt, u, ln.pp, sl, h->peer_ctas, ef, st);
   } else if (N > 1) {
     // Eq. 3: Dbar = sum_n w_n Delta_n, the weight applied inside NCCL (PreMulSum)
     NCCL_TRY(h, ncclAllReduce(S, S, (size_t)n, ncclFloat32, ln.ops[layer], ln.sync, st));
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
-    launched += launch_sumsq(S, n, scr, h->part2[layer], st);
+    launched += launch_sumsq(S, n, scr, h->part2[layer], ef, st);
     CUDA_TRY(h, cudaGetLastError());
     if (M > 1) {
       NCCL_TRY(h, ncclAllGather(&scr->send2, scr->recv2, 1, ncclFloat64, ln.shard, st));
@@ -461,7 +469,7 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
     u.gparts = &scr->gsq;
     u.n_gparts = 1;
   }
-  if (!h->peer) launched += launch_update(dt, u, st);
+  if (!h->peer) launched += launch_update(dt, u, ef, st);
   CUDA_TRY(h, cudaGetLastError());
   if (ev) {
     CUDA_TRY(h, cudaEventRecord(ev[5], st));
@@ -476,7 +484,7 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
                               void* stream) {
   edit_status_t rc = check_unit_args(h, layer, local, anchor, momentum);
   if (rc != EDIT_OK) return rc;
-  return sync_unit(h, h->lanes[0], layer, local, anchor, momentum, static_cast<cudaStream_t>(stream));
+  return sync_unit(h, h->lanes[0], layer, local, anchor, momentum, static_cast<cudaStream_t>(stream), h->ef_direct);
 }
 
 edit_status_t edit_sync_round(edit_sync_t h, void* const* locals, float* const* anchors, float* const* momenta,
@@ -497,7 +505,7 @@ edit_status_t edit_sync_round(edit_sync_t h, void* const* locals, float* const* 
   for (Lane& ln : h->lanes) CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->fork, 0));
   for (int u = 0; u < L; ++u) {
     Lane& ln = h->lanes[u % nl];
-    edit_status_t rc = sync_unit(h, ln, u, locals[u], anchors[u], momenta[u], ln.stream);
+    edit_status_t rc = sync_unit(h, ln, u, locals[u], anchors[u], momenta[u], ln.stream, h->ef_direct);
     if (rc != EDIT_OK) return rc;
   }
   for (Lane& ln : h->lanes) {
@@ -570,7 +578,7 @@ edit_status_t edit_sync_host_wait(edit_sync_t h, void* stream) {
 static edit_status_t sched_enqueue_next(edit_sync_t h) {
   const int u = h->sched_next_sync++;
   Lane& ln = h->lanes[u % h->lanes.size()];
-  return sync_unit(h, ln, u, h->sched_local[u], h->sched_anchor[u], h->sched_mom[u], ln.stream);
+  return sync_unit(h, ln, u, h->sched_local[u], h->sched_anchor[u], h->sched_mom[u], ln.stream, h->ef_sched);
 }
 
 edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* const* anchors,

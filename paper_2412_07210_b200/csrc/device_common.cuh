@@ -10,16 +10,43 @@ namespace edit {
 namespace dev {
 
 // ---------------------------------------------------------------- vector IO
-// 8 elements per vector: one 16-byte access of bf16 or two of fp32.  Plain ld/st: the
-// streaming cache hints (.cs / L1::no_allocate / .lu) measured 2-10% slower on K4.
-__device__ __forceinline__ void load8(const float* __restrict__ p, float (&v)[8]) {
-  const float4 a = *reinterpret_cast<const float4*>(p);
-  const float4 b = *(reinterpret_cast<const float4*>(p) + 1);
-  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+// 8 elements per vector: one 16-byte access of bf16 or two of fp32.
+// kEF = stream with an L2 evict_first policy (createpolicy ... L2::evict_first +
+// ld/st .L2::cache_hint): the sync's bytes are then the first to leave the 126 MB L2, so a
+// concurrent forward keeps its GEMM operand tiles resident (profiles/r1_coresidency_*).
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
-__device__ __forceinline__ void load8(const __nv_bfloat16* __restrict__ p, float (&v)[8]) {
-  const uint4 r = *reinterpret_cast<const uint4*>(p);
+template <bool kEF>
+__device__ __forceinline__ uint4 ldg16(const void* p, uint64_t pol) {
+  uint4 r;
+  if (kEF)
+    asm volatile("ld.global.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+  else
+    r = *reinterpret_cast<const uint4*>(p);
+  return r;
+}
+template <bool kEF>
+__device__ __forceinline__ void stg16(void* p, uint4 v, uint64_t pol) {
+  if (kEF)
+    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w), "l"(pol)
+                 : "memory");
+  else
+    *reinterpret_cast<uint4*>(p) = v;
+}
+template <bool kEF = false>
+__device__ __forceinline__ void load8(const float* __restrict__ p, float (&v)[8], uint64_t pol = 0) {
+  const uint4 a = ldg16<kEF>(p, pol), b = ldg16<kEF>(p + 4, pol);
+  v[0] = __uint_as_float(a.x); v[1] = __uint_as_float(a.y); v[2] = __uint_as_float(a.z); v[3] = __uint_as_float(a.w);
+  v[4] = __uint_as_float(b.x); v[5] = __uint_as_float(b.y); v[6] = __uint_as_float(b.z); v[7] = __uint_as_float(b.w);
+}
+template <bool kEF = false>
+__device__ __forceinline__ void load8(const __nv_bfloat16* __restrict__ p, float (&v)[8], uint64_t pol = 0) {
+  const uint4 r = ldg16<kEF>(p, pol);
   const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -27,18 +54,23 @@ __device__ __forceinline__ void load8(const __nv_bfloat16* __restrict__ p, float
     v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
   }
 }
-__device__ __forceinline__ void store8(float* __restrict__ p, const float (&v)[8]) {
-  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-  *(reinterpret_cast<float4*>(p) + 1) = make_float4(v[4], v[5], v[6], v[7]);
+template <bool kEF = false>
+__device__ __forceinline__ void store8(float* __restrict__ p, const float (&v)[8], uint64_t pol = 0) {
+  stg16<kEF>(p, make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3])),
+             pol);
+  stg16<kEF>(p + 4,
+             make_uint4(__float_as_uint(v[4]), __float_as_uint(v[5]), __float_as_uint(v[6]), __float_as_uint(v[7])),
+             pol);
 }
-__device__ __forceinline__ void store8(__nv_bfloat16* __restrict__ p, const float (&v)[8]) {
+template <bool kEF = false>
+__device__ __forceinline__ void store8(__nv_bfloat16* __restrict__ p, const float (&v)[8], uint64_t pol = 0) {
   uint32_t w[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);  // RNE (R16)
     w[i] = *reinterpret_cast<uint32_t*>(&h);
   }
-  *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  stg16<kEF>(p, make_uint4(w[0], w[1], w[2], w[3]), pol);
 }
 __device__ __forceinline__ float load1(const float* p) { return *p; }
 __device__ __forceinline__ float load1(const __nv_bfloat16* p) { return __bfloat162float(*p); }
@@ -131,11 +163,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 // 1-D bulk copy global (local HBM or an NVLink peer's memory) -> shared, completing on `bar`
-__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst_smem)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
+template <bool kEF = false>
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar,
+                                            uint64_t pol = 0) {
+  if (kEF)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_u32(dst_smem)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+  else
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst_smem)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 
 }  // namespace dev

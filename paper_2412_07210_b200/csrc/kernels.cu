@@ -28,7 +28,7 @@ using namespace dev;
 // Shape: CTA b owns vectors [b*T*U*I, (b+1)*T*U*I); a thread walks I steps of U vectors
 // (stride T), issuing the U vectors' loads before any arithmetic.
 // kCopy: also store the local unchanged into Lcopy (the peer-memory path's staging buffer).
-template <typename T, bool kWriteS, int U, int I, bool kCopy = false>
+template <typename T, bool kWriteS, int U, int I, bool kCopy = false, bool kEF = false>
 __global__ void __launch_bounds__(kThreads) pg_norm_kernel(const T* __restrict__ local,
                                                            const float* __restrict__ anchor,
                                                            float* __restrict__ S, int64_t n,
@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(kThreads) pg_norm_kernel(const T* __restrict__
                                                            T* __restrict__ Lcopy = nullptr) {
   const int64_t n8 = n >> 3;
   const int64_t cta0 = (int64_t)blockIdx.x * kThreads * U * I + threadIdx.x;
+  const uint64_t pol = kEF ? l2_evict_first_policy() : 0;
   float acc = 0.f;
 #pragma unroll 1
   for (int it = 0; it < I; ++it) {
@@ -46,15 +47,15 @@ __global__ void __launch_bounds__(kThreads) pg_norm_kernel(const T* __restrict__
     for (int u = 0; u < U; ++u) {
       const int64_t i = base + (int64_t)u * kThreads;
       if (i < n8) {
-        load8(local + 8 * i, l[u]);
-        load8(anchor + 8 * i, a[u]);
+        load8<kEF>(local + 8 * i, l[u], pol);
+        load8<kEF>(anchor + 8 * i, a[u], pol);
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = base + (int64_t)u * kThreads;
       if (i < n8) {
-        if (kCopy) store8(Lcopy + 8 * i, l[u]);  // exact: bf16 -> f32 -> bf16 round-trips
+        if (kCopy) store8<kEF>(Lcopy + 8 * i, l[u], pol);  // exact: bf16 -> f32 -> bf16 round-trips
         float d[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(kThreads) pg_norm_kernel(const T* __restrict__
         if (kWriteS) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) d[j] = isfinite(d[j]) ? d[j] : 0.f;  // R9: w = 0 must give 0
-          store8(S + 8 * i, d);
+          store8<kEF>(S + 8 * i, d, pol);
         }
       }
     }
@@ -84,12 +85,13 @@ __global__ void __launch_bounds__(kThreads) pg_norm_kernel(const T* __restrict__
 
 // ---------------------------------------------------------------- K3
 // Eq. 4: partial ||Dbar||^2 of this shard of the all-reduced pseudo-gradient.
-template <int U, int I>
+template <int U, int I, bool kEF = false>
 __global__ void __launch_bounds__(kThreads) sumsq_kernel(const float* __restrict__ x, int64_t n,
                                                          LayerScratch* __restrict__ scr,
                                                          double* __restrict__ cta_parts) {
   const int64_t n8 = n >> 3;
   const int64_t cta0 = (int64_t)blockIdx.x * kThreads * U * I + threadIdx.x;
+  const uint64_t pol = kEF ? l2_evict_first_policy() : 0;
   float acc = 0.f;
 #pragma unroll 1
   for (int it = 0; it < I; ++it) {
@@ -98,7 +100,7 @@ __global__ void __launch_bounds__(kThreads) sumsq_kernel(const float* __restrict
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = base + (int64_t)u * kThreads;
-      if (i < n8) load8(x + 8 * i, v[u]);
+      if (i < n8) load8<kEF>(x + 8 * i, v[u], pol);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -192,7 +194,7 @@ __global__ void decide_kernel(DecideArgs p) {
 // ---------------------------------------------------------------- K4
 // beta (Eq. 4), then OuterOpt = Nesterov (R2) on (anchor, momentum) and the
 // write-back local = rne(anchor) (Alg. 2 l.454-455).  Rollback: local = rne(anchor).
-template <typename T, bool kFromS, int U, int I>
+template <typename T, bool kFromS, int U, int I, bool kEF = false>
 __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
   T* __restrict__ local = static_cast<T*>(p.local);
   float* __restrict__ anchor = p.anchor;
@@ -219,6 +221,7 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
   }
   __syncthreads();
   const float beta = s_beta, mu = p.mu, nu = p.nu;
+  const uint64_t pol = kEF ? l2_evict_first_policy() : 0;
   const int64_t n8 = p.n >> 3;
   // CTAs walk the unit from its END: the producer pass right before (K1 at N == 1, K3 at
   // N > 1) streamed it forward, so its last ~100 MB are still in the 126 MB L2.
@@ -233,8 +236,8 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
         const int64_t i = cta0 + (int64_t)(it * U + u) * kThreads;
         if (i < n8) {
           float a[8];
-          load8(anchor + 8 * i, a);
-          store8(local + 8 * i, a);
+          load8<kEF>(anchor + 8 * i, a, pol);
+          store8<kEF>(local + 8 * i, a, pol);
         }
       }
     if (tail) {
@@ -252,12 +255,12 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
       const int64_t i = base + (int64_t)u * kThreads;
       if (i < n8) {
         if (kFromS) {
-          load8(dbar + 8 * i, d[u]);
+          load8<kEF>(dbar + 8 * i, d[u], pol);
         } else {
-          load8(local + 8 * i, d[u]);  // the local; Delta formed below
+          load8<kEF>(local + 8 * i, d[u], pol);  // the local; Delta formed below
         }
-        load8(anchor + 8 * i, a[u]);
-        load8(mom + 8 * i, m[u]);
+        load8<kEF>(anchor + 8 * i, a[u], pol);
+        load8<kEF>(mom + 8 * i, m[u], pol);
       }
     }
 #pragma unroll
@@ -271,9 +274,9 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
           m[u][j] = fmaf(mu, m[u][j], g);               // m' = mu m + g
           a[u][j] = a[u][j] - nu * fmaf(mu, m[u][j], g);  // a' = a - nu (g + mu m')
         }
-        store8(mom + 8 * i, m[u]);
-        store8(anchor + 8 * i, a[u]);
-        store8(local + 8 * i, a[u]);
+        store8<kEF>(mom + 8 * i, m[u], pol);
+        store8<kEF>(anchor + 8 * i, a[u], pol);
+        store8<kEF>(local + 8 * i, a[u], pol);
       }
     }
   }
@@ -292,42 +295,46 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
-// Production shapes (profiles/r1_k4_variants_microbench.txt, tools/kbench.cu).
+// Production shapes (profiles/r1_kbench_shapes.txt, tools/kbench.cu).
 constexpr int kRedU = kReduceShape[0], kRedI = kReduceShape[1];
 constexpr int kUpdU = kUpdateShape[0], kUpdI = kUpdateShape[1];
 
+template <typename T, bool kWriteS, bool kCopy>
+void pg_norm_ef(bool ef, unsigned grid, cudaStream_t st, const void* local, const float* anchor, float* S, int64_t n,
+                LayerScratch* scr, double* cta_parts, void* Lcopy) {
+  if (ef)
+    pg_norm_kernel<T, kWriteS, kRedU, kRedI, kCopy, true><<<grid, kThreads, 0, st>>>(
+        static_cast<const T*>(local), anchor, S, n, scr, cta_parts, static_cast<T*>(Lcopy));
+  else
+    pg_norm_kernel<T, kWriteS, kRedU, kRedI, kCopy, false><<<grid, kThreads, 0, st>>>(
+        static_cast<const T*>(local), anchor, S, n, scr, cta_parts, static_cast<T*>(Lcopy));
+}
+
 int launch_pg_norm(int dtype, const void* local, const float* anchor, float* S, int64_t n,
-                   LayerScratch* scr, double* cta_parts, cudaStream_t st) {
+                   LayerScratch* scr, double* cta_parts, bool ef, cudaStream_t st) {
   const unsigned grid = (unsigned)grid_of(n, kRedU * kRedI);
   if (dtype == EDIT_BF16) {
-    if (S) pg_norm_kernel<__nv_bfloat16, true, kRedU, kRedI><<<grid, kThreads, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(local), anchor, S, n, scr, cta_parts);
-    else pg_norm_kernel<__nv_bfloat16, false, kRedU, kRedI><<<grid, kThreads, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(local), anchor, S, n, scr, cta_parts);
+    if (S) pg_norm_ef<__nv_bfloat16, true, false>(ef, grid, st, local, anchor, S, n, scr, cta_parts, nullptr);
+    else pg_norm_ef<__nv_bfloat16, false, false>(ef, grid, st, local, anchor, S, n, scr, cta_parts, nullptr);
   } else {
-    if (S) pg_norm_kernel<float, true, kRedU, kRedI><<<grid, kThreads, 0, st>>>(
-        static_cast<const float*>(local), anchor, S, n, scr, cta_parts);
-    else pg_norm_kernel<float, false, kRedU, kRedI><<<grid, kThreads, 0, st>>>(
-        static_cast<const float*>(local), anchor, S, n, scr, cta_parts);
+    if (S) pg_norm_ef<float, true, false>(ef, grid, st, local, anchor, S, n, scr, cta_parts, nullptr);
+    else pg_norm_ef<float, false, false>(ef, grid, st, local, anchor, S, n, scr, cta_parts, nullptr);
   }
   return 1;
 }
 
-int launch_sumsq(const float* x, int64_t n, LayerScratch* scr, double* cta_parts, cudaStream_t st) {
-  sumsq_kernel<kRedU, kRedI><<<(unsigned)grid_of(n, kRedU * kRedI), kThreads, 0, st>>>(x, n, scr, cta_parts);
+int launch_pg_norm_copy(int dtype, const void* local, const float* anchor, void* Lcopy, int64_t n,
+                        LayerScratch* scr, double* cta_parts, bool ef, cudaStream_t st) {
+  const unsigned grid = (unsigned)grid_of(n, kRedU * kRedI);
+  if (dtype == EDIT_BF16) pg_norm_ef<__nv_bfloat16, false, true>(ef, grid, st, local, anchor, nullptr, n, scr, cta_parts, Lcopy);
+  else pg_norm_ef<float, false, true>(ef, grid, st, local, anchor, nullptr, n, scr, cta_parts, Lcopy);
   return 1;
 }
 
-int launch_pg_norm_copy(int dtype, const void* local, const float* anchor, void* Lcopy, int64_t n,
-                        LayerScratch* scr, double* cta_parts, cudaStream_t st) {
+int launch_sumsq(const float* x, int64_t n, LayerScratch* scr, double* cta_parts, bool ef, cudaStream_t st) {
   const unsigned grid = (unsigned)grid_of(n, kRedU * kRedI);
-  if (dtype == EDIT_BF16)
-    pg_norm_kernel<__nv_bfloat16, false, kRedU, kRedI, true><<<grid, kThreads, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(local), anchor, nullptr, n, scr, cta_parts,
-        static_cast<__nv_bfloat16*>(Lcopy));
-  else
-    pg_norm_kernel<float, false, kRedU, kRedI, true><<<grid, kThreads, 0, st>>>(
-        static_cast<const float*>(local), anchor, nullptr, n, scr, cta_parts, static_cast<float*>(Lcopy));
+  if (ef) sumsq_kernel<kRedU, kRedI, true><<<grid, kThreads, 0, st>>>(x, n, scr, cta_parts);
+  else sumsq_kernel<kRedU, kRedI, false><<<grid, kThreads, 0, st>>>(x, n, scr, cta_parts);
   return 1;
 }
 
@@ -336,14 +343,20 @@ int launch_decide(const DecideArgs& a, cudaStream_t st) {
   return 1;
 }
 
-int launch_update(int dtype, const UpdateArgs& a, cudaStream_t st) {
+template <typename T, bool kFromS>
+void update_ef(bool ef, unsigned grid, cudaStream_t st, const UpdateArgs& a) {
+  if (ef) outer_update_kernel<T, kFromS, kUpdU, kUpdI, true><<<grid, kThreads, 0, st>>>(a);
+  else outer_update_kernel<T, kFromS, kUpdU, kUpdI, false><<<grid, kThreads, 0, st>>>(a);
+}
+
+int launch_update(int dtype, const UpdateArgs& a, bool ef, cudaStream_t st) {
   const unsigned grid = (unsigned)grid_of(a.n, kUpdU * kUpdI);
   if (dtype == EDIT_BF16) {
-    if (a.dbar) outer_update_kernel<__nv_bfloat16, true, kUpdU, kUpdI><<<grid, kThreads, 0, st>>>(a);
-    else outer_update_kernel<__nv_bfloat16, false, kUpdU, kUpdI><<<grid, kThreads, 0, st>>>(a);
+    if (a.dbar) update_ef<__nv_bfloat16, true>(ef, grid, st, a);
+    else update_ef<__nv_bfloat16, false>(ef, grid, st, a);
   } else {
-    if (a.dbar) outer_update_kernel<float, true, kUpdU, kUpdI><<<grid, kThreads, 0, st>>>(a);
-    else outer_update_kernel<float, false, kUpdU, kUpdI><<<grid, kThreads, 0, st>>>(a);
+    if (a.dbar) update_ef<float, true>(ef, grid, st, a);
+    else update_ef<float, false>(ef, grid, st, a);
   }
   return 1;
 }

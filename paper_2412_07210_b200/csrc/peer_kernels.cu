@@ -51,7 +51,7 @@ __device__ __forceinline__ void ring_init(RingBars* b, int K) {
 }
 
 // ------------------------------------------------------------------------------ RS
-template <typename T>
+template <typename T, bool kEF>
 __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_constant__ PeerPtrs pp, Slicing sl,
                                                               const float* __restrict__ anchor,
                                                               float* __restrict__ Dmine,
@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_const
   }
   const int lbytes = (int)sizeof(T);
   const bool skip = scr->rollback != 0;
+  const uint64_t pol = kEF ? l2_evict_first_policy() : 0;
   const int64_t n8 = sl.n >> 3;
   const int64_t s0 = (int64_t)sl.me * sl.slice;                       // first vector of my slice
   const int64_t s1 = min(s0 + sl.slice, n8);                           // end (full vectors only)
@@ -90,11 +91,11 @@ __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_const
           const int nv = (int)min((int64_t)V, s1 - v0);
           char* st = smem + (size_t)s * stage_bytes;
           mbar_arrive_expect_tx(&bars.full[s], (uint32_t)(nv * 8 * (4 + nact * lbytes)));
-          tma_load_1d(st, anchor + 8 * v0, nv * 32, &bars.full[s]);
+          tma_load_1d<kEF>(st, anchor + 8 * v0, nv * 32, &bars.full[s], pol);
           for (int j = 0; j < N; ++j) {
             if (w[j] == 0.f) continue;
-            tma_load_1d(st + V * 32 + j * V * 8 * lbytes, static_cast<const T*>(pp.L[j]) + 8 * v0,
-                        (uint32_t)(nv * 8 * lbytes), &bars.full[s]);
+            tma_load_1d<kEF>(st + V * 32 + j * V * 8 * lbytes, static_cast<const T*>(pp.L[j]) + 8 * v0,
+                             (uint32_t)(nv * 8 * lbytes), &bars.full[s], pol);
           }
         }
       }
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_const
           }
 #pragma unroll
           for (int k = 0; k < 8; ++k) acc = fmaf(d[k], d[k], acc);
-          store8(Dmine + 8 * (v0 - s0 + v), d);
+          store8<kEF>(Dmine + 8 * (v0 - s0 + v), d, pol);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.empty[s]);
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_const
 }
 
 // ------------------------------------------------------------------------------ AG + update
-template <typename T>
+template <typename T, bool kEF>
 __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs p,
                                                                      const __grid_constant__ PeerPtrs pp,
                                                                      Slicing sl, int K) {
@@ -178,6 +179,7 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
   }
   ring_init(&bars, K);  // (contains __syncthreads)
   const float beta = s_beta, mu = p.mu, nu = p.nu;
+  const uint64_t pol = kEF ? l2_evict_first_policy() : 0;
   const int64_t n8 = p.n >> 3;
   const int N = sl.N;
   const int64_t tps = sl.slice / V;                      // tiles per slice (slices are tile-aligned)
@@ -195,8 +197,8 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += stride) {
       float a[8];
-      load8(anchor + 8 * i, a);
-      store8(local + 8 * i, a);
+      load8<kEF>(anchor + 8 * i, a, pol);
+      store8<kEF>(local + 8 * i, a, pol);
     }
     if (blockIdx.x == 0 && threadIdx.x < (p.n & 7)) {
       const int64_t k = 8 * n8 + threadIdx.x;
@@ -216,9 +218,9 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
         if (use > 0) mbar_wait(&bars.empty[s], (use - 1) & 1);
         char* st = smem + (size_t)s * stage_bytes;
         mbar_arrive_expect_tx(&bars.full[s], (uint32_t)(nv * 96));
-        tma_load_1d(st, pp.D[owner] + 8 * (v0 - owner * sl.slice), nv * 32, &bars.full[s]);
-        tma_load_1d(st + V * 32, anchor + 8 * v0, nv * 32, &bars.full[s]);
-        tma_load_1d(st + V * 64, mom + 8 * v0, nv * 32, &bars.full[s]);
+        tma_load_1d<kEF>(st, pp.D[owner] + 8 * (v0 - owner * sl.slice), nv * 32, &bars.full[s], pol);
+        tma_load_1d<kEF>(st + V * 32, anchor + 8 * v0, nv * 32, &bars.full[s], pol);
+        tma_load_1d<kEF>(st + V * 64, mom + 8 * v0, nv * 32, &bars.full[s], pol);
         ++it;
       }
     }
@@ -245,9 +247,9 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
           a[k] = a[k] - nu * fmaf(mu, m[k], g);    // a' = a - nu (g + mu m')
         }
         const int64_t i = v0 + v;
-        store8(mom + 8 * i, m);
-        store8(anchor + 8 * i, a);
-        store8(local + 8 * i, a);
+        store8<kEF>(mom + 8 * i, m, pol);
+        store8<kEF>(anchor + 8 * i, a, pol);
+        store8<kEF>(local + 8 * i, a, pol);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.empty[s]);
@@ -287,8 +289,15 @@ int stages_for(KernelT kernel, int stage_bytes) {
 
 }  // namespace
 
+template <typename T, bool kEF>
+void rs_go(unsigned grid, int stage_bytes, cudaStream_t st, const PeerPtrs& pp, const Slicing& sl, const float* anchor,
+           float* Dmine, LayerScratch* scr, double* cta_parts) {
+  const int K = stages_for(rs_tma_kernel<T, kEF>, stage_bytes);
+  rs_tma_kernel<T, kEF><<<grid, kPeerThreads, K * stage_bytes, st>>>(pp, sl, anchor, Dmine, scr, cta_parts, K);
+}
+
 int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anchor, float* Dmine,
-              LayerScratch* scr, double* cta_parts, int max_ctas, cudaStream_t st) {
+              LayerScratch* scr, double* cta_parts, int max_ctas, bool ef, cudaStream_t st) {
   const int64_t n8 = sl.n >> 3;
   const int64_t s0 = (int64_t)sl.me * sl.slice;
   const int64_t s1 = n8 < s0 + sl.slice ? n8 : s0 + sl.slice;
@@ -297,27 +306,33 @@ int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anc
   const int esz = dtype == EDIT_BF16 ? 2 : 4;
   const int stage_bytes = sl.tile * 8 * (4 + sl.N * esz);
   if (dtype == EDIT_BF16) {
-    const int K = stages_for(rs_tma_kernel<__nv_bfloat16>, stage_bytes);
-    rs_tma_kernel<__nv_bfloat16><<<grid, kPeerThreads, K * stage_bytes, st>>>(pp, sl, anchor, Dmine, scr,
-                                                                              cta_parts, K);
+    if (ef) rs_go<__nv_bfloat16, true>(grid, stage_bytes, st, pp, sl, anchor, Dmine, scr, cta_parts);
+    else rs_go<__nv_bfloat16, false>(grid, stage_bytes, st, pp, sl, anchor, Dmine, scr, cta_parts);
   } else {
-    const int K = stages_for(rs_tma_kernel<float>, stage_bytes);
-    rs_tma_kernel<float><<<grid, kPeerThreads, K * stage_bytes, st>>>(pp, sl, anchor, Dmine, scr, cta_parts, K);
+    if (ef) rs_go<float, true>(grid, stage_bytes, st, pp, sl, anchor, Dmine, scr, cta_parts);
+    else rs_go<float, false>(grid, stage_bytes, st, pp, sl, anchor, Dmine, scr, cta_parts);
   }
   return 1;
 }
 
+template <typename T, bool kEF>
+void ag_go(unsigned grid, int stage_bytes, cudaStream_t st, const UpdateArgs& a, const PeerPtrs& pp,
+           const Slicing& sl) {
+  const int K = stages_for(ag_update_tma_kernel<T, kEF>, stage_bytes);
+  ag_update_tma_kernel<T, kEF><<<grid, kPeerThreads, K * stage_bytes, st>>>(a, pp, sl, K);
+}
+
 int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl, int max_ctas,
-                     cudaStream_t st) {
+                     bool ef, cudaStream_t st) {
   const int64_t nq = (int64_t)sl.N * (sl.slice / sl.tile);
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nq, max_ctas));
   const int stage_bytes = sl.tile * 8 * 12;
   if (dtype == EDIT_BF16) {
-    const int K = stages_for(ag_update_tma_kernel<__nv_bfloat16>, stage_bytes);
-    ag_update_tma_kernel<__nv_bfloat16><<<grid, kPeerThreads, K * stage_bytes, st>>>(a, pp, sl, K);
+    if (ef) ag_go<__nv_bfloat16, true>(grid, stage_bytes, st, a, pp, sl);
+    else ag_go<__nv_bfloat16, false>(grid, stage_bytes, st, a, pp, sl);
   } else {
-    const int K = stages_for(ag_update_tma_kernel<float>, stage_bytes);
-    ag_update_tma_kernel<float><<<grid, kPeerThreads, K * stage_bytes, st>>>(a, pp, sl, K);
+    if (ef) ag_go<float, true>(grid, stage_bytes, st, a, pp, sl);
+    else ag_go<float, false>(grid, stage_bytes, st, a, pp, sl);
   }
   return 1;
 }

@@ -106,5 +106,17 @@ int main(int argc, char** argv) {
   K3(2, 1) K3(2, 2) K3(4, 1) K3(4, 2) K3(2, 4)
   K4(1, 1, false) K4(2, 1, false) K4(1, 2, false) K4(2, 2, false) K4(1, 4, false) K4(4, 1, false)
   K4(1, 1, true) K4(2, 1, true) K4(1, 2, true)
+  {  // L2 evict_first streaming variants of the production shapes
+    UpdateArgs a{};
+    a.local = local; a.anchor = anchor; a.momentum = mom; a.dbar = nullptr; a.n = n;
+    a.gparts = gparts; a.n_gparts = 1; a.rollback = rb; a.nu = 0.8f; a.mu = 0.85f; a.phi = 10.0;
+    a.eps = 1e-6; a.flags = 0; a.rec = rec;
+    unsigned g = (unsigned)grid_of(n, 1);
+    float ms = time_it([&] { outer_update_kernel<__nv_bfloat16, false, 1, 1, true><<<g, kThreads>>>(a); }, reps);
+    printf("K4 update bf16 EF U=1 I=1: %.1f us %.0f GB/s\n", ms * 1e3, 20.0 * n / ms / 1e6);
+    unsigned g1 = (unsigned)grid_of(n, 8);
+    float ms1 = time_it([&] { pg_norm_kernel<__nv_bfloat16, false, 2, 4, false, true><<<g1, kThreads>>>(local, anchor, nullptr, n, scr, parts); }, reps);
+    printf("K1 pg_norm bf16 EF U=2 I=4: %.1f us %.0f GB/s\n", ms1 * 1e3, 6.0 * n / ms1 / 1e6);
+  }
   return 0;
 }

@@ -29,7 +29,8 @@ def key_of(name: str) -> str:
     base = m.group(1).replace("_kernel", "")
     args = m.group(2)
     dt = "bf16" if "bfloat16" in args else ("f32" if "float" in args else "")
-    flag = args.split(",")[-1].strip() if "," in args else ""
+    parts = [a.strip() for a in args.split(",")]
+    flag = parts[1] if len(parts) > 1 else ""
     if base == "outer_update":
         return f"outer_update_{dt}_{'S' if flag in ('1', 'true') else 'local'}"
     if base == "pg_norm":
