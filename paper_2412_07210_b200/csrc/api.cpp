@@ -138,6 +138,10 @@ struct edit_sync {
   int peer_tile = kPeerTileVec;  // vectors per TMA tile (EDIT_PEER_TILE env; must match on all ranks)
   bool ef_direct = false;        // L2 evict_first streaming for edit_layer_sync / edit_sync_round
   bool ef_sched = true;          // ... for the prefetch scheduler (a forward runs concurrently)
+  // scheduler (co-resident) mode: at most sched_ctas CTAs per streaming kernel, each small
+  // enough (registers, shared memory) to sit next to a GEMM CTA on an SM (EDIT_SCHED_CTAS)
+  int sched_ctas = 148;
+  int sched_smem_kb = 18;
   bool ready = false;            // init completed (destroy may then barrier with the peers)
   char* ws = nullptr;
   LayerScratch* scratch = nullptr;
@@ -266,6 +270,15 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
     if (!strcmp(e, "1")) h->ef_direct = h->ef_sched = true;
     else if (!strcmp(e, "0")) h->ef_direct = h->ef_sched = false;
   }
+  h->sched_ctas = h->num_sms;
+  if (const char* e = getenv("EDIT_SCHED_CTAS")) {  // 0 = full grids also in scheduler rounds
+    const int v = atoi(e);
+    if (v >= 0) h->sched_ctas = std::min(v, kMaxPeerCtas);
+  }
+  if (const char* e = getenv("EDIT_SCHED_SMEM_KB")) {
+    const int v = atoi(e);
+    if (v > 0) h->sched_smem_kb = v;
+  }
   if (const char* e = getenv("EDIT_PEER_CTAS")) {
     const int v = atoi(e);
     if (v > 0) h->peer_ctas = std::min(v, kMaxPeerCtas);
@@ -379,8 +392,16 @@ static edit_status_t check_unit_args(edit_sync_t h, int32_t layer, const void* l
 }
 
 // Enqueue Sync() of one unit on stream `st` using lane `ln`'s communicators and buffers.
+struct Mode {
+  bool ef;        // L2 evict_first streaming
+  int cap;        // max CTAs of the LDG streaming kernels (0 = full grid)
+  int peer_ctas;  // persistent grid of the TMA peer kernels
+  int smem_kb;    // shared-memory ring of the TMA peer kernels (0 = default)
+};
+
 static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* local, float* anchor, float* momentum,
-                               cudaStream_t st, bool ef) {
+                               cudaStream_t st, const Mode& mode) {
+  const bool ef = mode.ef;
   const int64_t n = h->numel[layer];
   const int dt = h->cfg.param_dtype;
   LayerScratch* scr = &h->scratch[layer];
@@ -393,9 +414,9 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
   // K1: Delta and its shard norm (Alg. 2 l.442-443)
   float* S = (N > 1 && !h->peer) ? ln.S : nullptr;
   if (h->peer)
-    launched += launch_pg_norm_copy(dt, local, anchor, ln.Lown, n, scr, h->part1[layer], ef, st);
+    launched += launch_pg_norm_copy(dt, local, anchor, ln.Lown, n, scr, h->part1[layer], ef, mode.cap, st);
   else
-    launched += launch_pg_norm(dt, local, anchor, S, n, scr, h->part1[layer], ef, st);
+    launched += launch_pg_norm(dt, local, anchor, S, n, scr, h->part1[layer], ef, mode.cap, st);
   CUDA_TRY(h, cudaGetLastError());
   if (ev) CUDA_TRY(h, cudaEventRecord(ev[1], st));
   // module norms of every replica on every rank: one K-scalar gather (R6)
@@ -438,7 +459,7 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
   if (h->peer) {
     // Eq. 3 as a reduce-scatter over NVLink peer memory: this rank's slice of Dbar
     const Slicing sl = slicing_of(n, N, h->sync_idx, h->peer_tile);
-    launched += launch_rs(dt, ln.pp, sl, anchor, ln.Down, scr, h->part2[layer], h->peer_ctas, ef, st);
+    launched += launch_rs(dt, ln.pp, sl, anchor, ln.Down, scr, h->part2[layer], mode.peer_ctas, ef, mode.smem_kb, st);
     CUDA_TRY(h, cudaGetLastError());
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
     // ||Dbar||^2 of the module = sum over every slice of every shard: one K-scalar gather
@@ -447,12 +468,12 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[4], st));
     u.gparts = scr->recv2;
     u.n_gparts = h->K;
-    launched += launch_ag_update(dt, u, ln.pp, sl, h->peer_ctas, ef, st);
+    launched += launch_ag_update(dt, u, ln.pp, sl, mode.peer_ctas, ef, mode.smem_kb, st);
   } else if (N > 1) {
     // Eq. 3: Dbar = sum_n w_n Delta_n, the weight applied inside NCCL (PreMulSum)
     NCCL_TRY(h, ncclAllReduce(S, S, (size_t)n, ncclFloat32, ln.ops[layer], ln.sync, st));
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
-    launched += launch_sumsq(S, n, scr, h->part2[layer], ef, st);
+    launched += launch_sumsq(S, n, scr, h->part2[layer], ef, mode.cap, st);
     CUDA_TRY(h, cudaGetLastError());
     if (M > 1) {
       NCCL_TRY(h, ncclAllGather(&scr->send2, scr->recv2, 1, ncclFloat64, ln.shard, st));
@@ -469,7 +490,7 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
     u.gparts = &scr->gsq;
     u.n_gparts = 1;
   }
-  if (!h->peer) launched += launch_update(dt, u, ef, st);
+  if (!h->peer) launched += launch_update(dt, u, ef, mode.cap, st);
   CUDA_TRY(h, cudaGetLastError());
   if (ev) {
     CUDA_TRY(h, cudaEventRecord(ev[5], st));
@@ -484,7 +505,8 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
                               void* stream) {
   edit_status_t rc = check_unit_args(h, layer, local, anchor, momentum);
   if (rc != EDIT_OK) return rc;
-  return sync_unit(h, h->lanes[0], layer, local, anchor, momentum, static_cast<cudaStream_t>(stream), h->ef_direct);
+  return sync_unit(h, h->lanes[0], layer, local, anchor, momentum, static_cast<cudaStream_t>(stream),
+                   Mode{h->ef_direct, 0, h->peer_ctas, 0});
 }
 
 edit_status_t edit_sync_round(edit_sync_t h, void* const* locals, float* const* anchors, float* const* momenta,
@@ -505,7 +527,8 @@ edit_status_t edit_sync_round(edit_sync_t h, void* const* locals, float* const* 
   for (Lane& ln : h->lanes) CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->fork, 0));
   for (int u = 0; u < L; ++u) {
     Lane& ln = h->lanes[u % nl];
-    edit_status_t rc = sync_unit(h, ln, u, locals[u], anchors[u], momenta[u], ln.stream, h->ef_direct);
+    edit_status_t rc = sync_unit(h, ln, u, locals[u], anchors[u], momenta[u], ln.stream,
+                                 Mode{h->ef_direct, 0, h->peer_ctas, 0});
     if (rc != EDIT_OK) return rc;
   }
   for (Lane& ln : h->lanes) {
@@ -578,7 +601,9 @@ edit_status_t edit_sync_host_wait(edit_sync_t h, void* stream) {
 static edit_status_t sched_enqueue_next(edit_sync_t h) {
   const int u = h->sched_next_sync++;
   Lane& ln = h->lanes[u % h->lanes.size()];
-  return sync_unit(h, ln, u, h->sched_local[u], h->sched_anchor[u], h->sched_mom[u], ln.stream, h->ef_sched);
+  return sync_unit(h, ln, u, h->sched_local[u], h->sched_anchor[u], h->sched_mom[u], ln.stream,
+                   Mode{h->ef_sched, h->sched_ctas, h->sched_ctas > 0 ? h->sched_ctas : h->peer_ctas,
+                        h->sched_ctas > 0 ? h->sched_smem_kb : 0});
 }
 
 edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* const* anchors,

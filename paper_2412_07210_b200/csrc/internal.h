@@ -103,22 +103,25 @@ inline Slicing slicing_of(int64_t n, int N, int me, int tile = kPeerTileVec) {
 
 // Launchers (kernels.cu).  Each returns the number of kernels launched.
 // cta_parts: grid_of(n, kVecReduce) fp64 slots for the per-CTA partials.
-// ef: stream with an L2 evict_first policy (device_common.cuh).
+// ef: stream with an L2 evict_first policy (device_common.cuh).  cap > 0: at most `cap` CTAs
+// (grid-stride over chunks) -- the co-resident mode next to a forward's GEMMs.
 int launch_pg_norm(int dtype, const void* local, const float* anchor, float* S, int64_t n,
-                   LayerScratch* scr, double* cta_parts, bool ef, cudaStream_t st);
-int launch_sumsq(const float* x, int64_t n, LayerScratch* scr, double* cta_parts, bool ef, cudaStream_t st);
+                   LayerScratch* scr, double* cta_parts, bool ef, int cap, cudaStream_t st);
+int launch_sumsq(const float* x, int64_t n, LayerScratch* scr, double* cta_parts, bool ef, int cap,
+                 cudaStream_t st);
 int launch_decide(const DecideArgs& a, cudaStream_t st);
 // K1 variant for the peer-memory path: also copies the local into this rank's staging L.
 int launch_pg_norm_copy(int dtype, const void* local, const float* anchor, void* Lcopy, int64_t n,
-                        LayerScratch* scr, double* cta_parts, bool ef, cudaStream_t st);
+                        LayerScratch* scr, double* cta_parts, bool ef, int cap, cudaStream_t st);
 // RS (peer_kernels.cu): Dbar = sum_j w_j (anchor - L_j) over this rank's slice, written to its D;
 // ||Dbar_slice||^2 -> scr->send2 (persistent grid <= max_ctas; cta_parts needs that many slots).
+// smem_kb > 0: shared-memory ring budget per CTA (tiles shrink to fit; co-resident mode).
 int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anchor, float* Dmine,
-              LayerScratch* scr, double* cta_parts, int max_ctas, bool ef, cudaStream_t st);
+              LayerScratch* scr, double* cta_parts, int max_ctas, bool ef, int smem_kb, cudaStream_t st);
 // AG + update: Dbar pulled from each slice's owner, then the K4 math on the whole shard.
 int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl, int max_ctas,
-                     bool ef, cudaStream_t st);
+                     bool ef, int smem_kb, cudaStream_t st);
 inline int64_t rs_partial_slots(int64_t, int) { return kMaxPeerCtas; }
-int launch_update(int dtype, const UpdateArgs& a, bool ef, cudaStream_t st);
+int launch_update(int dtype, const UpdateArgs& a, bool ef, int cap, cudaStream_t st);
 
 }  // namespace edit

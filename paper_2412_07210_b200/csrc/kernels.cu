@@ -36,9 +36,13 @@ __global__ void __launch_bounds__(kThreads) pg_norm_kernel(const T* __restrict__
                                                            double* __restrict__ cta_parts,
                                                            T* __restrict__ Lcopy = nullptr) {
   const int64_t n8 = n >> 3;
-  const int64_t cta0 = (int64_t)blockIdx.x * kThreads * U * I + threadIdx.x;
+  const int64_t nchunks = (n8 + kThreads * U * I - 1) / (kThreads * U * I);
   const uint64_t pol = kEF ? l2_evict_first_policy() : 0;
   float acc = 0.f;
+  // one chunk per CTA with the full grid; grid-stride over chunks when the grid is capped
+  // (the scheduler's co-resident mode, 1 CTA per SM)
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+  const int64_t cta0 = c * kThreads * U * I + threadIdx.x;
 #pragma unroll 1
   for (int it = 0; it < I; ++it) {
     const int64_t base = cta0 + (int64_t)it * kThreads * U;
@@ -70,6 +74,7 @@ __global__ void __launch_bounds__(kThreads) pg_norm_kernel(const T* __restrict__
       }
     }
   }
+  }
   double accd = (double)acc;
   if (blockIdx.x == 0 && threadIdx.x < (n & 7)) {  // ragged tail (< 8 elements)
     const int64_t k = 8 * n8 + threadIdx.x;
@@ -90,9 +95,11 @@ __global__ void __launch_bounds__(kThreads) sumsq_kernel(const float* __restrict
                                                          LayerScratch* __restrict__ scr,
                                                          double* __restrict__ cta_parts) {
   const int64_t n8 = n >> 3;
-  const int64_t cta0 = (int64_t)blockIdx.x * kThreads * U * I + threadIdx.x;
+  const int64_t nchunks = (n8 + kThreads * U * I - 1) / (kThreads * U * I);
   const uint64_t pol = kEF ? l2_evict_first_policy() : 0;
   float acc = 0.f;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+  const int64_t cta0 = c * kThreads * U * I + threadIdx.x;
 #pragma unroll 1
   for (int it = 0; it < I; ++it) {
     const int64_t base = cta0 + (int64_t)it * kThreads * U;
@@ -110,6 +117,7 @@ __global__ void __launch_bounds__(kThreads) sumsq_kernel(const float* __restrict
         for (int j = 0; j < 8; ++j) acc = fmaf(v[u][j], v[u][j], acc);
       }
     }
+  }
   }
   double accd = (double)acc;
   if (blockIdx.x == 0 && threadIdx.x < (n & 7)) {
@@ -223,12 +231,11 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
   const float beta = s_beta, mu = p.mu, nu = p.nu;
   const uint64_t pol = kEF ? l2_evict_first_policy() : 0;
   const int64_t n8 = p.n >> 3;
-  // CTAs walk the unit from its END: the producer pass right before (K1 at N == 1, K3 at
-  // N > 1) streamed it forward, so its last ~100 MB are still in the 126 MB L2.
-  const int64_t chunk = (int64_t)gridDim.x - 1 - blockIdx.x;
-  const int64_t cta0 = chunk * kThreads * U * I + threadIdx.x;
-  const bool tail = chunk == (int64_t)gridDim.x - 1 && threadIdx.x < (p.n & 7);
+  const int64_t nchunks = (n8 + kThreads * U * I - 1) / (kThreads * U * I);
+  const bool tail = blockIdx.x == 0 && threadIdx.x < (p.n & 7);
   if (s_rollback) {  // Alg. 2 l.449: theta_{t+1,0} = theta_t (R14)
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const int64_t cta0 = c * kThreads * U * I + threadIdx.x;
 #pragma unroll 1
     for (int it = 0; it < I; ++it)
 #pragma unroll
@@ -240,12 +247,17 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
           store8<kEF>(local + 8 * i, a, pol);
         }
       }
+    }
     if (tail) {
       const int64_t k = 8 * n8 + threadIdx.x;
       store1(local + k, anchor[k]);
     }
     return;
   }
+  // chunks are walked from the unit's END: the producer pass right before (K1 at N == 1,
+  // K3 at N > 1) streamed it forward, so its last ~100 MB are still in the 126 MB L2
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+  const int64_t cta0 = (nchunks - 1 - c) * kThreads * U * I + threadIdx.x;
 #pragma unroll 1
   for (int it = 0; it < I; ++it) {
     const int64_t base = cta0 + (int64_t)it * kThreads * U;
@@ -280,6 +292,7 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
       }
     }
   }
+  }
   if (tail) {
     const int64_t k = 8 * n8 + threadIdx.x;
     const float d = kFromS ? dbar[k] : anchor[k] - load1(local + k);
@@ -310,9 +323,11 @@ void pg_norm_ef(bool ef, unsigned grid, cudaStream_t st, const void* local, cons
         static_cast<const T*>(local), anchor, S, n, scr, cta_parts, static_cast<T*>(Lcopy));
 }
 
+static unsigned capped(int64_t g, int cap) { return (unsigned)(cap > 0 && g > cap ? cap : g); }
+
 int launch_pg_norm(int dtype, const void* local, const float* anchor, float* S, int64_t n,
-                   LayerScratch* scr, double* cta_parts, bool ef, cudaStream_t st) {
-  const unsigned grid = (unsigned)grid_of(n, kRedU * kRedI);
+                   LayerScratch* scr, double* cta_parts, bool ef, int cap, cudaStream_t st) {
+  const unsigned grid = capped(grid_of(n, kRedU * kRedI), cap);
   if (dtype == EDIT_BF16) {
     if (S) pg_norm_ef<__nv_bfloat16, true, false>(ef, grid, st, local, anchor, S, n, scr, cta_parts, nullptr);
     else pg_norm_ef<__nv_bfloat16, false, false>(ef, grid, st, local, anchor, S, n, scr, cta_parts, nullptr);
@@ -324,15 +339,16 @@ int launch_pg_norm(int dtype, const void* local, const float* anchor, float* S, 
 }
 
 int launch_pg_norm_copy(int dtype, const void* local, const float* anchor, void* Lcopy, int64_t n,
-                        LayerScratch* scr, double* cta_parts, bool ef, cudaStream_t st) {
-  const unsigned grid = (unsigned)grid_of(n, kRedU * kRedI);
+                        LayerScratch* scr, double* cta_parts, bool ef, int cap, cudaStream_t st) {
+  const unsigned grid = capped(grid_of(n, kRedU * kRedI), cap);
   if (dtype == EDIT_BF16) pg_norm_ef<__nv_bfloat16, false, true>(ef, grid, st, local, anchor, nullptr, n, scr, cta_parts, Lcopy);
   else pg_norm_ef<float, false, true>(ef, grid, st, local, anchor, nullptr, n, scr, cta_parts, Lcopy);
   return 1;
 }
 
-int launch_sumsq(const float* x, int64_t n, LayerScratch* scr, double* cta_parts, bool ef, cudaStream_t st) {
-  const unsigned grid = (unsigned)grid_of(n, kRedU * kRedI);
+int launch_sumsq(const float* x, int64_t n, LayerScratch* scr, double* cta_parts, bool ef, int cap,
+                 cudaStream_t st) {
+  const unsigned grid = capped(grid_of(n, kRedU * kRedI), cap);
   if (ef) sumsq_kernel<kRedU, kRedI, true><<<grid, kThreads, 0, st>>>(x, n, scr, cta_parts);
   else sumsq_kernel<kRedU, kRedI, false><<<grid, kThreads, 0, st>>>(x, n, scr, cta_parts);
   return 1;
@@ -349,8 +365,8 @@ void update_ef(bool ef, unsigned grid, cudaStream_t st, const UpdateArgs& a) {
   else outer_update_kernel<T, kFromS, kUpdU, kUpdI, false><<<grid, kThreads, 0, st>>>(a);
 }
 
-int launch_update(int dtype, const UpdateArgs& a, bool ef, cudaStream_t st) {
-  const unsigned grid = (unsigned)grid_of(a.n, kUpdU * kUpdI);
+int launch_update(int dtype, const UpdateArgs& a, bool ef, int cap, cudaStream_t st) {
+  const unsigned grid = capped(grid_of(a.n, kUpdU * kUpdI), cap);
   if (dtype == EDIT_BF16) {
     if (a.dbar) update_ef<__nv_bfloat16, true>(ef, grid, st, a);
     else update_ef<__nv_bfloat16, false>(ef, grid, st, a);

@@ -56,10 +56,9 @@ __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_const
                                                               const float* __restrict__ anchor,
                                                               float* __restrict__ Dmine,
                                                               LayerScratch* __restrict__ scr,
-                                                              double* __restrict__ cta_parts, int K) {
+                                                              double* __restrict__ cta_parts, int K, int V) {
   extern __shared__ __align__(128) char smem[];
   __shared__ RingBars bars;
-  const int V = sl.tile;
   const int N = sl.N;
   float w[EDIT_MAX_SYNC];
   int nact = 0;
@@ -151,12 +150,11 @@ __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_const
 template <typename T, bool kEF>
 __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs p,
                                                                      const __grid_constant__ PeerPtrs pp,
-                                                                     Slicing sl, int K) {
+                                                                     Slicing sl, int K, int V) {
   extern __shared__ __align__(128) char smem[];
   __shared__ RingBars bars;
   __shared__ float s_beta;
   __shared__ int s_rollback;
-  const int V = sl.tile;
   T* __restrict__ local = static_cast<T*>(p.local);
   float* __restrict__ anchor = p.anchor;
   float* __restrict__ mom = p.momentum;
@@ -269,7 +267,7 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
   }
 }
 
-int smem_budget() {
+int default_smem_budget() {
   static int b = [] {
     const char* e = getenv("EDIT_PEER_SMEM_KB");  // shared-memory ring per CTA (default 200 KB)
     const int v = e ? atoi(e) : 0;
@@ -278,61 +276,73 @@ int smem_budget() {
   return b;
 }
 
+// Kernel tile V (vectors) and ring depth K for a shared-memory budget: the largest V that
+// divides the slicing tile and leaves >= 3 stages (V >= 32), K = as many stages as fit (<= 8).
+struct Ring {
+  int V, K, stage_bytes;
+};
+Ring ring_for(int tile, int bytes_per_vec, int smem_kb) {
+  const int budget = smem_kb > 0 ? smem_kb * 1024 : default_smem_budget();
+  int V = tile;
+  while (V > 32 && 3 * V * bytes_per_vec > budget) V /= 2;
+  Ring r;
+  r.V = V;
+  r.stage_bytes = V * bytes_per_vec;
+  r.K = std::max(2, std::min(kMaxStages, budget / r.stage_bytes));
+  return r;
+}
+
 template <typename KernelT>
-int stages_for(KernelT kernel, int stage_bytes) {
-  int K = smem_budget() / stage_bytes;
-  K = K > kMaxStages ? kMaxStages : K;
-  K = K < 2 ? 2 : K;
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, K * stage_bytes);
-  return K;
+void set_smem(KernelT kernel, int bytes) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 }  // namespace
 
 template <typename T, bool kEF>
-void rs_go(unsigned grid, int stage_bytes, cudaStream_t st, const PeerPtrs& pp, const Slicing& sl, const float* anchor,
+void rs_go(unsigned grid, const Ring& r, cudaStream_t st, const PeerPtrs& pp, const Slicing& sl, const float* anchor,
            float* Dmine, LayerScratch* scr, double* cta_parts) {
-  const int K = stages_for(rs_tma_kernel<T, kEF>, stage_bytes);
-  rs_tma_kernel<T, kEF><<<grid, kPeerThreads, K * stage_bytes, st>>>(pp, sl, anchor, Dmine, scr, cta_parts, K);
+  set_smem(rs_tma_kernel<T, kEF>, r.K * r.stage_bytes);
+  rs_tma_kernel<T, kEF><<<grid, kPeerThreads, r.K * r.stage_bytes, st>>>(pp, sl, anchor, Dmine, scr, cta_parts,
+                                                                          r.K, r.V);
 }
 
 int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anchor, float* Dmine,
-              LayerScratch* scr, double* cta_parts, int max_ctas, bool ef, cudaStream_t st) {
+              LayerScratch* scr, double* cta_parts, int max_ctas, bool ef, int smem_kb, cudaStream_t st) {
+  const int esz = dtype == EDIT_BF16 ? 2 : 4;
+  const Ring r = ring_for(sl.tile, 8 * (4 + sl.N * esz), smem_kb);
   const int64_t n8 = sl.n >> 3;
   const int64_t s0 = (int64_t)sl.me * sl.slice;
   const int64_t s1 = n8 < s0 + sl.slice ? n8 : s0 + sl.slice;
-  const int64_t ntiles = s1 > s0 ? (s1 - s0 + sl.tile - 1) / sl.tile : 0;
+  const int64_t ntiles = s1 > s0 ? (s1 - s0 + r.V - 1) / r.V : 0;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, max_ctas));
-  const int esz = dtype == EDIT_BF16 ? 2 : 4;
-  const int stage_bytes = sl.tile * 8 * (4 + sl.N * esz);
   if (dtype == EDIT_BF16) {
-    if (ef) rs_go<__nv_bfloat16, true>(grid, stage_bytes, st, pp, sl, anchor, Dmine, scr, cta_parts);
-    else rs_go<__nv_bfloat16, false>(grid, stage_bytes, st, pp, sl, anchor, Dmine, scr, cta_parts);
+    if (ef) rs_go<__nv_bfloat16, true>(grid, r, st, pp, sl, anchor, Dmine, scr, cta_parts);
+    else rs_go<__nv_bfloat16, false>(grid, r, st, pp, sl, anchor, Dmine, scr, cta_parts);
   } else {
-    if (ef) rs_go<float, true>(grid, stage_bytes, st, pp, sl, anchor, Dmine, scr, cta_parts);
-    else rs_go<float, false>(grid, stage_bytes, st, pp, sl, anchor, Dmine, scr, cta_parts);
+    if (ef) rs_go<float, true>(grid, r, st, pp, sl, anchor, Dmine, scr, cta_parts);
+    else rs_go<float, false>(grid, r, st, pp, sl, anchor, Dmine, scr, cta_parts);
   }
   return 1;
 }
 
 template <typename T, bool kEF>
-void ag_go(unsigned grid, int stage_bytes, cudaStream_t st, const UpdateArgs& a, const PeerPtrs& pp,
-           const Slicing& sl) {
-  const int K = stages_for(ag_update_tma_kernel<T, kEF>, stage_bytes);
-  ag_update_tma_kernel<T, kEF><<<grid, kPeerThreads, K * stage_bytes, st>>>(a, pp, sl, K);
+void ag_go(unsigned grid, const Ring& r, cudaStream_t st, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl) {
+  set_smem(ag_update_tma_kernel<T, kEF>, r.K * r.stage_bytes);
+  ag_update_tma_kernel<T, kEF><<<grid, kPeerThreads, r.K * r.stage_bytes, st>>>(a, pp, sl, r.K, r.V);
 }
 
 int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl, int max_ctas,
-                     bool ef, cudaStream_t st) {
-  const int64_t nq = (int64_t)sl.N * (sl.slice / sl.tile);
+                     bool ef, int smem_kb, cudaStream_t st) {
+  const Ring r = ring_for(sl.tile, 8 * 12, smem_kb);
+  const int64_t nq = (int64_t)sl.N * (sl.slice / r.V);
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nq, max_ctas));
-  const int stage_bytes = sl.tile * 8 * 12;
   if (dtype == EDIT_BF16) {
-    if (ef) ag_go<__nv_bfloat16, true>(grid, stage_bytes, st, a, pp, sl);
-    else ag_go<__nv_bfloat16, false>(grid, stage_bytes, st, a, pp, sl);
+    if (ef) ag_go<__nv_bfloat16, true>(grid, r, st, a, pp, sl);
+    else ag_go<__nv_bfloat16, false>(grid, r, st, a, pp, sl);
   } else {
-    if (ef) ag_go<float, true>(grid, stage_bytes, st, a, pp, sl);
-    else ag_go<float, false>(grid, stage_bytes, st, a, pp, sl);
+    if (ef) ag_go<float, true>(grid, r, st, a, pp, sl);
+    else ag_go<float, false>(grid, r, st, a, pp, sl);
   }
   return 1;
 }
