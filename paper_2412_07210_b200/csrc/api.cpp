@@ -137,10 +137,11 @@ struct edit_sync {
   int peer_ctas = 148;           // persistent grid of the peer kernels (EDIT_PEER_CTAS env overrides)
   int peer_tile = kPeerTileVec;  // vectors per TMA tile (EDIT_PEER_TILE env; must match on all ranks)
   bool ef_direct = false;        // L2 evict_first streaming for edit_layer_sync / edit_sync_round
-  bool ef_sched = true;          // ... for the prefetch scheduler (a forward runs concurrently)
+  bool ef_sched = false;         // ... for the prefetch scheduler (a forward runs concurrently)
   // scheduler (co-resident) mode: at most sched_ctas CTAs per streaming kernel, each small
   // enough (registers, shared memory) to sit next to a GEMM CTA on an SM (EDIT_SCHED_CTAS)
-  int sched_ctas = 148;
+  // (default 0 = full grids: measured, capping does not buy overlap on B200 -- DESIGN.md 7)
+  int sched_ctas = 0;
   int sched_smem_kb = 18;
   bool ready = false;            // init completed (destroy may then barrier with the peers)
   char* ws = nullptr;
@@ -264,13 +265,12 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
     const int v = atoi(e);
     if (v >= 32 && v <= 4096 && (v & 31) == 0) h->peer_tile = v;
   }
-  // L2 policy of the streaming passes: EDIT_L2_EVICT_FIRST = 0 | 1 | sched (default sched:
-  // only when a forward shares the GPU, i.e. scheduler rounds)
+  // L2 policy of the streaming passes: EDIT_L2_EVICT_FIRST = 0 | 1 | sched (default 0;
+  // measured neutral standalone and no overlap gain, profiles/r1_overlap_experiments.md)
   if (const char* e = getenv("EDIT_L2_EVICT_FIRST")) {
     if (!strcmp(e, "1")) h->ef_direct = h->ef_sched = true;
-    else if (!strcmp(e, "0")) h->ef_direct = h->ef_sched = false;
+    else if (!strcmp(e, "sched")) h->ef_sched = true;
   }
-  h->sched_ctas = h->num_sms;
   if (const char* e = getenv("EDIT_SCHED_CTAS")) {  // 0 = full grids also in scheduler rounds
     const int v = atoi(e);
     if (v >= 0) h->sched_ctas = std::min(v, kMaxPeerCtas);
