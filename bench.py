@@ -212,6 +212,8 @@ def main() -> None:
     ap.add_argument("--overlap-tokens", type=int, default=8192,
                     help="tokens/GPU of the synthetic forward for the prefetch-overlap measurement (0 = skip)")
     ap.add_argument("--overlap-steps", type=int, default=3)
+    ap.add_argument("--no-register", action="store_true",
+                    help="peer path: do not register the locals for direct IPC reads (stage a copy)")
     ap.add_argument("--sequential", action="store_true",
                     help="time per-unit edit_layer_sync calls on one stream instead of edit_sync_round")
     args = ap.parse_args()
@@ -254,6 +256,9 @@ def main() -> None:
         moms.append(synth.shard_momentum(u, i, M, m_idx, dev))
         locs.append(torch.empty(numel[i], dtype=dtype, device=dev))
     torch.cuda.synchronize()
+    registered = N > 1 and args.algo == "peer" and not args.no_register
+    if registered:
+        sync.register_locals(locs)   # members read each other's locals directly (no staging copy)
 
     def redraw(step: int) -> None:
         # "tau inner steps" of every worker, outside the timed region
@@ -349,7 +354,7 @@ def main() -> None:
         k4_bound, k4_peak, k4_B = "hbm", hbm_peak, k4_hbm_B
     k4_achieved = k4_B * k4_elems / (k4_ms * 1e-3) / 1e9 if k4_ms > 0 else None
     k4_iso = k4_B * iso_elems / (iso_ms["outer_update"] * 1e-3) / 1e9 if iso_ms["outer_update"] > 0 else None
-    k1_B = (2 * b_l + 4) if peer else (b_l + 4 + (4 if N > 1 else 0))   # K1 reads local+anchor (+ writes L copy / S)
+    k1_B = (2 * b_l + 4) if (peer and not registered) else (b_l + 4 + (4 if (N > 1 and not peer) else 0))
     k1_iso = k1_B * iso_elems / (iso_ms["pg_norm"] * 1e-3) / 1e9 if iso_ms["pg_norm"] > 0 else None
     if peer:
         b_nvl = 6.0 * (N - 1) / N if b_l == 2 else 8.0 * (N - 1) / N  # bytes the peer path moves
@@ -453,7 +458,8 @@ def main() -> None:
                                    f"of {len(units)} units ({P_r} params/rank), {args.dtype} local + f32 "
                                    "anchor/momentum",
                        "mesh": f"{M}x{N}", "params_per_rank": P_r, "param_dtype": args.dtype,
-                       "exchange": (args.algo if N > 1 else "none (N = 1)"),
+                       "exchange": (args.algo + (" (registered locals)" if registered else "") if N > 1
+                                    else "none (N = 1)"),
                        "api": "edit_layer_sync x L (sequential)" if args.sequential else
                        f"edit_sync_round ({os.environ.get('EDIT_LANES', '2')} lanes)",
                        "l2": "inputs (%.1f GB/rank) larger than L2" % (P_r * (b_l + 8) / 1e9),

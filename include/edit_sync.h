@@ -145,6 +145,16 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
 edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* anchor, float* momentum,
                               void* stream);
 
+/* Peer path only (N > 1, EDIT_ALGO_PEER), optional: register the caller's L local buffers
+ * (device pointers, the same ones later passed to edit_layer_sync / edit_sync_round /
+ * the scheduler) so the members of a sync row read each other's params straight from
+ * those buffers (CUDA IPC of their allocations) instead of from a staging copy the norm
+ * pass writes -- saves b_l bytes per param of HBM writes.  Collective over all ranks.
+ * The buffers must stay allocated (not moved or freed) until edit_sync_destroy; a sync
+ * called with a different pointer for a unit falls back to the staging copy.
+ * No-op returning EDIT_OK when N == 1 or algo == EDIT_ALGO_NCCL. */
+edit_status_t edit_sync_register_locals(edit_sync_t h, void* const* locals);
+
 /* One full sync round: every unit 0..L-1 (arrays of L device pointers), equivalent to
  * calling edit_layer_sync for u = 0..L-1 in order but pipelined: units are dealt
  * round-robin over the library's lanes (EDIT_LANES, default 2; each lane = an internal

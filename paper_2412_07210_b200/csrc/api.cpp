@@ -14,6 +14,8 @@
 // Delta from local and anchor): two HBM passes.
 #include <cuda_runtime.h>
 #include <nccl.h>
+
+typedef int CUresult_t;  // CUresult (driver API) without including cuda.h
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -161,6 +163,10 @@ struct edit_sync {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t slot_in[2] = {nullptr, nullptr}, slot_done[2] = {nullptr, nullptr},
               slot_free[2] = {nullptr, nullptr};
+  // registered caller locals (peer path): my pointers and every member's mapped pointer
+  std::vector<void*> reg_local;                     // [L]
+  std::vector<std::vector<const void*>> reg_peer;   // [L][N]
+  std::vector<void*> reg_opened;                    // distinct IPC mappings to close
   // prefetch scheduler state
   std::vector<void*> sched_local;
   std::vector<float*> sched_anchor, sched_mom;
@@ -413,7 +419,12 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
   if (ev) CUDA_TRY(h, cudaEventRecord(ev[0], st));
   // K1: Delta and its shard norm (Alg. 2 l.442-443)
   float* S = (N > 1 && !h->peer) ? ln.S : nullptr;
-  if (h->peer)
+  // peer path: read the members' registered locals directly, else stage a copy of ours
+  const bool direct = h->peer && !h->reg_local.empty() && h->reg_local[layer] == local;
+  PeerPtrs pp = ln.pp;
+  if (direct)
+    for (int j = 0; j < N; ++j) pp.L[j] = h->reg_peer[layer][j];
+  if (h->peer && !direct)
     launched += launch_pg_norm_copy(dt, local, anchor, ln.Lown, n, scr, h->part1[layer], ef, mode.cap, st);
   else
     launched += launch_pg_norm(dt, local, anchor, S, n, scr, h->part1[layer], ef, mode.cap, st);
@@ -459,7 +470,7 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
   if (h->peer) {
     // Eq. 3 as a reduce-scatter over NVLink peer memory: this rank's slice of Dbar
     const Slicing sl = slicing_of(n, N, h->sync_idx, h->peer_tile);
-    launched += launch_rs(dt, ln.pp, sl, anchor, ln.Down, scr, h->part2[layer], mode.peer_ctas, ef, mode.smem_kb, st);
+    launched += launch_rs(dt, pp, sl, anchor, ln.Down, scr, h->part2[layer], mode.peer_ctas, ef, mode.smem_kb, st);
     CUDA_TRY(h, cudaGetLastError());
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
     // ||Dbar||^2 of the module = sum over every slice of every shard: one K-scalar gather
@@ -468,7 +479,7 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[4], st));
     u.gparts = scr->recv2;
     u.n_gparts = h->K;
-    launched += launch_ag_update(dt, u, ln.pp, sl, mode.peer_ctas, ef, mode.smem_kb, st);
+    launched += launch_ag_update(dt, u, pp, sl, mode.peer_ctas, ef, mode.smem_kb, st);
   } else if (N > 1) {
     // Eq. 3: Dbar = sum_n w_n Delta_n, the weight applied inside NCCL (PreMulSum)
     NCCL_TRY(h, ncclAllReduce(S, S, (size_t)n, ncclFloat32, ln.ops[layer], ln.sync, st));
@@ -507,6 +518,78 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
   if (rc != EDIT_OK) return rc;
   return sync_unit(h, h->lanes[0], layer, local, anchor, momentum, static_cast<cudaStream_t>(stream),
                    Mode{h->ef_direct, 0, h->peer_ctas, 0});
+}
+
+typedef CUresult_t (*AddrRangeFn)(unsigned long long*, size_t*, unsigned long long);
+
+edit_status_t edit_sync_register_locals(edit_sync_t h, void* const* locals) {
+  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
+  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  if (!locals) return fail(EDIT_ERR_INVALID_ARG, "null buffer array");
+  if (!h->peer) return EDIT_OK;
+  if (!h->reg_local.empty()) return fail(EDIT_ERR_INVALID_ARG, "locals already registered");
+  const int L = h->cfg.num_layers, N = h->N;
+  for (int u = 0; u < L; ++u)
+    if ((h->numel[u] > 0 && !locals[u]) || ((uintptr_t)locals[u] & 15u))
+      return fail(EDIT_ERR_INVALID_ARG, "null or misaligned local");
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  // base of each unit's allocation (driver cuMemGetAddressRange, fetched at run time so the
+  // library does not link libcuda) -> (IPC handle of the allocation, offset) per unit
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CUDA_TRY(h, cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) return fail(EDIT_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  AddrRangeFn range = reinterpret_cast<AddrRangeFn>(fn);
+  struct Rec {
+    cudaIpcMemHandle_t handle;
+    uint64_t offset;
+  };
+  std::vector<Rec> mine(L);
+  for (int u = 0; u < L; ++u) {
+    memset(&mine[u], 0, sizeof(Rec));
+    if (h->numel[u] == 0) continue;
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (unsigned long long)(uintptr_t)locals[u]) != 0)
+      return fail(EDIT_ERR_CUDA, "cuMemGetAddressRange failed for a local buffer");
+    CUDA_TRY(h, cudaIpcGetMemHandle(&mine[u].handle, locals[u]));
+    mine[u].offset = (uint64_t)((uintptr_t)locals[u] - (uintptr_t)base);
+  }
+  // exchange over the sync row
+  Lane& ln = h->lanes[0];
+  const size_t rb = sizeof(Rec) * (size_t)L;
+  char* dev = nullptr;
+  CUDA_TRY(h, cudaMalloc(&dev, rb * (N + 1)));
+  CUDA_TRY(h, cudaMemcpy(dev, mine.data(), rb, cudaMemcpyHostToDevice));
+  NCCL_TRY(h, ncclAllGather(dev, dev + rb, rb, ncclChar, ln.sync, ln.stream));
+  CUDA_TRY(h, cudaStreamSynchronize(ln.stream));
+  std::vector<Rec> all((size_t)L * N);
+  CUDA_TRY(h, cudaMemcpy(all.data(), dev + rb, rb * N, cudaMemcpyDeviceToHost));
+  CUDA_TRY(h, cudaFree(dev));
+  h->reg_local.assign(locals, locals + L);
+  h->reg_peer.assign(L, std::vector<const void*>(N, nullptr));
+  std::vector<std::pair<std::string, void*>> mapped;  // one mapping per distinct handle
+  for (int j = 0; j < N; ++j) {
+    for (int u = 0; u < L; ++u) {
+      if (j == h->sync_idx) {
+        h->reg_peer[u][j] = locals[u];
+        continue;
+      }
+      if (h->numel[u] == 0) continue;
+      const Rec& r = all[(size_t)j * L + u];
+      const std::string key(reinterpret_cast<const char*>(&r.handle), sizeof r.handle);
+      void* basep = nullptr;
+      for (auto& m : mapped)
+        if (m.first == key) basep = m.second;
+      if (!basep) {
+        CUDA_TRY(h, cudaIpcOpenMemHandle(&basep, r.handle, cudaIpcMemLazyEnablePeerAccess));
+        mapped.emplace_back(key, basep);
+        h->reg_opened.push_back(basep);
+      }
+      h->reg_peer[u][j] = static_cast<const char*>(basep) + r.offset;
+    }
+  }
+  return EDIT_OK;
 }
 
 edit_status_t edit_sync_round(edit_sync_t h, void* const* locals, float* const* anchors, float* const* momenta,
@@ -778,6 +861,7 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
       cudaFree(tmpd);
     }
   }
+  for (void* p : h->reg_opened) cudaIpcCloseMemHandle(p);
   for (Lane& ln : h->lanes) {
     for (size_t l = 0; l < ln.ops.size(); ++l)
       if (ln.sync) ncclRedOpDestroy(ln.ops[l], ln.sync);

@@ -23,7 +23,7 @@ ALGOS = {"peer": 0, "nccl": 1}
 NO_AE, NO_WA, NO_GC = 1, 2, 4
 
 EXPORTED = ("edit_sync_get_unique_id", "edit_sync_workspace_bytes", "edit_sync_init", "edit_layer_sync",
-            "edit_layer_sync_host", "edit_sync_host_wait", "edit_sync_round", "edit_sched_begin_round", "edit_sched_acquire",
+            "edit_layer_sync_host", "edit_sync_host_wait", "edit_sync_round", "edit_sync_register_locals", "edit_sched_begin_round", "edit_sched_acquire",
             "edit_sched_end_round",
             "edit_sync_stats", "edit_sync_get_state", "edit_sync_set_state", "edit_sync_kernel_launches",
             "edit_sync_set_profiling", "edit_sync_profile_collect",
@@ -81,6 +81,7 @@ def load_library() -> ctypes.CDLL:
     lib.edit_layer_sync_host.argtypes, lib.edit_layer_sync_host.restype = [P, I32, P, P, P, P], S
     lib.edit_sync_host_wait.argtypes, lib.edit_sync_host_wait.restype = [P, P], S
     lib.edit_sync_round.argtypes, lib.edit_sync_round.restype = [P, P, P, P, P], S
+    lib.edit_sync_register_locals.argtypes, lib.edit_sync_register_locals.restype = [P, P], S
     lib.edit_sched_begin_round.argtypes, lib.edit_sched_begin_round.restype = [P, P, P, P, I32, P], S
     lib.edit_sched_acquire.argtypes, lib.edit_sched_acquire.restype = [P, I32, P], S
     lib.edit_sched_end_round.argtypes, lib.edit_sched_end_round.restype = [P, P], S
@@ -246,6 +247,20 @@ class EditSync:
                     raise ValueError(f"unit {u} {name}: wrong device/dtype/shape")
         arr = lambda ts: (ctypes.c_void_p * L)(*[t.data_ptr() for t in ts])
         return arr(locals_), arr(anchors), arr(momenta)
+
+    def register_locals(self, locals_) -> None:
+        """Peer path: let the sync row read these local buffers directly (CUDA IPC); they must
+        stay allocated until close().  Collective."""
+        L = self.num_layers
+        if len(locals_) != L:
+            raise ValueError(f"need {L} units")
+        for u, t in enumerate(locals_):
+            if t.device != self.device or t.dtype != self.param_dtype or not t.is_contiguous() or \
+                    t.numel() != self.layer_numel[u]:
+                raise ValueError(f"unit {u} local: wrong device/dtype/shape")
+        self._registered = list(locals_)
+        arr = (ctypes.c_void_p * L)(*[t.data_ptr() for t in locals_])
+        _check(self._lib.edit_sync_register_locals(self._h, arr))
 
     def sync_round(self, locals_, anchors, momenta, stream=None) -> None:
         """One full round (all units), pipelined over the library's lanes (edit_sync_round)."""

@@ -86,7 +86,9 @@ def main():
     loc, anc, mom = inputs_of(units, M, m_idx, n_idx, dtype, dev, plant, recipe)
     if config == "nan" and n_idx == N - 1:
         loc[0][1234 % loc[0].numel()] = float("nan")   # replica N-1 has a NaN param (R9)
-    if api == "round":
+    if api in ("round", "reg"):
+        if api == "reg":
+            s.register_locals(loc)     # peer path reads the members' locals directly
         s.sync_round(loc, anc, mom)
     else:
         for i in range(len(units)):

@@ -50,3 +50,11 @@ def test_multirank_parity(mesh, dtype, config, algo):
 def test_multirank_parity_round_api(mesh, dtype, config, algo):
     # edit_sync_round: units pipelined over two lanes (own comms / exchange buffers each)
     _run(mesh, dtype, config, algo, "round")
+
+
+@pytest.mark.parametrize("mesh,dtype,config", [("1x2", "bf16", "ragged"), ("2x2", "f32", "toy"), ("1x4", "bf16", "nan"),
+                                               ("1x2", "f32", "rollback"), ("4x2", "bf16", "ragged"),
+                                               ("1x8", "bf16", "toy")])
+def test_multirank_parity_registered_locals(mesh, dtype, config):
+    # peer path reading the members' registered local buffers directly (no staging copy)
+    _run(mesh, dtype, config, "peer", "reg")
