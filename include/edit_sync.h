@@ -222,6 +222,29 @@ int64_t edit_sync_kernel_launches(edit_sync_t h);
 /* Frees library-owned resources (NCCL comms, ops, events); never the workspace. */
 edit_status_t edit_sync_destroy(edit_sync_t h);
 
+/* ---------------------------------------------------------------------------------------
+ * When to sync (host logic only; no device work).
+ *   EDIT_TRIGGER_STEPS: EDiT, Alg. 1 l.408 -- the forward of global inner step s = t*tau + p
+ *     syncs iff s > t_warm and p == 0 (s % tau == 0).
+ *   EDIT_TRIGGER_TIME:  A-EDiT, §3.3 -- after the warm-up, each rank runs whole inner
+ *     steps until its own time since its last sync reaches tau_time, then syncs; ranks may
+ *     complete different numbers of inner steps; no extra communication (the sync's first
+ *     collective is where early ranks wait, at most one step of the slowest rank).
+ * sync_now(step, now) is asked at the start of every inner step `step` (a running step count)
+ * with the caller's clock in seconds; mark_synced(now) restarts the A-EDiT time base after
+ * the sync completed.  in_warmup(step): Alg. 1 l.422 "(t*tau + p) <= t_warm" -- the
+ * synchronous mini-batch phase whose gradients are all-reduced over the sync group. */
+typedef struct edit_trigger* edit_trigger_t;
+#define EDIT_TRIGGER_STEPS 0
+#define EDIT_TRIGGER_TIME 1
+edit_status_t edit_trigger_create(int32_t kind, int64_t tau_steps, double tau_time_s, int64_t t_warm,
+                                  double start_time_s, edit_trigger_t* out);
+int32_t edit_trigger_sync_now(edit_trigger_t t, int64_t step, double now_s);
+int32_t edit_trigger_in_warmup(edit_trigger_t t, int64_t step);
+edit_status_t edit_trigger_mark_synced(edit_trigger_t t, double now_s);
+int64_t edit_trigger_syncs(edit_trigger_t t);
+edit_status_t edit_trigger_destroy(edit_trigger_t t);
+
 /* Text of the last error on the calling thread ("" if none). */
 const char* edit_sync_last_error(void);
 

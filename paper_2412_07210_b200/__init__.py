@@ -4,7 +4,7 @@ The hot path (Alg. 2) runs in libedit_sync.so (csrc/, C ABI in include/
 this package is the thin Python binding around it.
 """
 from .edit_sync import (EDIT_BF16, EDIT_F32, NO_AE, NO_GC, NO_WA, EditSync, EditSyncError,  # noqa: F401
-                        LayerStats, broadcast_unique_id, get_unique_id, load_library)
+                        LayerStats, Trigger, broadcast_unique_id, get_unique_id, load_library)
 
-__all__ = ["EditSync", "EditSyncError", "LayerStats", "broadcast_unique_id", "get_unique_id", "load_library",
+__all__ = ["EditSync", "EditSyncError", "LayerStats", "Trigger", "broadcast_unique_id", "get_unique_id", "load_library",
            "NO_AE", "NO_WA", "NO_GC", "EDIT_BF16", "EDIT_F32"]

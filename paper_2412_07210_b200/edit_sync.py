@@ -26,7 +26,8 @@ EXPORTED = ("edit_sync_get_unique_id", "edit_sync_workspace_bytes", "edit_sync_i
             "edit_layer_sync_host", "edit_sync_host_wait", "edit_sync_round", "edit_sync_register_locals", "edit_sched_begin_round", "edit_sched_acquire",
             "edit_sched_end_round",
             "edit_sync_stats", "edit_sync_get_state", "edit_sync_set_state", "edit_sync_kernel_launches",
-            "edit_sync_set_profiling", "edit_sync_profile_collect",
+            "edit_sync_set_profiling", "edit_sync_profile_collect", "edit_trigger_create", "edit_trigger_sync_now",
+            "edit_trigger_in_warmup", "edit_trigger_mark_synced", "edit_trigger_syncs", "edit_trigger_destroy",
             "edit_sync_destroy", "edit_sync_last_error", "edit_sync_version")
 
 _STATUS = {0: "EDIT_OK", 1: "EDIT_ERR_INVALID_ARG", 2: "EDIT_ERR_CUDA", 3: "EDIT_ERR_NCCL",
@@ -96,6 +97,14 @@ def load_library() -> ctypes.CDLL:
     lib.edit_sync_profile_collect.restype = S
     lib.edit_sync_kernel_launches.argtypes, lib.edit_sync_kernel_launches.restype = [P], I64
     lib.edit_sync_destroy.argtypes, lib.edit_sync_destroy.restype = [P], S
+    D = ctypes.c_double
+    lib.edit_trigger_create.argtypes = [I32, I64, D, I64, D, ctypes.POINTER(P)]
+    lib.edit_trigger_create.restype = S
+    lib.edit_trigger_sync_now.argtypes, lib.edit_trigger_sync_now.restype = [P, I64, D], I32
+    lib.edit_trigger_in_warmup.argtypes, lib.edit_trigger_in_warmup.restype = [P, I64], I32
+    lib.edit_trigger_mark_synced.argtypes, lib.edit_trigger_mark_synced.restype = [P, D], S
+    lib.edit_trigger_syncs.argtypes, lib.edit_trigger_syncs.restype = [P], I64
+    lib.edit_trigger_destroy.argtypes, lib.edit_trigger_destroy.restype = [P], S
     lib.edit_sync_last_error.argtypes, lib.edit_sync_last_error.restype = [], ctypes.c_char_p
     lib.edit_sync_version.argtypes, lib.edit_sync_version.restype = [], ctypes.c_char_p
     _lib = lib
@@ -327,3 +336,47 @@ class EditSync:
 
     def __exit__(self, *exc):
         self.close()
+
+
+class Trigger:
+    """When to sync: EDiT's step trigger (Alg. 1 l.408) or A-EDiT's time trigger (§3.3).
+
+    Trigger.steps(tau, t_warm) / Trigger.time(tau_time_s, t_warm, start_time_s).  Ask
+    sync_now(step, now) at the start of every inner step; call mark_synced(now) after the sync."""
+
+    def __init__(self, kind: int, tau_steps: int = 1, tau_time_s: float = 0.0, t_warm: int = 0,
+                 start_time_s: float = 0.0):
+        self._lib = load_library()
+        h = ctypes.c_void_p()
+        _check(self._lib.edit_trigger_create(int(kind), int(tau_steps), float(tau_time_s), int(t_warm),
+                                             float(start_time_s), ctypes.byref(h)))
+        self._h = h
+
+    @classmethod
+    def steps(cls, tau: int, t_warm: int = 0) -> "Trigger":
+        return cls(0, tau_steps=tau, t_warm=t_warm)
+
+    @classmethod
+    def time(cls, tau_time_s: float, t_warm: int = 0, start_time_s: float = 0.0) -> "Trigger":
+        return cls(1, tau_time_s=tau_time_s, t_warm=t_warm, start_time_s=start_time_s)
+
+    def sync_now(self, step: int, now_s: float = 0.0) -> bool:
+        return bool(self._lib.edit_trigger_sync_now(self._h, int(step), float(now_s)))
+
+    def in_warmup(self, step: int) -> bool:
+        return bool(self._lib.edit_trigger_in_warmup(self._h, int(step)))
+
+    def mark_synced(self, now_s: float = 0.0) -> None:
+        _check(self._lib.edit_trigger_mark_synced(self._h, float(now_s)))
+
+    @property
+    def syncs(self) -> int:
+        return int(self._lib.edit_trigger_syncs(self._h))
+
+    def __del__(self):
+        try:
+            if self._h:
+                self._lib.edit_trigger_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
