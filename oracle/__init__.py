@@ -77,6 +77,7 @@ def _load():
             lib.oracle_sync_unit.restype = ctypes.c_int
             lib.oracle_f32_to_bf16_rne.argtypes, lib.oracle_f32_to_bf16_rne.restype = [ctypes.c_float], ctypes.c_uint16
             lib.oracle_bf16_to_f64.argtypes, lib.oracle_bf16_to_f64.restype = [ctypes.c_uint16], D
+            lib.oracle_allreduce_mean.argtypes, lib.oracle_allreduce_mean.restype = [I32, I64, I32, P, P], None
             lib.oracle_set_threads.argtypes, lib.oracle_set_threads.restype = [ctypes.c_int], None
             lib.oracle_get_threads.argtypes, lib.oracle_get_threads.restype = [], ctypes.c_int
             _lib = lib
@@ -221,3 +222,14 @@ def sync_unit(cfg: Config, locals_, anchors, momenta, ema: list[Ema]):
     out = Outcome(G=np.array(o.G[:N]), z=np.array(o.z[:N]), anomalous=np.array(o.anomalous[:N], dtype=bool),
                   w=np.array(o.w[:N]), G_bar=o.G_bar, beta=o.beta, rollback=bool(o.rollback))
     return out_loc, anc, mom, new_ema, out
+
+
+def allreduce_mean(grads) -> np.ndarray:
+    """Warm-up gradient sync (Alg. 1 l.422-424): mean over the N members, rounded to the
+    stored type.  grads: [N, numel] float32 or uint16 (bf16 bits)."""
+    g = np.ascontiguousarray(grads)
+    if g.ndim != 2 or g.dtype not in (np.float32, np.uint16):
+        raise TypeError("grads must be [N, numel] float32 or uint16 (bf16 bits)")
+    out = np.empty(g.shape[1], dtype=g.dtype)
+    _load().oracle_allreduce_mean(g.shape[0], g.shape[1], int(g.dtype == np.uint16), g.ctypes.data, out.ctypes.data)
+    return out

@@ -364,3 +364,25 @@ int oracle_sync_unit(const oracle_cfg_t* cfg, int32_t M, int32_t N, int64_t nume
   free(dbar);
   return 0;
 }
+
+/* ---------------------------------------------------------------------------
+ * Warm-up phase gradient synchronisation (Alg. 1 l.422-424):
+ *   "If the current step t is within the warmup phase, an additional all-reduce
+ *    operation will be performed within each model sync group to synchronize
+ *    gradients across all workers" -- read as the MEAN over the N members (SPEC
+ *    S:313-321 all_reduce_mean; the shard group's reduce-scatter averages too).
+ * grads [N][numel] as stored (bf16 bits or fp32); out [numel] in the same type:
+ *   out[k] = round_to_dtype( (1/N) * sum_n grads[n][k] )   (fp64 sum in n order)
+ * ------------------------------------------------------------------------- */
+void oracle_allreduce_mean(int32_t N, int64_t numel, int32_t is_bf16, const void* grads, void* out) {
+  const uint16_t* gb = (const uint16_t*)grads;
+  const float* gf = (const float*)grads;
+  for (int64_t k = 0; k < numel; ++k) {
+    double s = 0.0;
+    for (int n = 0; n < N; ++n)
+      s += is_bf16 ? oracle_bf16_to_f64(gb[(size_t)n * numel + k]) : (double)gf[(size_t)n * numel + k];
+    float m = (float)(s / (double)N);
+    if (is_bf16) ((uint16_t*)out)[k] = oracle_f32_to_bf16_rne(m);
+    else ((float*)out)[k] = m;
+  }
+}

@@ -215,3 +215,21 @@ def test_appc_worked_example_whole_sync(golden):
     np.testing.assert_array_equal(loc[0, 0], anc[0])
     np.testing.assert_array_equal(loc[0, 1], anc[0])
     assert all(e.count == 1 for e in ema) and not out.rollback
+
+
+def test_allreduce_mean_spec_values(golden):
+    for c in golden("spec_examples.json")["all_reduce_mean"]:
+        got = oracle.allreduce_mean(np.array(c["grads"], np.float32))
+        np.testing.assert_array_equal(got, np.array(c["expect"], np.float32), err_msg=c["cite"])
+
+
+def test_allreduce_mean_vs_numpy_and_identical_inputs():
+    rng = np.random.default_rng(31)
+    g = rng.normal(0, 1e-3, (5, 1001)).astype(np.float32)
+    np.testing.assert_allclose(oracle.allreduce_mean(g), g.astype(np.float64).mean(0), rtol=6e-8, atol=1e-12)
+    same = np.repeat(g[:1], 4, axis=0)                     # identical inputs -> that input
+    np.testing.assert_array_equal(oracle.allreduce_mean(same), g[0])
+    gb = oracle.f32_to_bf16_bits(g).reshape(g.shape)
+    ref = torch.from_numpy(oracle.bf16_bits_to_f64(gb).reshape(g.shape).mean(0).astype(np.float32)).to(
+        torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    np.testing.assert_array_equal(oracle.allreduce_mean(gb), ref)
