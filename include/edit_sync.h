@@ -196,6 +196,17 @@ edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* 
 edit_status_t edit_sched_acquire(edit_sync_t h, int32_t layer, void* compute_stream);
 edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream);
 
+/* Warm-up phase (Alg. 1 l.422-424): while (t*tau + p) <= t_warm the gradients
+ * of the synchronous mini-batch phase are all-reduced within the model sync group, after the
+ * shard group's reduce-scatter.  grad [layer_numel[layer]] param_dtype, device: this rank's
+ * gradient shard of the unit, replaced in place by the MEAN over the N members of its sync
+ * row, bit-identical on every member.  Collective over the sync row
+ * (every rank calls it for the same units in the same order).  Peer path: the gradient is
+ * staged (copied) into the IPC-exported buffer, each member averages its 1/N slice straight
+ * from the others over NVLink, then pulls every averaged slice from its owner; NCCL path:
+ * ncclAllReduce(ncclAvg).  N == 1: no-op. */
+edit_status_t edit_warmup_allreduce(edit_sync_t h, int32_t layer, void* grad, void* stream);
+
 /* Blocks until this unit's last enqueued sync has completed, then copies its
  * outcome record to *out. */
 edit_status_t edit_sync_stats(edit_sync_t h, int32_t layer, edit_layer_stats_t* out);

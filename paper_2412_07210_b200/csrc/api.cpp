@@ -163,6 +163,7 @@ struct edit_sync {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t slot_in[2] = {nullptr, nullptr}, slot_done[2] = {nullptr, nullptr},
               slot_free[2] = {nullptr, nullptr};
+  double* warm_dev = nullptr;  // warm-up all-reduce: barrier scalars (N + 1)
   // registered caller locals (peer path): my pointers and every member's mapped pointer
   std::vector<void*> reg_local;                     // [L]
   std::vector<std::vector<const void*>> reg_peer;   // [L][N]
@@ -621,6 +622,37 @@ edit_status_t edit_sync_round(edit_sync_t h, void* const* locals, float* const* 
   return EDIT_OK;
 }
 
+edit_status_t edit_warmup_allreduce(edit_sync_t h, int32_t layer, void* grad, void* stream) {
+  edit_status_t rc = check_unit_args(h, layer, grad, grad, grad);
+  if (rc != EDIT_OK) return rc;
+  if (h->N == 1) return EDIT_OK;
+  const int64_t n = h->numel[layer];
+  const int dt = h->cfg.param_dtype;
+  const size_t esz = dt == EDIT_BF16 ? 2 : 4;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Lane& ln = h->lanes[0];
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  if (!h->peer) {
+    NCCL_TRY(h, ncclAllReduce(grad, grad, (size_t)n, dt == EDIT_BF16 ? ncclBfloat16 : ncclFloat32, ncclAvg,
+                              ln.sync, st));
+    return EDIT_OK;
+  }
+  if (!h->warm_dev) CUDA_TRY(h, cudaMalloc(reinterpret_cast<void**>(&h->warm_dev), sizeof(double) * (h->N + 1)));
+  const Slicing sl = slicing_of(n, h->N, h->sync_idx, h->peer_tile);
+  int launched = 0;
+  // stage this member's gradient where the row can read it; the scalar gathers are the
+  // cross-rank barriers (staging complete before any RS; every RS complete before any AG)
+  CUDA_TRY(h, cudaMemcpyAsync(ln.Lown, grad, (size_t)n * esz, cudaMemcpyDeviceToDevice, st));
+  NCCL_TRY(h, ncclAllGather(h->warm_dev, h->warm_dev + 1, 1, ncclFloat64, ln.sync, st));
+  launched += launch_warm_rs(dt, ln.pp, sl, ln.Down, st);
+  CUDA_TRY(h, cudaGetLastError());
+  NCCL_TRY(h, ncclAllGather(h->warm_dev, h->warm_dev + 1, 1, ncclFloat64, ln.sync, st));
+  launched += launch_warm_ag(dt, ln.pp, sl, grad, st);
+  CUDA_TRY(h, cudaGetLastError());
+  h->launches += launched;
+  return EDIT_OK;
+}
+
 edit_status_t edit_layer_sync_host(edit_sync_t h, int32_t layer, void* local_host, float* anchor_host,
                                    float* momentum_host, void* stream) {
   if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
@@ -876,6 +908,7 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
     if (ln.stream) cudaStreamDestroy(ln.stream);
   }
   if (h->fork) cudaEventDestroy(h->fork);
+  if (h->warm_dev) cudaFree(h->warm_dev);
   for (auto e : h->done)
     if (e) cudaEventDestroy(e);
   for (auto e : h->prof)

@@ -267,6 +267,60 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
   }
 }
 
+// ------------------------------------------------------------------------------ warm-up
+// Alg. 1 l.422-424: during the warm-up the sync group all-reduces the gradients
+// (mean, R-warm).  Same two-kernel shape as the sync's exchange, with uniform weights and no
+// anchor: member n averages its 1/N slice straight from every member's staged gradient
+// (fixed member order), then every member pulls each averaged slice from its owner.
+// Full-grid LDG (the gradient is consumed right after; plain loads reach ~780 GB/s from a
+// peer with the whole GPU, profiles/r1_peer_bench_2gpu.txt).
+template <typename T>
+__global__ void __launch_bounds__(kThreads) warm_rs_kernel(const __grid_constant__ PeerPtrs pp, Slicing sl,
+                                                           float* __restrict__ Dmine) {
+  const int64_t s0 = (int64_t)sl.me * sl.slice;
+  const int64_t n8 = sl.n >> 3;
+  const int64_t s1 = min(s0 + sl.slice, n8);
+  const int64_t i = s0 + (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const float inv = 1.f / (float)sl.N;
+  if (i < s1) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < sl.N; ++j) {
+      float g[8];
+      load8(static_cast<const T*>(pp.L[j]) + 8 * i, g);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] += g[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] *= inv;
+    store8(Dmine + 8 * (i - s0), acc);
+  }
+  // the partial last vector (n % 8 elements) belongs to the owner of vector n8
+  if ((sl.n & 7) && n8 >= s0 && n8 < s0 + sl.slice && blockIdx.x == 0 && threadIdx.x < (sl.n & 7)) {
+    const int64_t k = 8 * n8 + threadIdx.x;
+    float acc = 0.f;
+    for (int j = 0; j < sl.N; ++j) acc += load1(static_cast<const T*>(pp.L[j]) + k);
+    Dmine[k - 8 * s0] = acc * inv;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) warm_ag_kernel(const __grid_constant__ PeerPtrs pp, Slicing sl,
+                                                           T* __restrict__ out) {
+  const int64_t n8 = sl.n >> 3;
+  const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (i < n8) {
+    const int64_t j = i / sl.slice;
+    float g[8];
+    load8(pp.D[j] + 8 * (i - j * sl.slice), g);
+    store8(out + 8 * i, g);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (sl.n & 7)) {
+    const int64_t k = 8 * n8 + threadIdx.x;
+    const int64_t j = n8 / sl.slice;
+    store1(out + k, pp.D[j][k - 8 * j * sl.slice]);
+  }
+}
+
 int default_smem_budget() {
   static int b = [] {
     const char* e = getenv("EDIT_PEER_SMEM_KB");  // shared-memory ring per CTA (default 200 KB)
@@ -344,6 +398,23 @@ int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const S
     if (ef) ag_go<float, true>(grid, r, st, a, pp, sl);
     else ag_go<float, false>(grid, r, st, a, pp, sl);
   }
+  return 1;
+}
+
+int launch_warm_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, float* Dmine, cudaStream_t st) {
+  const int64_t n8 = sl.n >> 3;
+  const int64_t s0 = (int64_t)sl.me * sl.slice;
+  const int64_t cnt = std::max<int64_t>(0, std::min(s0 + sl.slice, n8) - s0);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + kThreads - 1) / kThreads);
+  if (dtype == EDIT_BF16) warm_rs_kernel<__nv_bfloat16><<<grid, kThreads, 0, st>>>(pp, sl, Dmine);
+  else warm_rs_kernel<float><<<grid, kThreads, 0, st>>>(pp, sl, Dmine);
+  return 1;
+}
+
+int launch_warm_ag(int dtype, const PeerPtrs& pp, const Slicing& sl, void* out, cudaStream_t st) {
+  const unsigned grid = (unsigned)std::max<int64_t>(1, ((sl.n >> 3) + kThreads - 1) / kThreads);
+  if (dtype == EDIT_BF16) warm_ag_kernel<__nv_bfloat16><<<grid, kThreads, 0, st>>>(pp, sl, static_cast<__nv_bfloat16*>(out));
+  else warm_ag_kernel<float><<<grid, kThreads, 0, st>>>(pp, sl, static_cast<float*>(out));
   return 1;
 }
 

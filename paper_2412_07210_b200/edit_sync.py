@@ -23,7 +23,8 @@ ALGOS = {"peer": 0, "nccl": 1}
 NO_AE, NO_WA, NO_GC = 1, 2, 4
 
 EXPORTED = ("edit_sync_get_unique_id", "edit_sync_workspace_bytes", "edit_sync_init", "edit_layer_sync",
-            "edit_layer_sync_host", "edit_sync_host_wait", "edit_sync_round", "edit_sync_register_locals", "edit_sched_begin_round", "edit_sched_acquire",
+            "edit_layer_sync_host", "edit_sync_host_wait", "edit_sync_round", "edit_sync_register_locals",
+            "edit_warmup_allreduce", "edit_sched_begin_round", "edit_sched_acquire",
             "edit_sched_end_round",
             "edit_sync_stats", "edit_sync_get_state", "edit_sync_set_state", "edit_sync_kernel_launches",
             "edit_sync_set_profiling", "edit_sync_profile_collect", "edit_trigger_create", "edit_trigger_sync_now",
@@ -83,6 +84,7 @@ def load_library() -> ctypes.CDLL:
     lib.edit_sync_host_wait.argtypes, lib.edit_sync_host_wait.restype = [P, P], S
     lib.edit_sync_round.argtypes, lib.edit_sync_round.restype = [P, P, P, P, P], S
     lib.edit_sync_register_locals.argtypes, lib.edit_sync_register_locals.restype = [P, P], S
+    lib.edit_warmup_allreduce.argtypes, lib.edit_warmup_allreduce.restype = [P, I32, P, P], S
     lib.edit_sched_begin_round.argtypes, lib.edit_sched_begin_round.restype = [P, P, P, P, I32, P], S
     lib.edit_sched_acquire.argtypes, lib.edit_sched_acquire.restype = [P, I32, P], S
     lib.edit_sched_end_round.argtypes, lib.edit_sched_end_round.restype = [P, P], S
@@ -256,6 +258,15 @@ class EditSync:
                     raise ValueError(f"unit {u} {name}: wrong device/dtype/shape")
         arr = lambda ts: (ctypes.c_void_p * L)(*[t.data_ptr() for t in ts])
         return arr(locals_), arr(anchors), arr(momenta)
+
+    def warmup_allreduce(self, layer: int, grad: torch.Tensor, stream=None) -> None:
+        """Warm-up phase (Alg. 1 l.422-424): grad <- mean over the sync row, in place."""
+        n = self.layer_numel[layer] if 0 <= layer < self.num_layers else -1
+        if grad.device != self.device or grad.dtype != self.param_dtype or not grad.is_contiguous() or \
+                grad.numel() != n:
+            raise ValueError(f"grad: need a contiguous {self.param_dtype} tensor of {n} elements on {self.device}")
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _check(self._lib.edit_warmup_allreduce(self._h, int(layer), grad.data_ptr(), st.cuda_stream))
 
     def register_locals(self, locals_) -> None:
         """Peer path: let the sync row read these local buffers directly (CUDA IPC); they must

@@ -31,6 +31,41 @@ def inputs_of(units, M, m, n, dtype, dev, plant, recipe, salt=0):
     return loc, anc, mom
 
 
+def grad_of(u, i, M, m, n, dtype, dev):
+    # a seeded per-rank gradient shard (kind 5), zero in the padded tail
+    numel = synth.shard_numel(u.numel, M)
+    g = synth._randn(numel, synth.seed_of(5, i, m, n), dev).mul_(1e-3)
+    g[max(0, min(numel, u.numel - m * numel)):] = 0
+    return g.to(dtype)
+
+
+def warm_check(units, M, N, m_idx, n_idx, rank, world, dtype, dtype_s, dev, s, mesh, algo, local_rank):
+    """Warm-up gradient all-reduce (Alg. 1 l.422-424) vs the oracle's mean over the sync row."""
+    grads = [grad_of(u, i, M, m_idx, n_idx, dtype, dev) for i, u in enumerate(units)]
+    for i in range(len(units)):
+        s.warmup_allreduce(i, grads[i])
+    torch.cuda.synchronize()
+    mine = {"rank": rank, "g": [parity.to_oracle_local(g) for g in grads]}
+    gathered = [None] * world if rank == 0 else None
+    dist.gather_object(mine, gathered, dst=0)
+    if rank == 0:
+        by_rank = {g["rank"]: g for g in gathered}
+        for i, u in enumerate(units):
+            for m in range(M):
+                inp = np.stack([parity.to_oracle_local(grad_of(u, i, M, m, n, dtype, dev)) for n in range(N)])
+                ref = oracle.allreduce_mean(inp)
+                for n in range(N):
+                    r = n * M + m
+                    got = by_rank[r]["g"][i]
+                    parity.assert_local_close(got, ref, f"warm {mesh} unit {i} rank {r}")
+                    assert np.array_equal(got, by_rank[m]["g"][i]), "sync row members differ"
+        print(f"PARITY OK warm {mesh} {dtype_s} {algo} unit: {len(units)} units", flush=True)
+    s.close()
+    dist.barrier(device_ids=[local_rank])
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     mesh, dtype_s, config = sys.argv[1], sys.argv[2], sys.argv[3]
     algo = sys.argv[4] if len(sys.argv) > 4 else "peer"
@@ -65,6 +100,9 @@ def main():
     elif config == "nan":
         units = [synth.Unit("a", 300_001, ()), synth.Unit("b", 9, ())]
         seed_ema = False
+    elif config == "warm":
+        units = [synth.Unit("a", 1_000_003, ()), synth.Unit("b", 13, ()), synth.Unit("c", 65_536, ())]
+        seed_ema = False
     elif config == "llama350m_sample":
         all_units = synth.llama_units("350M")
         units = [all_units[0], all_units[1], all_units[33]]
@@ -83,6 +121,8 @@ def main():
         ema0 = [[oracle.Ema(mu[i, n], 0.1 * mu[i, n], recipe.ema_warmup_rounds) for n in range(N)]
                 for i in range(len(units))]
 
+    if config == "warm":
+        return warm_check(units, M, N, m_idx, n_idx, rank, world, dtype, dtype_s, dev, s, mesh, algo, local_rank)
     loc, anc, mom = inputs_of(units, M, m_idx, n_idx, dtype, dev, plant, recipe)
     if config == "nan" and n_idx == N - 1:
         loc[0][1234 % loc[0].numel()] = float("nan")   # replica N-1 has a NaN param (R9)

@@ -58,3 +58,11 @@ def test_multirank_parity_round_api(mesh, dtype, config, algo):
 def test_multirank_parity_registered_locals(mesh, dtype, config):
     # peer path reading the members' registered local buffers directly (no staging copy)
     _run(mesh, dtype, config, "peer", "reg")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("mesh,dtype", [("1x2", "bf16"), ("1x2", "f32"), ("2x2", "bf16"), ("1x4", "f32"),
+                                        ("2x4", "bf16"), ("1x8", "bf16")])
+def test_warmup_allreduce_parity(mesh, dtype, algo):
+    # NEXT-3: the warm-up phase's gradient all-reduce over the sync group (Alg. 1 l.422-424)
+    _run(mesh, dtype, "warm", algo, "unit")
