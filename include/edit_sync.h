@@ -155,6 +155,17 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
  * No-op returning EDIT_OK when N == 1 or algo == EDIT_ALGO_NCCL. */
 edit_status_t edit_sync_register_locals(edit_sync_t h, void* const* locals);
 
+/* NEXT-2, fused write-back -> shard-group all-gather (Alg. 1 l.411: after the sync, "gather
+ * module parameters in G^s_n" for the forward).  Register, per unit, a device buffer of
+ * M * layer_numel[u] elements (param_dtype) that receives the whole module: shard m at
+ * [m * layer_numel[u], (m+1) * layer_numel[u]).  From then on every sync of a unit stores
+ * its updated local ALSO into that slot of every shard-group member's buffer (NVLink stores
+ * through CUDA IPC mappings, fused into the update kernel), followed by one scalar gather on
+ * the shard comm, so when the unit's sync has completed on a rank its gathered module is
+ * complete there -- no separate all-gather pass.  Collective over all ranks; buffers must
+ * stay allocated until edit_sync_destroy.  M == 1: nothing to gather, returns EDIT_OK. */
+edit_status_t edit_sync_register_gather(edit_sync_t h, void* const* full_bufs);
+
 /* One full sync round: every unit 0..L-1 (arrays of L device pointers), equivalent to
  * calling edit_layer_sync for u = 0..L-1 in order but pipelined: units are dealt
  * round-robin over the library's lanes (EDIT_LANES, default 2; each lane = an internal

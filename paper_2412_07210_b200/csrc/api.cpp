@@ -164,6 +164,10 @@ struct edit_sync {
   cudaEvent_t slot_in[2] = {nullptr, nullptr}, slot_done[2] = {nullptr, nullptr},
               slot_free[2] = {nullptr, nullptr};
   double* warm_dev = nullptr;  // warm-up all-reduce: barrier scalars (N + 1)
+  // NEXT-2 registered gather buffers: [L][M] (member q's full-module buffer, mapped)
+  std::vector<std::vector<void*>> reg_gather;
+  std::vector<void*> gather_opened;
+  double* gather_dev = nullptr;  // gather barrier scalars per unit [L][M + 1]
   // registered caller locals (peer path): my pointers and every member's mapped pointer
   std::vector<void*> reg_local;                     // [L]
   std::vector<std::vector<const void*>> reg_peer;   // [L][N]
@@ -468,6 +472,12 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
   u.eps = h->cfg.clip_eps;
   u.flags = h->cfg.flags;
   u.rec = h->rec + layer;
+  const bool gathered = !h->reg_gather.empty() && h->numel[layer] > 0;
+  if (gathered) {
+    u.gather_M = h->M;
+    u.gather_off = (int64_t)h->shard_idx * n;
+    for (int q = 0; q < h->M; ++q) u.gather[q] = h->reg_gather[layer][q];
+  }
   if (h->peer) {
     // Eq. 3 as a reduce-scatter over NVLink peer memory: this rank's slice of Dbar
     const Slicing sl = slicing_of(n, N, h->sync_idx, h->peer_tile);
@@ -504,6 +514,12 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
   }
   if (!h->peer) launched += launch_update(dt, u, ef, mode.cap, st);
   CUDA_TRY(h, cudaGetLastError());
+  if (gathered) {
+    // every member of the shard group has stored its shard into every gathered module once
+    // this scalar gather completes (their update kernels precede their contributions)
+    double* gd = h->gather_dev + (size_t)layer * (h->M + 1);
+    NCCL_TRY(h, ncclAllGather(gd, gd + 1, 1, ncclFloat64, ln.shard, st));
+  }
   if (ev) {
     CUDA_TRY(h, cudaEventRecord(ev[5], st));
     h->pending.push_back(layer);
@@ -523,19 +539,11 @@ edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* 
 
 typedef CUresult_t (*AddrRangeFn)(unsigned long long*, size_t*, unsigned long long);
 
-edit_status_t edit_sync_register_locals(edit_sync_t h, void* const* locals) {
-  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
-  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
-  if (!locals) return fail(EDIT_ERR_INVALID_ARG, "null buffer array");
-  if (!h->peer) return EDIT_OK;
-  if (!h->reg_local.empty()) return fail(EDIT_ERR_INVALID_ARG, "locals already registered");
-  const int L = h->cfg.num_layers, N = h->N;
-  for (int u = 0; u < L; ++u)
-    if ((h->numel[u] > 0 && !locals[u]) || ((uintptr_t)locals[u] & 15u))
-      return fail(EDIT_ERR_INVALID_ARG, "null or misaligned local");
-  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
-  // base of each unit's allocation (driver cuMemGetAddressRange, fetched at run time so the
-  // library does not link libcuda) -> (IPC handle of the allocation, offset) per unit
+// Map `ptrs` (L device pointers of this rank, inside cudaMalloc allocations) on every member of
+// `comm` (size P, this rank = `me`): out[u][j] = member j's pointer for unit u in this process.
+static edit_status_t exchange_ipc(edit_sync_t h, void* const* ptrs, int L, ncclComm_t comm, int P, int me,
+                                  cudaStream_t st, std::vector<std::vector<void*>>& out,
+                                  std::vector<void*>& opened) {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
   CUDA_TRY(h, cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
@@ -544,40 +552,39 @@ edit_status_t edit_sync_register_locals(edit_sync_t h, void* const* locals) {
   struct Rec {
     cudaIpcMemHandle_t handle;
     uint64_t offset;
+    uint64_t valid;
   };
   std::vector<Rec> mine(L);
   for (int u = 0; u < L; ++u) {
     memset(&mine[u], 0, sizeof(Rec));
-    if (h->numel[u] == 0) continue;
+    if (!ptrs[u]) continue;
     unsigned long long base = 0;
     size_t size = 0;
-    if (range(&base, &size, (unsigned long long)(uintptr_t)locals[u]) != 0)
-      return fail(EDIT_ERR_CUDA, "cuMemGetAddressRange failed for a local buffer");
-    CUDA_TRY(h, cudaIpcGetMemHandle(&mine[u].handle, locals[u]));
-    mine[u].offset = (uint64_t)((uintptr_t)locals[u] - (uintptr_t)base);
+    if (range(&base, &size, (unsigned long long)(uintptr_t)ptrs[u]) != 0)
+      return fail(EDIT_ERR_CUDA, "cuMemGetAddressRange failed for a registered buffer");
+    CUDA_TRY(h, cudaIpcGetMemHandle(&mine[u].handle, ptrs[u]));
+    mine[u].offset = (uint64_t)((uintptr_t)ptrs[u] - (uintptr_t)base);
+    mine[u].valid = 1;
   }
-  // exchange over the sync row
-  Lane& ln = h->lanes[0];
   const size_t rb = sizeof(Rec) * (size_t)L;
   char* dev = nullptr;
-  CUDA_TRY(h, cudaMalloc(&dev, rb * (N + 1)));
+  CUDA_TRY(h, cudaMalloc(&dev, rb * (P + 1)));
   CUDA_TRY(h, cudaMemcpy(dev, mine.data(), rb, cudaMemcpyHostToDevice));
-  NCCL_TRY(h, ncclAllGather(dev, dev + rb, rb, ncclChar, ln.sync, ln.stream));
-  CUDA_TRY(h, cudaStreamSynchronize(ln.stream));
-  std::vector<Rec> all((size_t)L * N);
-  CUDA_TRY(h, cudaMemcpy(all.data(), dev + rb, rb * N, cudaMemcpyDeviceToHost));
+  NCCL_TRY(h, ncclAllGather(dev, dev + rb, rb, ncclChar, comm, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  std::vector<Rec> all((size_t)L * P);
+  CUDA_TRY(h, cudaMemcpy(all.data(), dev + rb, rb * P, cudaMemcpyDeviceToHost));
   CUDA_TRY(h, cudaFree(dev));
-  h->reg_local.assign(locals, locals + L);
-  h->reg_peer.assign(L, std::vector<const void*>(N, nullptr));
+  out.assign(L, std::vector<void*>(P, nullptr));
   std::vector<std::pair<std::string, void*>> mapped;  // one mapping per distinct handle
-  for (int j = 0; j < N; ++j) {
+  for (int j = 0; j < P; ++j)
     for (int u = 0; u < L; ++u) {
-      if (j == h->sync_idx) {
-        h->reg_peer[u][j] = locals[u];
+      if (j == me) {
+        out[u][j] = ptrs[u];
         continue;
       }
-      if (h->numel[u] == 0) continue;
       const Rec& r = all[(size_t)j * L + u];
+      if (!r.valid) continue;
       const std::string key(reinterpret_cast<const char*>(&r.handle), sizeof r.handle);
       void* basep = nullptr;
       for (auto& m : mapped)
@@ -585,11 +592,57 @@ edit_status_t edit_sync_register_locals(edit_sync_t h, void* const* locals) {
       if (!basep) {
         CUDA_TRY(h, cudaIpcOpenMemHandle(&basep, r.handle, cudaIpcMemLazyEnablePeerAccess));
         mapped.emplace_back(key, basep);
-        h->reg_opened.push_back(basep);
+        opened.push_back(basep);
       }
-      h->reg_peer[u][j] = static_cast<const char*>(basep) + r.offset;
+      out[u][j] = static_cast<char*>(basep) + r.offset;
     }
-  }
+  return EDIT_OK;
+}
+
+edit_status_t edit_sync_register_gather(edit_sync_t h, void* const* full_bufs) {
+  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
+  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  if (!full_bufs) return fail(EDIT_ERR_INVALID_ARG, "null buffer array");
+  if (h->M == 1) return EDIT_OK;
+  if (!h->reg_gather.empty()) return fail(EDIT_ERR_INVALID_ARG, "gather buffers already registered");
+  const int L = h->cfg.num_layers;
+  for (int u = 0; u < L; ++u)
+    if ((h->numel[u] > 0 && !full_bufs[u]) || ((uintptr_t)full_bufs[u] & 15u))
+      return fail(EDIT_ERR_INVALID_ARG, "null or misaligned gather buffer");
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  std::vector<void*> ptrs(full_bufs, full_bufs + L);
+  for (int u = 0; u < L; ++u)
+    if (h->numel[u] == 0) ptrs[u] = nullptr;
+  Lane& ln = h->lanes[0];
+  edit_status_t rc = exchange_ipc(h, ptrs.data(), L, ln.shard, h->M, h->shard_idx, ln.stream, h->reg_gather,
+                                  h->gather_opened);
+  if (rc != EDIT_OK) return rc;
+  CUDA_TRY(h, cudaMalloc(reinterpret_cast<void**>(&h->gather_dev), sizeof(double) * (size_t)L * (h->M + 1)));
+  return EDIT_OK;
+}
+
+edit_status_t edit_sync_register_locals(edit_sync_t h, void* const* locals) {
+  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
+  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  if (!locals) return fail(EDIT_ERR_INVALID_ARG, "null buffer array");
+  if (!h->peer) return EDIT_OK;
+  if (!h->reg_local.empty()) return fail(EDIT_ERR_INVALID_ARG, "locals already registered");
+  const int L = h->cfg.num_layers;
+  for (int u = 0; u < L; ++u)
+    if ((h->numel[u] > 0 && !locals[u]) || ((uintptr_t)locals[u] & 15u))
+      return fail(EDIT_ERR_INVALID_ARG, "null or misaligned local");
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  std::vector<void*> ptrs(locals, locals + L);
+  for (int u = 0; u < L; ++u)
+    if (h->numel[u] == 0) ptrs[u] = nullptr;
+  std::vector<std::vector<void*>> peers;
+  Lane& ln = h->lanes[0];
+  edit_status_t rc = exchange_ipc(h, ptrs.data(), L, ln.sync, h->N, h->sync_idx, ln.stream, peers, h->reg_opened);
+  if (rc != EDIT_OK) return rc;
+  h->reg_peer.assign(L, std::vector<const void*>(h->N, nullptr));
+  for (int u = 0; u < L; ++u)
+    for (int j = 0; j < h->N; ++j) h->reg_peer[u][j] = peers[u][j];
+  h->reg_local.assign(locals, locals + L);
   return EDIT_OK;
 }
 
@@ -883,7 +936,8 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
   edit_status_t st = EDIT_OK;
   cudaSetDevice(h->cfg.device);
   if (!h->poisoned) cudaDeviceSynchronize();
-  if (h->peer && h->ready && !h->poisoned && !h->lanes.empty() && h->lanes[0].global) {
+  if ((h->peer || !h->reg_gather.empty()) && h->ready && !h->poisoned && !h->lanes.empty() &&
+      h->lanes[0].global) {
     // barrier: no member may free its IPC-exported buffers while a peer still reads them
     double* tmpd = nullptr;
     if (cudaMalloc(&tmpd, sizeof(double) * (h->K + 1)) == cudaSuccess) {
@@ -894,6 +948,8 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
     }
   }
   for (void* p : h->reg_opened) cudaIpcCloseMemHandle(p);
+  for (void* p : h->gather_opened) cudaIpcCloseMemHandle(p);
+  if (h->gather_dev) cudaFree(h->gather_dev);
   for (Lane& ln : h->lanes) {
     for (size_t l = 0; l < ln.ops.size(); ++l)
       if (ln.sync) ncclRedOpDestroy(ln.ops[l], ln.sync);

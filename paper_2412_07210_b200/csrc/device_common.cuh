@@ -77,6 +77,19 @@ __device__ __forceinline__ float load1(const __nv_bfloat16* p) { return __bfloat
 __device__ __forceinline__ void store1(float* p, float v) { *p = v; }
 __device__ __forceinline__ void store1(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
 
+// NEXT-2: the updated local, also stored into every shard-group member's full-module buffer
+// (UpdateArgs::gather; no-op when gather_M == 0).  The element type follows the local's.
+template <bool kEF, typename T>
+__device__ __forceinline__ void gather_store8_t(const UpdateArgs& p, int64_t k, const float (&v)[8], uint64_t pol) {
+#pragma unroll
+  for (int q = 0; q < EDIT_MAX_SHARD; ++q)
+    if (q < p.gather_M) store8<kEF>(static_cast<T*>(p.gather[q]) + p.gather_off + k, v, pol);
+}
+template <typename T>
+__device__ __forceinline__ void gather_store1_t(const UpdateArgs& p, int64_t k, float v) {
+  for (int q = 0; q < p.gather_M; ++q) store1(static_cast<T*>(p.gather[q]) + p.gather_off + k, v);
+}
+
 // ---------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -68,6 +68,12 @@ struct UpdateArgs {
   double phi, eps;
   uint32_t flags;
   edit_layer_stats_t* rec;
+  // NEXT-2 fused write-back -> shard-group all-gather: the updated local is also stored at
+  // element offset gather_off of every shard-group member's full-module buffer (gather[q],
+  // q < gather_M; peers' buffers are NVLink/IPC mappings).  gather_M == 0: no gather.
+  void* gather[EDIT_MAX_SHARD];
+  int32_t gather_M;
+  int64_t gather_off;
 };
 
 // Peer-memory view of a sync row (the N members sharing shard index m): every member's

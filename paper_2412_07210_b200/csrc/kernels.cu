@@ -245,12 +245,14 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
           float a[8];
           load8<kEF>(anchor + 8 * i, a, pol);
           store8<kEF>(local + 8 * i, a, pol);
+          gather_store8_t<kEF, T>(p, 8 * i, a, pol);
         }
       }
     }
     if (tail) {
       const int64_t k = 8 * n8 + threadIdx.x;
       store1(local + k, anchor[k]);
+      gather_store1_t<T>(p, k, anchor[k]);
     }
     return;
   }
@@ -289,6 +291,7 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
         store8<kEF>(mom + 8 * i, m[u], pol);
         store8<kEF>(anchor + 8 * i, a[u], pol);
         store8<kEF>(local + 8 * i, a[u], pol);
+        gather_store8_t<kEF, T>(p, 8 * i, a[u], pol);
       }
     }
   }
@@ -302,6 +305,7 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
     mom[k] = m1;
     anchor[k] = a1;
     store1(local + k, a1);
+    gather_store1_t<T>(p, k, a1);
   }
 }
 

@@ -197,10 +197,12 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
       float a[8];
       load8<kEF>(anchor + 8 * i, a, pol);
       store8<kEF>(local + 8 * i, a, pol);
+      gather_store8_t<kEF, T>(p, 8 * i, a, pol);
     }
     if (blockIdx.x == 0 && threadIdx.x < (p.n & 7)) {
       const int64_t k = 8 * n8 + threadIdx.x;
       store1(local + k, anchor[k]);
+      gather_store1_t<T>(p, k, anchor[k]);
     }
     return;
   }
@@ -248,6 +250,7 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
         store8<kEF>(mom + 8 * i, m, pol);
         store8<kEF>(anchor + 8 * i, a, pol);
         store8<kEF>(local + 8 * i, a, pol);
+        gather_store8_t<kEF, T>(p, 8 * i, a, pol);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.empty[s]);
@@ -264,6 +267,7 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
     mom[k] = m1;
     anchor[k] = a1;
     store1(local + k, a1);
+    gather_store1_t<T>(p, k, a1);
   }
 }
 

@@ -24,7 +24,7 @@ NO_AE, NO_WA, NO_GC = 1, 2, 4
 
 EXPORTED = ("edit_sync_get_unique_id", "edit_sync_workspace_bytes", "edit_sync_init", "edit_layer_sync",
             "edit_layer_sync_host", "edit_sync_host_wait", "edit_sync_round", "edit_sync_register_locals",
-            "edit_warmup_allreduce", "edit_sched_begin_round", "edit_sched_acquire",
+            "edit_warmup_allreduce", "edit_sync_register_gather", "edit_sched_begin_round", "edit_sched_acquire",
             "edit_sched_end_round",
             "edit_sync_stats", "edit_sync_get_state", "edit_sync_set_state", "edit_sync_kernel_launches",
             "edit_sync_set_profiling", "edit_sync_profile_collect", "edit_trigger_create", "edit_trigger_sync_now",
@@ -85,6 +85,7 @@ def load_library() -> ctypes.CDLL:
     lib.edit_sync_round.argtypes, lib.edit_sync_round.restype = [P, P, P, P, P], S
     lib.edit_sync_register_locals.argtypes, lib.edit_sync_register_locals.restype = [P, P], S
     lib.edit_warmup_allreduce.argtypes, lib.edit_warmup_allreduce.restype = [P, I32, P, P], S
+    lib.edit_sync_register_gather.argtypes, lib.edit_sync_register_gather.restype = [P, P], S
     lib.edit_sched_begin_round.argtypes, lib.edit_sched_begin_round.restype = [P, P, P, P, I32, P], S
     lib.edit_sched_acquire.argtypes, lib.edit_sched_acquire.restype = [P, I32, P], S
     lib.edit_sched_end_round.argtypes, lib.edit_sched_end_round.restype = [P, P], S
@@ -267,6 +268,21 @@ class EditSync:
             raise ValueError(f"grad: need a contiguous {self.param_dtype} tensor of {n} elements on {self.device}")
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         _check(self._lib.edit_warmup_allreduce(self._h, int(layer), grad.data_ptr(), st.cuda_stream))
+
+    def register_gather(self, full_bufs) -> None:
+        """NEXT-2: per unit a buffer of M * layer_numel elements that every sync fills with the
+        whole module (each shard-group member stores its updated shard into it).  Collective."""
+        L = self.num_layers
+        if len(full_bufs) != L:
+            raise ValueError(f"need {L} units")
+        for u, t in enumerate(full_bufs):
+            if t.device != self.device or t.dtype != self.param_dtype or not t.is_contiguous() or \
+                    t.numel() != self.shard_dim * self.layer_numel[u]:
+                raise ValueError(f"unit {u} gather buffer: need {self.shard_dim * self.layer_numel[u]} "
+                                 f"{self.param_dtype} elements on {self.device}")
+        self._gather = list(full_bufs)
+        arr = (ctypes.c_void_p * L)(*[t.data_ptr() for t in full_bufs])
+        _check(self._lib.edit_sync_register_gather(self._h, arr))
 
     def register_locals(self, locals_) -> None:
         """Peer path: let the sync row read these local buffers directly (CUDA IPC); they must

@@ -126,7 +126,11 @@ def main():
     loc, anc, mom = inputs_of(units, M, m_idx, n_idx, dtype, dev, plant, recipe)
     if config == "nan" and n_idx == N - 1:
         loc[0][1234 % loc[0].numel()] = float("nan")   # replica N-1 has a NaN param (R9)
-    if api in ("round", "reg"):
+    full = None
+    if api == "gather":                # NEXT-2: fused write-back -> shard-group all-gather
+        full = [torch.zeros(M * n_, dtype=dtype, device=dev) for n_ in numel]
+        s.register_gather(full)
+    if api in ("round", "reg", "gather"):
         if api == "reg":
             s.register_locals(loc)     # peer path reads the members' locals directly
         s.sync_round(loc, anc, mom)
@@ -136,7 +140,8 @@ def main():
     torch.cuda.synchronize()
     mine = {"rank": rank, "loc": [parity.to_oracle_local(x) for x in loc],
             "anc": [x.cpu().numpy() for x in anc], "mom": [x.cpu().numpy() for x in mom],
-            "stats": [s.stats(i) for i in range(len(units))]}
+            "stats": [s.stats(i) for i in range(len(units))],
+            "full": [parity.to_oracle_local(f) for f in full] if full is not None else None}
     # invariant: local == rne(anchor) bitwise on every rank (R16)
     for i in range(len(units)):
         assert torch.equal(loc[i], anc[i].to(dtype)), f"rank {rank} unit {i}: local != rne(anchor)"
@@ -172,6 +177,15 @@ def main():
                 # sync-row identity: bitwise identical anchors across the N replicas of shard m
                 g0 = by_rank[m]
                 assert np.array_equal(g["anc"][i], g0["anc"][i]), tag + " anchors differ across the sync row"
+            if api == "gather" and M > 1:
+                # every rank's gathered module == its shard group's new locals, bitwise
+                for r in range(world):
+                    m, n = r % M, r // M
+                    f = by_rank[r]["full"][i]
+                    nl = numel[i]
+                    for q in range(M):
+                        assert np.array_equal(f[q * nl:(q + 1) * nl], by_rank[n * M + q]["loc"][i]), \
+                            f"gathered module of rank {r}, shard {q}, unit {i}"
             if config == "toy" and N > 1:
                 assert out.anomalous[1] and not out.rollback
             if config == "rollback":

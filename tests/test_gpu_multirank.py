@@ -66,3 +66,13 @@ def test_multirank_parity_registered_locals(mesh, dtype, config):
 def test_warmup_allreduce_parity(mesh, dtype, algo):
     # NEXT-3: the warm-up phase's gradient all-reduce over the sync group (Alg. 1 l.422-424)
     _run(mesh, dtype, "warm", algo, "unit")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("mesh,dtype,config", [("2x1", "bf16", "ragged"), ("2x2", "f32", "toy"), ("4x1", "bf16", "ragged"),
+                                               ("2x2", "bf16", "rollback"), ("2x4", "bf16", "ragged"),
+                                               ("4x2", "f32", "toy")])
+def test_fused_shard_allgather_parity(mesh, dtype, config, algo):
+    # NEXT-2: the update kernel also writes the new local into every shard-group member's
+    # full-module buffer; each rank's gathered module must equal its group's new locals
+    _run(mesh, dtype, config, algo, "gather")
