@@ -18,6 +18,7 @@
 typedef int CUresult_t;  // CUresult (driver API) without including cuda.h
 #include <stdio.h>
 #include <stdlib.h>
+#include <dlfcn.h>
 #include <string.h>
 
 #include <algorithm>
@@ -541,14 +542,18 @@ typedef CUresult_t (*AddrRangeFn)(unsigned long long*, size_t*, unsigned long lo
 
 // Map `ptrs` (L device pointers of this rank, inside cudaMalloc allocations) on every member of
 // `comm` (size P, this rank = `me`): out[u][j] = member j's pointer for unit u in this process.
-static edit_status_t exchange_ipc(edit_sync_t h, void* const* ptrs, int L, ncclComm_t comm, int P, int me,
-                                  cudaStream_t st, std::vector<std::vector<void*>>& out,
+static edit_status_t exchange_ipc(edit_sync_t h, void* const* ptrs, const size_t* bytes, int L, ncclComm_t comm,
+                                  int P, int me, cudaStream_t st, std::vector<std::vector<void*>>& out,
                                   std::vector<void*>& opened) {
-  void* fn = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  CUDA_TRY(h, cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
-  if (!fn || q != cudaDriverEntryPointSuccess) return fail(EDIT_ERR_CUDA, "cuMemGetAddressRange unavailable");
-  AddrRangeFn range = reinterpret_cast<AddrRangeFn>(fn);
+  const bool dbg = getenv("EDIT_DEBUG") != nullptr;
+  // cuMemGetAddressRange_v2 from the driver itself (dlopen: the library must load on
+  // machines without a driver, and the unversioned entry point may resolve to the 32-bit v1)
+  static AddrRangeFn range = [] {
+    void* lib = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+    if (!lib) lib = dlopen("libcuda.so.1", RTLD_NOW);
+    return lib ? reinterpret_cast<AddrRangeFn>(dlsym(lib, "cuMemGetAddressRange_v2")) : nullptr;
+  }();
+  if (!range) return fail(EDIT_ERR_CUDA, "cuMemGetAddressRange_v2 unavailable");
   struct Rec {
     cudaIpcMemHandle_t handle;
     uint64_t offset;
@@ -562,8 +567,14 @@ static edit_status_t exchange_ipc(edit_sync_t h, void* const* ptrs, int L, ncclC
     size_t size = 0;
     if (range(&base, &size, (unsigned long long)(uintptr_t)ptrs[u]) != 0)
       return fail(EDIT_ERR_CUDA, "cuMemGetAddressRange failed for a registered buffer");
+    const uintptr_t p = (uintptr_t)ptrs[u];
+    if (p < base || p + bytes[u] > base + size)
+      return fail(EDIT_ERR_INVALID_ARG, "registered buffer does not lie inside one device allocation");
     CUDA_TRY(h, cudaIpcGetMemHandle(&mine[u].handle, ptrs[u]));
-    mine[u].offset = (uint64_t)((uintptr_t)ptrs[u] - (uintptr_t)base);
+    mine[u].offset = (uint64_t)(p - (uintptr_t)base);
+    if (dbg)
+      fprintf(stderr, "[edit_sync] ipc export unit %d ptr %p base %#llx size %zu offset %llu\n", u, ptrs[u], base,
+              size, (unsigned long long)mine[u].offset);
     mine[u].valid = 1;
   }
   const size_t rb = sizeof(Rec) * (size_t)L;
@@ -595,6 +606,9 @@ static edit_status_t exchange_ipc(edit_sync_t h, void* const* ptrs, int L, ncclC
         opened.push_back(basep);
       }
       out[u][j] = static_cast<char*>(basep) + r.offset;
+      if (dbg)
+        fprintf(stderr, "[edit_sync] ipc import unit %d member %d base %p offset %llu -> %p\n", u, j, basep,
+                (unsigned long long)r.offset, out[u][j]);
     }
   return EDIT_OK;
 }
@@ -611,11 +625,15 @@ edit_status_t edit_sync_register_gather(edit_sync_t h, void* const* full_bufs) {
       return fail(EDIT_ERR_INVALID_ARG, "null or misaligned gather buffer");
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   std::vector<void*> ptrs(full_bufs, full_bufs + L);
-  for (int u = 0; u < L; ++u)
+  std::vector<size_t> bytes(L);
+  const size_t esz = h->cfg.param_dtype == EDIT_BF16 ? 2 : 4;
+  for (int u = 0; u < L; ++u) {
     if (h->numel[u] == 0) ptrs[u] = nullptr;
+    bytes[u] = (size_t)h->M * h->numel[u] * esz;
+  }
   Lane& ln = h->lanes[0];
-  edit_status_t rc = exchange_ipc(h, ptrs.data(), L, ln.shard, h->M, h->shard_idx, ln.stream, h->reg_gather,
-                                  h->gather_opened);
+  edit_status_t rc = exchange_ipc(h, ptrs.data(), bytes.data(), L, ln.shard, h->M, h->shard_idx, ln.stream,
+                                  h->reg_gather, h->gather_opened);
   if (rc != EDIT_OK) return rc;
   CUDA_TRY(h, cudaMalloc(reinterpret_cast<void**>(&h->gather_dev), sizeof(double) * (size_t)L * (h->M + 1)));
   return EDIT_OK;
@@ -633,11 +651,16 @@ edit_status_t edit_sync_register_locals(edit_sync_t h, void* const* locals) {
       return fail(EDIT_ERR_INVALID_ARG, "null or misaligned local");
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   std::vector<void*> ptrs(locals, locals + L);
-  for (int u = 0; u < L; ++u)
+  std::vector<size_t> bytes(L);
+  const size_t esz = h->cfg.param_dtype == EDIT_BF16 ? 2 : 4;
+  for (int u = 0; u < L; ++u) {
     if (h->numel[u] == 0) ptrs[u] = nullptr;
+    bytes[u] = (size_t)h->numel[u] * esz;
+  }
   std::vector<std::vector<void*>> peers;
   Lane& ln = h->lanes[0];
-  edit_status_t rc = exchange_ipc(h, ptrs.data(), L, ln.sync, h->N, h->sync_idx, ln.stream, peers, h->reg_opened);
+  edit_status_t rc = exchange_ipc(h, ptrs.data(), bytes.data(), L, ln.sync, h->N, h->sync_idx, ln.stream, peers,
+                                  h->reg_opened);
   if (rc != EDIT_OK) return rc;
   h->reg_peer.assign(L, std::vector<const void*>(h->N, nullptr));
   for (int u = 0; u < L; ++u)
