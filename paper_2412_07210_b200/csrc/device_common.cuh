@@ -79,11 +79,19 @@ __device__ __forceinline__ void store1(__nv_bfloat16* p, float v) { *p = __float
 
 // NEXT-2: the updated local, also stored into every shard-group member's full-module buffer
 // (UpdateArgs::gather; no-op when gather_M == 0).  The element type follows the local's.
+// A shard's slot in the full module starts at element m * numel, which is 16-byte aligned
+// only when numel is a multiple of 8: otherwise the 8 elements are stored one by one.
 template <bool kEF, typename T>
 __device__ __forceinline__ void gather_store8_t(const UpdateArgs& p, int64_t k, const float (&v)[8], uint64_t pol) {
+  if ((p.gather_off & 7) == 0) {
 #pragma unroll
-  for (int q = 0; q < EDIT_MAX_SHARD; ++q)
-    if (q < p.gather_M) store8<kEF>(static_cast<T*>(p.gather[q]) + p.gather_off + k, v, pol);
+    for (int q = 0; q < EDIT_MAX_SHARD; ++q)
+      if (q < p.gather_M) store8<kEF>(static_cast<T*>(p.gather[q]) + p.gather_off + k, v, pol);
+  } else {
+    for (int q = 0; q < p.gather_M; ++q)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) store1(static_cast<T*>(p.gather[q]) + p.gather_off + k + j, v[j]);
+  }
 }
 template <typename T>
 __device__ __forceinline__ void gather_store1_t(const UpdateArgs& p, int64_t k, float v) {
