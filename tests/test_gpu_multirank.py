@@ -34,7 +34,7 @@ def _run(mesh, dtype, config, algo, api):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={M * N}",
            "--master-addr=127.0.0.1", "--master-port=29611", os.path.join(ROOT, "tests", "mp_parity_worker.py"),
            mesh, dtype, config, algo, api]
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     assert f"PARITY OK {config} {mesh} {dtype} {algo} {api}" in r.stdout
 
