@@ -62,21 +62,17 @@ def warm_check(units, M, N, m_idx, n_idx, rank, world, dtype, dtype_s, dev, s, m
         print(f"PARITY OK warm {mesh} {dtype_s} {algo} unit: {len(units)} units", flush=True)
     s.close()
     dist.barrier(device_ids=[local_rank])
-    dist.destroy_process_group()
     return 0
 
 
-def main():
-    mesh, dtype_s, config = sys.argv[1], sys.argv[2], sys.argv[3]
-    algo = sys.argv[4] if len(sys.argv) > 4 else "peer"
-    api = sys.argv[5] if len(sys.argv) > 5 else "unit"   # unit: edit_layer_sync x L; round: edit_sync_round
+def run_case(mesh, dtype_s, config, algo="peer", api="unit"):
+    # api -- unit: edit_layer_sync x L; round: edit_sync_round; reg: registered locals + round;
+    # gather: fused shard all-gather + round
     M, N = (int(x) for x in mesh.split("x"))
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     assert world == M * N
     local_rank = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    dist.init_process_group("nccl", device_id=dev)
     m_idx, n_idx = rank % M, rank // M
     dtype = torch.bfloat16 if dtype_s == "bf16" else torch.float32
     recipe = synth.Recipe()
@@ -197,8 +193,25 @@ def main():
         print(f"PARITY OK {config} {mesh} {dtype_s} {algo} {api}: {len(units)} units", flush=True)
     s.close()
     dist.barrier(device_ids=[local_rank])
-    dist.destroy_process_group()
     return 0 if ok else 1
+
+
+def main():
+    # usage: worker.py MESH dtype:config:algo:api [dtype:config:algo:api ...]
+    #    or: worker.py MESH dtype config [algo [api]]        (one case)
+    mesh = sys.argv[1]
+    if len(sys.argv) > 2 and ":" in sys.argv[2]:
+        cases = [a.split(":") for a in sys.argv[2:]]
+    else:
+        cases = [sys.argv[2:]]
+    local_rank = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    rc = 0
+    for c in cases:
+        rc |= run_case(mesh, *c)
+    dist.destroy_process_group()
+    return rc
 
 
 if __name__ == "__main__":
