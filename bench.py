@@ -212,6 +212,8 @@ def main() -> None:
     ap.add_argument("--overlap-tokens", type=int, default=8192,
                     help="tokens/GPU of the synthetic forward for the prefetch-overlap measurement (0 = skip)")
     ap.add_argument("--overlap-steps", type=int, default=3)
+    ap.add_argument("--warmup-allreduce", action="store_true", help="NEXT-3 measurement (N > 1)")
+    ap.add_argument("--gather", action="store_true", help="NEXT-2 fused shard all-gather measurement (M > 1)")
     ap.add_argument("--no-register", action="store_true",
                     help="peer path: do not register the locals for direct IPC reads (stage a copy)")
     ap.add_argument("--sequential", action="store_true",
@@ -416,6 +418,78 @@ def main() -> None:
         overlap["note"] = ("synthetic forward (bf16 GEMMs of each unit, weights = the synced local) on the "
                            "compute stream; syncs on the library's side stream; acquire(u) before forward(u)")
 
+    # NEXT-3: warm-up gradient all-reduce (mean over the sync group) of a full set of bf16
+    # gradient shards, library path vs torch.distributed/NCCL all_reduce on the same group
+    warm = None
+    if args.warmup_allreduce and N > 1:
+        grads = [torch.randn(numel[i], device=dev).mul_(1e-3).to(dtype) for i in range(len(units))]
+        row = [n * M + m_idx for n in range(N)]
+        groups = [dist.new_group([n * M + m for n in range(N)]) for m in range(M)]
+        my_group = groups[m_idx]
+
+        def lib_warm():
+            for i in range(len(units)):
+                sync.warmup_allreduce(i, grads[i], stream)
+
+        def torch_warm():
+            for i in range(len(units)):
+                dist.all_reduce(grads[i], op=dist.ReduceOp.AVG, group=my_group)
+
+        res = {}
+        for name, fn in (("library", lib_warm), ("torch_nccl", torch_warm)):
+            ts = []
+            for s_ in range(4):
+                barrier()
+                torch.cuda.synchronize()
+                ev0.record(stream)
+                fn()
+                ev1.record(stream)
+                torch.cuda.synchronize()
+                t = max_over_ranks(ev0.elapsed_time(ev1), world, dev)
+                if s_ > 0:
+                    ts.append(t)
+            res[name] = sum(ts) / len(ts)
+        warm = {"ms_per_round": res, "params_per_rank": P_r, "sync_row": row,
+                "GBps_of_grad_bytes_per_gpu": {k: P_r * b_l / (v * 1e-3) / 1e9 for k, v in res.items()},
+                "note": "all units' bf16 gradient shards averaged over the sync group (Alg. 1 l.422-424)"}
+        del grads
+
+    # NEXT-2: fused write-back -> shard-group all-gather (M > 1): a round with the gathered
+    # modules filled by the update kernels vs a round followed by an NCCL all-gather per unit
+    gather = None
+    if args.gather and M > 1:
+        full = [torch.empty(M * numel[i], dtype=dtype, device=dev) for i in range(len(units))]
+        col = [n_idx * M + q for q in range(M)]
+        sgroups = [dist.new_group([n * M + q for q in range(M)]) for n in range(N)]
+        my_sgroup = sgroups[n_idx]
+
+        def round_then_allgather():
+            run_round()
+            for i in range(len(units)):
+                dist.all_gather_into_tensor(full[i], locs[i], group=my_sgroup)
+
+        def timed_g(fn):
+            ts = []
+            for s_ in range(4):
+                redraw(7000 + s_)
+                barrier()
+                torch.cuda.synchronize()
+                ev0.record(stream)
+                fn()
+                ev1.record(stream)
+                torch.cuda.synchronize()
+                t = max_over_ranks(ev0.elapsed_time(ev1), world, dev)
+                if s_ > 0:
+                    ts.append(t)
+            return sum(ts) / len(ts)
+
+        t_sep = timed_g(round_then_allgather)
+        sync.register_gather(full)
+        t_fused = timed_g(run_round)
+        gather = {"t_round_plus_nccl_allgather_ms": t_sep, "t_round_fused_gather_ms": t_fused,
+                  "t_round_ms": ms_per_step, "shard_group": col,
+                  "note": "Alg. 1 l.411 all-gather of the freshly synced module within the shard group"}
+
     # e2e: same metric through the host-buffer C-ABI call (pinned host buffers; H2D of
     # local/anchor/momentum and D2H of the three results inside the timed region)
     e2e = None
@@ -491,6 +565,7 @@ def main() -> None:
             "per_gpu_GBps": bytes_per_rank_round / (ms_per_step * 1e-3) / 1e9,
             "rollbacks_last_round": rollbacks, "beta_sample": betas,
             "gpu_launches": launches, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "overlap": overlap,
+            "warmup_allreduce": warm, "fused_gather": gather,
         }
         print(json.dumps(line), flush=True)
     sync.close()
