@@ -129,7 +129,7 @@ int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const S
                      bool ef, int smem_kb, cudaStream_t st);
 inline int64_t rs_partial_slots(int64_t, int) { return kMaxPeerCtas; }
 // Warm-up gradient all-reduce (mean) over the sync row, peer path (peer_kernels.cu).
-int launch_warm_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, float* Dmine, cudaStream_t st);
+int launch_warm_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, void* Dmine, cudaStream_t st);
 int launch_warm_ag(int dtype, const PeerPtrs& pp, const Slicing& sl, void* out, cudaStream_t st);
 int launch_update(int dtype, const UpdateArgs& a, bool ef, int cap, cudaStream_t st);
 

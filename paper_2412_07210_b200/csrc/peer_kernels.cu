@@ -280,20 +280,27 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
 // peer with the whole GPU, profiles/r1_peer_bench_2gpu.txt).
 template <typename T>
 __global__ void __launch_bounds__(kThreads) warm_rs_kernel(const __grid_constant__ PeerPtrs pp, Slicing sl,
-                                                           float* __restrict__ Dmine) {
+                                                           T* __restrict__ Dmine) {
+  // the owner averages its slice in fp32 (fixed member order) and rounds ONCE to the
+  // gradient type, so the pull below moves b_l bytes per element and every member ends
+  // with the owner's bits
   const int64_t s0 = (int64_t)sl.me * sl.slice;
   const int64_t n8 = sl.n >> 3;
   const int64_t s1 = min(s0 + sl.slice, n8);
   const int64_t i = s0 + (int64_t)blockIdx.x * kThreads + threadIdx.x;
   const float inv = 1.f / (float)sl.N;
   if (i < s1) {
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int j = 0; j < sl.N; ++j) {
-      float g[8];
-      load8(static_cast<const T*>(pp.L[j]) + 8 * i, g);
+    float g[EDIT_MAX_SYNC][8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) acc[k] += g[k];
-    }
+    for (int j = 0; j < EDIT_MAX_SYNC; ++j)  // all members' loads in flight together
+      if (j < sl.N) load8(static_cast<const T*>(pp.L[j]) + 8 * i, g[j]);
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < EDIT_MAX_SYNC; ++j)
+      if (j < sl.N) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += g[j][k];
+      }
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] *= inv;
     store8(Dmine + 8 * (i - s0), acc);
@@ -303,7 +310,7 @@ __global__ void __launch_bounds__(kThreads) warm_rs_kernel(const __grid_constant
     const int64_t k = 8 * n8 + threadIdx.x;
     float acc = 0.f;
     for (int j = 0; j < sl.N; ++j) acc += load1(static_cast<const T*>(pp.L[j]) + k);
-    Dmine[k - 8 * s0] = acc * inv;
+    store1(Dmine + (k - 8 * s0), acc * inv);
   }
 }
 
@@ -312,16 +319,20 @@ __global__ void __launch_bounds__(kThreads) warm_ag_kernel(const __grid_constant
                                                            T* __restrict__ out) {
   const int64_t n8 = sl.n >> 3;
   const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if (i < n8) {
+  if (i < n8) {  // a pure copy of the owner's rounded mean (16 B per bf16 vector)
     const int64_t j = i / sl.slice;
-    float g[8];
-    load8(pp.D[j] + 8 * (i - j * sl.slice), g);
-    store8(out + 8 * i, g);
+    const T* src = reinterpret_cast<const T*>(pp.D[j]) + 8 * (i - j * sl.slice);
+    if (sizeof(T) == 2) {
+      *reinterpret_cast<uint4*>(out + 8 * i) = *reinterpret_cast<const uint4*>(src);
+    } else {
+      *reinterpret_cast<uint4*>(out + 8 * i) = *reinterpret_cast<const uint4*>(src);
+      *reinterpret_cast<uint4*>(out + 8 * i + 4) = *reinterpret_cast<const uint4*>(src + 4);
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x < (sl.n & 7)) {
     const int64_t k = 8 * n8 + threadIdx.x;
     const int64_t j = n8 / sl.slice;
-    store1(out + k, pp.D[j][k - 8 * j * sl.slice]);
+    out[k] = reinterpret_cast<const T*>(pp.D[j])[k - 8 * j * sl.slice];
   }
 }
 
@@ -405,13 +416,15 @@ int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const S
   return 1;
 }
 
-int launch_warm_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, float* Dmine, cudaStream_t st) {
+int launch_warm_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, void* Dmine, cudaStream_t st) {
   const int64_t n8 = sl.n >> 3;
   const int64_t s0 = (int64_t)sl.me * sl.slice;
   const int64_t cnt = std::max<int64_t>(0, std::min(s0 + sl.slice, n8) - s0);
   const unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + kThreads - 1) / kThreads);
-  if (dtype == EDIT_BF16) warm_rs_kernel<__nv_bfloat16><<<grid, kThreads, 0, st>>>(pp, sl, Dmine);
-  else warm_rs_kernel<float><<<grid, kThreads, 0, st>>>(pp, sl, Dmine);
+  if (dtype == EDIT_BF16)
+    warm_rs_kernel<__nv_bfloat16><<<grid, kThreads, 0, st>>>(pp, sl, static_cast<__nv_bfloat16*>(Dmine));
+  else
+    warm_rs_kernel<float><<<grid, kThreads, 0, st>>>(pp, sl, static_cast<float*>(Dmine));
   return 1;
 }
 
