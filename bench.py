@@ -119,38 +119,34 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def oracle_cpu_baseline(model: str, dtype, target_s: float = 15.0) -> dict:
+def oracle_cpu_baseline(model: str, dtype, target_s: float = 12.0) -> dict:
     """The oracle (as it stands) on this host's cores, on a bounded sample of the workload:
-    the first X elements of the 7B layer-0 shard (1 x 1 mesh), X sized for ~target_s."""
-    import numpy as np
-
+    whole decoder-unit shards of the 1 x 1 mesh (layer 0, 1, ...) until ~target_s of CPU work."""
     import oracle
     from tests import parity
     oracle.set_threads(os.cpu_count() or 1)
-    u = synth.llama_units(model)[1]
+    units = synth.llama_units(model)
     dev = torch.device("cuda", torch.cuda.current_device())
-
-    def sample(x):
-        sub = synth.Unit(u.name + f"[:{x}]", x, ())
-        a = synth.shard_anchor(sub, 1, 1, 0, dev)
-        m = synth.shard_momentum(sub, 1, 1, 0, dev)
-        l = synth.shard_local(sub, 1, 1, 0, 0, a, dtype, dev)
-        return (parity.to_oracle_local(l)[None, None], a.cpu().numpy()[None], m.cpu().numpy()[None])
-
-    def run(x):
-        L, A, Mo = sample(x)
+    total_t, total_n, done = 0.0, 0, []
+    for i in range(1, len(units) - 1):
+        u = units[i]
+        a = synth.shard_anchor(u, i, 1, 0, dev)
+        m = synth.shard_momentum(u, i, 1, 0, dev)
+        l = synth.shard_local(u, i, 1, 0, 0, a, dtype, dev)
+        L, A, Mo = parity.to_oracle_local(l)[None, None], a.cpu().numpy()[None], m.cpu().numpy()[None]
+        del a, m, l
+        mu, sg, cnt = synth.ema_seed(u, 0)
         t0 = time.perf_counter()
-        oracle.sync_unit(oracle.Config(), L, A, Mo, [oracle.Ema()])
-        return time.perf_counter() - t0
-
-    x = 2_000_000
-    t = run(x)
-    x2 = int(min(u.numel, max(x, x * target_s / max(t, 1e-3))))
-    t2 = run(x2)
-    return {"value": 4.0 * x2 / t2 / 1e9, "unit": "GB/s", "cores": oracle.get_threads(), "kind": "oracle",
-            "sample": f"1 sync of the first {x2} params of the Llama-{model} layer-0 shard (1x1 mesh, "
-                      f"{'bf16' if dtype == torch.bfloat16 else 'f32'} local), {t2:.2f} s on {oracle.get_threads()} "
-                      "threads; fp32 pseudo-gradient bytes / s"}
+        oracle.sync_unit(oracle.Config(), L, A, Mo, [oracle.Ema(mu, sg, cnt)])
+        total_t += time.perf_counter() - t0
+        total_n += u.numel
+        done.append(u.name)
+        if total_t >= target_s or len(done) >= 8:
+            break
+    return {"value": 4.0 * total_n / total_t / 1e9, "unit": "GB/s", "cores": oracle.get_threads(), "kind": "oracle",
+            "sample": f"1 sync of the Llama-{model} shards {done[0]}..{done[-1]} ({len(done)} decoder units, "
+                      f"{total_n} params, 1x1 mesh, {'bf16' if dtype == torch.bfloat16 else 'f32'} local): "
+                      f"{total_t:.1f} s on {oracle.get_threads()} threads; fp32 pseudo-gradient bytes / s"}
 
 
 def reference_arm(args) -> None:
