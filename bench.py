@@ -201,7 +201,7 @@ def main() -> None:
     ap.add_argument("--mesh", default=None, help="MxN shard x sync mesh (default 1xN)")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--algo", default="peer", choices=["peer", "nccl"], help="N > 1 exchange of Eq. 3")
-    ap.add_argument("--e2e-units", default="1,2,3", help="unit indices timed through the host-buffer API")
+    ap.add_argument("--e2e-units", default="1,2,3,4,5,6", help="unit indices timed through the host-buffer API")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=4_000_000)

@@ -178,11 +178,11 @@ edit_status_t edit_sync_round(edit_sync_t h, void* const* locals, float* const* 
 
 /* Host-buffer variant (the paper's CPU offload of the extra parameters and outer
  * momentum): local/anchor/momentum live in host memory (page-locked for the
- * copies to be asynchronous).  Per call: H2D of the three shards into one of two
+ * copies to be asynchronous).  Per call: H2D of the three shards into one of three
  * library-owned device staging slots (on an internal copy stream), the same device
  * sync as edit_layer_sync on `stream`, then D2H of the three results back into the
  * host buffers (on a second copy stream), so consecutive units overlap copy-in,
- * compute and copy-out.  Staging is allocated on the first call (2 x max numel x
+ * compute and copy-out.  Staging is allocated on the first call (3 x max numel x
  * (elem + 8) bytes).  The host buffers must stay valid and untouched until
  * edit_sync_host_wait() on a stream has been reached. */
 edit_status_t edit_layer_sync_host(edit_sync_t h, int32_t layer, void* local_host, float* anchor_host,

@@ -162,8 +162,9 @@ struct edit_sync {
   size_t slot_bytes = 0;
   int next_slot = 0;
   cudaStream_t h2d = nullptr, d2h = nullptr;
-  cudaEvent_t slot_in[2] = {nullptr, nullptr}, slot_done[2] = {nullptr, nullptr},
-              slot_free[2] = {nullptr, nullptr};
+  // kHostSlots staging slots: copy-in of unit u+2 need not wait for copy-out of unit u
+  static constexpr int kHostSlots = 3;
+  cudaEvent_t slot_in[kHostSlots] = {}, slot_done[kHostSlots] = {}, slot_free[kHostSlots] = {};
   double* warm_dev = nullptr;  // warm-up all-reduce: barrier scalars (N + 1)
   // NEXT-2 registered gather buffers: [L][M] (member q's full-module buffer, mapped)
   std::vector<std::vector<void*>> reg_gather;
@@ -743,10 +744,10 @@ edit_status_t edit_layer_sync_host(edit_sync_t h, int32_t layer, void* local_hos
     for (int64_t x : h->numel) max_numel = std::max(max_numel, x);
     // per slot: anchor | momentum | local, each 256-byte aligned
     h->slot_bytes = align_up((size_t)max_numel * 4, 256) * 2 + align_up((size_t)max_numel * esz, 256);
-    CUDA_TRY(h, cudaMalloc(reinterpret_cast<void**>(&h->staging), 2 * h->slot_bytes));
+    CUDA_TRY(h, cudaMalloc(reinterpret_cast<void**>(&h->staging), edit_sync::kHostSlots * h->slot_bytes));
     CUDA_TRY(h, cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
     CUDA_TRY(h, cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < edit_sync::kHostSlots; ++i) {
       CUDA_TRY(h, cudaEventCreateWithFlags(&h->slot_in[i], cudaEventDisableTiming));
       CUDA_TRY(h, cudaEventCreateWithFlags(&h->slot_done[i], cudaEventDisableTiming));
       CUDA_TRY(h, cudaEventCreateWithFlags(&h->slot_free[i], cudaEventDisableTiming));
@@ -755,7 +756,7 @@ edit_status_t edit_layer_sync_host(edit_sync_t h, int32_t layer, void* local_hos
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int slot = h->next_slot;
-  h->next_slot ^= 1;
+  h->next_slot = (h->next_slot + 1) % edit_sync::kHostSlots;
   char* base = h->staging + (size_t)slot * h->slot_bytes;
   const size_t fbytes = align_up((size_t)std::max<int64_t>(n, 1) * 4, 256);
   float* anc = reinterpret_cast<float*>(base);
@@ -785,7 +786,7 @@ edit_status_t edit_sync_host_wait(edit_sync_t h, void* stream) {
   if (!h->staging) return EDIT_OK;
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  for (int i = 0; i < 2; ++i) CUDA_TRY(h, cudaStreamWaitEvent(st, h->slot_free[i], 0));
+  for (int i = 0; i < edit_sync::kHostSlots; ++i) CUDA_TRY(h, cudaStreamWaitEvent(st, h->slot_free[i], 0));
   return EDIT_OK;
 }
 
@@ -992,7 +993,7 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
     if (e) cudaEventDestroy(e);
   for (auto e : h->prof)
     if (e) cudaEventDestroy(e);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < edit_sync::kHostSlots; ++i) {
     if (h->slot_in[i]) cudaEventDestroy(h->slot_in[i]);
     if (h->slot_done[i]) cudaEventDestroy(h->slot_done[i]);
     if (h->slot_free[i]) cudaEventDestroy(h->slot_free[i]);
