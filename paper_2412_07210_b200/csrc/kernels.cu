@@ -202,7 +202,7 @@ __global__ void decide_kernel(DecideArgs p) {
 // ---------------------------------------------------------------- K4
 // beta (Eq. 4), then OuterOpt = Nesterov (R2) on (anchor, momentum) and the
 // write-back local = rne(anchor) (Alg. 2 l.454-455).  Rollback: local = rne(anchor).
-template <typename T, bool kFromS, int U, int I, bool kEF = false>
+template <typename T, bool kFromS, int U, int I, bool kEF = false, bool kG = false>
 __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
   T* __restrict__ local = static_cast<T*>(p.local);
   float* __restrict__ anchor = p.anchor;
@@ -245,14 +245,14 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
           float a[8];
           load8<kEF>(anchor + 8 * i, a, pol);
           store8<kEF>(local + 8 * i, a, pol);
-          gather_store8_t<kEF, T>(p, 8 * i, a, pol);
+          if (kG) gather_store8_t<kEF, T>(p, 8 * i, a, pol);
         }
       }
     }
     if (tail) {
       const int64_t k = 8 * n8 + threadIdx.x;
       store1(local + k, anchor[k]);
-      gather_store1_t<T>(p, k, anchor[k]);
+      if (kG) gather_store1_t<T>(p, k, anchor[k]);
     }
     return;
   }
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
         store8<kEF>(mom + 8 * i, m[u], pol);
         store8<kEF>(anchor + 8 * i, a[u], pol);
         store8<kEF>(local + 8 * i, a[u], pol);
-        gather_store8_t<kEF, T>(p, 8 * i, a[u], pol);
+        if (kG) gather_store8_t<kEF, T>(p, 8 * i, a[u], pol);
       }
     }
   }
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
     mom[k] = m1;
     anchor[k] = a1;
     store1(local + k, a1);
-    gather_store1_t<T>(p, k, a1);
+    if (kG) gather_store1_t<T>(p, k, a1);
   }
 }
 
@@ -365,8 +365,11 @@ int launch_decide(const DecideArgs& a, cudaStream_t st) {
 
 template <typename T, bool kFromS>
 void update_ef(bool ef, unsigned grid, cudaStream_t st, const UpdateArgs& a) {
-  if (ef) outer_update_kernel<T, kFromS, kUpdU, kUpdI, true><<<grid, kThreads, 0, st>>>(a);
-  else outer_update_kernel<T, kFromS, kUpdU, kUpdI, false><<<grid, kThreads, 0, st>>>(a);
+  const bool g = a.gather_M > 0;  // NEXT-2 stores compiled only into the gathering variants
+  if (ef && g) outer_update_kernel<T, kFromS, kUpdU, kUpdI, true, true><<<grid, kThreads, 0, st>>>(a);
+  else if (ef) outer_update_kernel<T, kFromS, kUpdU, kUpdI, true, false><<<grid, kThreads, 0, st>>>(a);
+  else if (g) outer_update_kernel<T, kFromS, kUpdU, kUpdI, false, true><<<grid, kThreads, 0, st>>>(a);
+  else outer_update_kernel<T, kFromS, kUpdU, kUpdI, false, false><<<grid, kThreads, 0, st>>>(a);
 }
 
 int launch_update(int dtype, const UpdateArgs& a, bool ef, int cap, cudaStream_t st) {

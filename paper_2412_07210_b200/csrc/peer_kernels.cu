@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_const
 }
 
 // ------------------------------------------------------------------------------ AG + update
-template <typename T, bool kEF>
+template <typename T, bool kEF, bool kG>
 __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs p,
                                                                      const __grid_constant__ PeerPtrs pp,
                                                                      Slicing sl, int K, int V) {
@@ -197,12 +197,12 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
       float a[8];
       load8<kEF>(anchor + 8 * i, a, pol);
       store8<kEF>(local + 8 * i, a, pol);
-      gather_store8_t<kEF, T>(p, 8 * i, a, pol);
+      if (kG) gather_store8_t<kEF, T>(p, 8 * i, a, pol);
     }
     if (blockIdx.x == 0 && threadIdx.x < (p.n & 7)) {
       const int64_t k = 8 * n8 + threadIdx.x;
       store1(local + k, anchor[k]);
-      gather_store1_t<T>(p, k, anchor[k]);
+      if (kG) gather_store1_t<T>(p, k, anchor[k]);
     }
     return;
   }
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
         store8<kEF>(mom + 8 * i, m, pol);
         store8<kEF>(anchor + 8 * i, a, pol);
         store8<kEF>(local + 8 * i, a, pol);
-        gather_store8_t<kEF, T>(p, 8 * i, a, pol);
+        if (kG) gather_store8_t<kEF, T>(p, 8 * i, a, pol);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.empty[s]);
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
     mom[k] = m1;
     anchor[k] = a1;
     store1(local + k, a1);
-    gather_store1_t<T>(p, k, a1);
+    if (kG) gather_store1_t<T>(p, k, a1);
   }
 }
 
@@ -397,8 +397,13 @@ int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anc
 
 template <typename T, bool kEF>
 void ag_go(unsigned grid, const Ring& r, cudaStream_t st, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl) {
-  set_smem(ag_update_tma_kernel<T, kEF>, r.K * r.stage_bytes);
-  ag_update_tma_kernel<T, kEF><<<grid, kPeerThreads, r.K * r.stage_bytes, st>>>(a, pp, sl, r.K, r.V);
+  if (a.gather_M > 0) {
+    set_smem(ag_update_tma_kernel<T, kEF, true>, r.K * r.stage_bytes);
+    ag_update_tma_kernel<T, kEF, true><<<grid, kPeerThreads, r.K * r.stage_bytes, st>>>(a, pp, sl, r.K, r.V);
+  } else {
+    set_smem(ag_update_tma_kernel<T, kEF, false>, r.K * r.stage_bytes);
+    ag_update_tma_kernel<T, kEF, false><<<grid, kPeerThreads, r.K * r.stage_bytes, st>>>(a, pp, sl, r.K, r.V);
+  }
 }
 
 int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl, int max_ctas,
