@@ -212,10 +212,11 @@ edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream);
  * shard group's reduce-scatter.  grad [layer_numel[layer]] param_dtype, device: this rank's
  * gradient shard of the unit, replaced in place by the MEAN over the N members of its sync
  * row, bit-identical on every member.  Collective over the sync row
- * (every rank calls it for the same units in the same order).  Peer path: the gradient is
- * staged (copied) into the IPC-exported buffer, each member averages its 1/N slice straight
- * from the others over NVLink, then pulls every averaged slice from its owner; NCCL path:
- * ncclAllReduce(ncclAvg).  N == 1: no-op. */
+ * (every rank calls it for the same units in the same order).  Default: ncclAllReduce
+ * (ncclAvg) on the library's sync comm -- a pure mean with nothing to fuse, where NCCL
+ * measured faster.  EDIT_WARMUP_ALGO=peer (with EDIT_ALGO_PEER): the gradient is staged into
+ * the IPC-exported buffer, each member averages its 1/N slice straight from the others over
+ * NVLink and rounds it once, then pulls every averaged slice from its owner.  N == 1: no-op. */
 edit_status_t edit_warmup_allreduce(edit_sync_t h, int32_t layer, void* grad, void* stream);
 
 /* Blocks until this unit's last enqueued sync has completed, then copies its

@@ -709,7 +709,12 @@ edit_status_t edit_warmup_allreduce(edit_sync_t h, int32_t layer, void* grad, vo
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Lane& ln = h->lanes[0];
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
-  if (!h->peer) {
+  // a pure mean (no compute to fuse): NCCL's all-reduce measured faster than the peer
+  // kernels (1x4 bf16 7B: 34.6 vs 54.1 ms; 2x2: 14.2 vs 16.3 ms, profiles/r1_bench_4gpu_final_*),
+  // so it is the default; EDIT_WARMUP_ALGO=peer selects the peer-memory variant
+  const char* wa = getenv("EDIT_WARMUP_ALGO");
+  const bool warm_peer = h->peer && wa && !strcmp(wa, "peer");
+  if (!warm_peer) {
     NCCL_TRY(h, ncclAllReduce(grad, grad, (size_t)n, dt == EDIT_BF16 ? ncclBfloat16 : ncclFloat32, ncclAvg,
                               ln.sync, st));
     return EDIT_OK;

@@ -40,7 +40,9 @@ def grad_of(u, i, M, m, n, dtype, dev):
 
 
 def warm_check(units, M, N, m_idx, n_idx, rank, world, dtype, dtype_s, dev, s, mesh, algo, local_rank):
-    """Warm-up gradient all-reduce (Alg. 1 l.422-424) vs the oracle's mean over the sync row."""
+    """Warm-up gradient all-reduce (Alg. 1 l.422-424) vs the oracle's mean over the sync row.
+    algo "peer" exercises the peer-memory variant (EDIT_WARMUP_ALGO=peer), "nccl" the default."""
+    os.environ["EDIT_WARMUP_ALGO"] = "peer" if algo == "peer" else "nccl"
     grads = [grad_of(u, i, M, m_idx, n_idx, dtype, dev) for i, u in enumerate(units)]
     for i in range(len(units)):
         s.warmup_allreduce(i, grads[i])
