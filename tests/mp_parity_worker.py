@@ -122,6 +122,16 @@ def run_case(mesh, dtype_s, config, algo="peer", api="unit"):
     if config == "warm":
         return warm_check(units, M, N, m_idx, n_idx, rank, world, dtype, dtype_s, dev, s, mesh, algo, local_rank)
     loc, anc, mom = inputs_of(units, M, m_idx, n_idx, dtype, dev, plant, recipe)
+    guards = []
+    if config == "ragged":
+        # guard zones around every buffer: no kernel (local or peer) may write outside a shard
+        G = 64
+        for lst in (loc, anc, mom):
+            for i, t in enumerate(lst):
+                big = torch.full((t.numel() + 2 * G,), 7.25, dtype=t.dtype, device=dev)
+                big[G:G + t.numel()].copy_(t)
+                guards.append((big, G, t.numel()))
+                lst[i] = big[G:G + t.numel()]
     if config == "nan" and n_idx == N - 1:
         loc[0][1234 % loc[0].numel()] = float("nan")   # replica N-1 has a NaN param (R9)
     full = None
@@ -140,6 +150,8 @@ def run_case(mesh, dtype_s, config, algo="peer", api="unit"):
             "anc": [x.cpu().numpy() for x in anc], "mom": [x.cpu().numpy() for x in mom],
             "stats": [s.stats(i) for i in range(len(units))],
             "full": [parity.to_oracle_local(f) for f in full] if full is not None else None}
+    for big, G, n_ in guards:
+        assert (big[:G] == 7.25).all() and (big[G + n_:] == 7.25).all(), f"rank {rank}: write outside a shard"
     # invariant: local == rne(anchor) bitwise on every rank (R16)
     for i in range(len(units)):
         assert torch.equal(loc[i], anc[i].to(dtype)), f"rank {rank} unit {i}: local != rne(anchor)"

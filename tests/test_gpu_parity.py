@@ -262,3 +262,26 @@ def test_round_api_matches_oracle_and_sequential_bitwise(dtype):
         parity.assert_f32_close(c.anchor[i].cpu().numpy(), anc[0], "round anchor")
         parity.assert_f32_close(c.mom[i].cpu().numpy(), mom[0], "round momentum")
         parity.assert_local_close(parity.to_oracle_local(c.local[i]), loc[0, 0], "round local")
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("numel", [1, 9, 1000, 65_543, 2_000_001])
+def test_no_writes_outside_the_shards(dtype, numel):
+    # guard zones around every buffer (compute-sanitizer is closed on this pool): the sync
+    # and the host-buffer path must not touch a single element outside [0, numel)
+    g = 64
+    dt = DTYPES[dtype]
+    units = [synth.Unit("u", numel, ())]
+    c = Case(units, dt)
+    guarded = []
+    for t in (c.local[0], c.anchor[0], c.mom[0]):
+        big = torch.full((numel + 2 * g,), 7.25, dtype=t.dtype, device=DEV)
+        big[g:g + numel].copy_(t)
+        guarded.append(big)
+    loc, anc, mom = (b[g:g + numel] for b in guarded)
+    c.sync.layer_sync(0, loc, anc, mom)
+    c.sync.sync_round([loc], [anc], [mom])
+    torch.cuda.synchronize()
+    for b in guarded:
+        assert (b[:g] == 7.25).all() and (b[g + numel:] == 7.25).all()
+    assert torch.equal(loc, anc.to(dt))
