@@ -149,6 +149,7 @@ def run_case(mesh, dtype_s, config, algo="peer", api="unit"):
     mine = {"rank": rank, "loc": [parity.to_oracle_local(x) for x in loc],
             "anc": [x.cpu().numpy() for x in anc], "mom": [x.cpu().numpy() for x in mom],
             "stats": [s.stats(i) for i in range(len(units))],
+            "ema": s.get_state(),
             "full": [parity.to_oracle_local(f) for f in full] if full is not None else None}
     for big, G, n_ in guards:
         assert (big[:G] == 7.25).all() and (big[G + n_:] == 7.25).all(), f"rank {rank}: write outside a shard"
@@ -160,6 +161,9 @@ def run_case(mesh, dtype_s, config, algo="peer", api="unit"):
     ok = True
     if rank == 0:
         by_rank = {g["rank"]: g for g in gathered}
+        # R6: every rank keeps all N replicas' EMA and updates them identically
+        for r in range(world):
+            assert np.array_equal(by_rank[r]["ema"], by_rank[0]["ema"]), f"EMA state of rank {r} differs"
         for i, u in enumerate(units):
             # regenerate every rank's inputs for unit i (seeded, rank-independent)
             locs, ancs, moms = [], [], []

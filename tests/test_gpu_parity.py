@@ -285,3 +285,28 @@ def test_no_writes_outside_the_shards(dtype, numel):
     for b in guarded:
         assert (b[:g] == 7.25).all() and (b[g + numel:] == 7.25).all()
     assert torch.equal(loc, anc.to(dt))
+
+
+def test_ema_checkpoint_resume_roundtrip():
+    # edit_sync_get_state / set_state: a resumed handle continues exactly like the original
+    units = [synth.Unit("a", 100_003, ()), synth.Unit("b", 4099, ())]
+    a = Case(units, torch.bfloat16)
+    a.run_and_check("r1")
+    state = a.sync.get_state()
+    assert (state["count"] == 1).all()
+    b = EditSync([u.numel for u in units], param_dtype=torch.bfloat16, device=DEV)
+    b.set_state(state)
+    assert np.array_equal(b.get_state(), state)
+    a.new_round(1)
+    locs = [l.clone() for l in a.local]
+    ancs = [x.clone() for x in a.anchor]
+    moms = [x.clone() for x in a.mom]
+    for i in range(len(units)):
+        b.layer_sync(i, locs[i], ancs[i], moms[i])
+    a.run_and_check("r2")
+    torch.cuda.synchronize()
+    for i in range(len(units)):
+        assert torch.equal(locs[i], a.local[i]) and torch.equal(ancs[i], a.anchor[i])
+        sa, sb = a.sync.stats(i), b.stats(i)
+        assert (sa.G == sb.G).all() and sa.beta == sb.beta and (sa.ema_mu == sb.ema_mu).all()
+    assert np.array_equal(a.sync.get_state()[["mu", "sigma", "count"]], b.get_state()[["mu", "sigma", "count"]])
