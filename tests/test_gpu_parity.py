@@ -309,4 +309,6 @@ def test_ema_checkpoint_resume_roundtrip():
         assert torch.equal(locs[i], a.local[i]) and torch.equal(ancs[i], a.anchor[i])
         sa, sb = a.sync.stats(i), b.stats(i)
         assert (sa.G == sb.G).all() and sa.beta == sb.beta and (sa.ema_mu == sb.ema_mu).all()
-    assert np.array_equal(a.sync.get_state()[["mu", "sigma", "count"]], b.get_state()[["mu", "sigma", "count"]])
+    sa_, sb_ = a.sync.get_state(), b.get_state()
+    for f in ("mu", "sigma", "count"):
+        assert np.array_equal(sa_[f], sb_[f])
