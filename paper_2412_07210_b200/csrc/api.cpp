@@ -127,6 +127,11 @@ struct Lane {
   float* Down = nullptr;
   PeerPtrs pp{};
   std::vector<void*> opened;  // IPC mappings to close
+  // device-side scalar exchange (EDIT_XCHG=nccl disables): own mailbox, all ranks' mapped
+  unsigned long long* mailbox = nullptr;
+  MailPtrs mp{};
+  unsigned long long seq[kXchgPhases] = {0, 0};
+  int* xerr = nullptr;
 };
 
 struct edit_sync {
@@ -139,6 +144,7 @@ struct edit_sync {
   bool peer = false;             // N > 1 and algo == EDIT_ALGO_PEER
   int peer_ctas = 148;           // persistent grid of the peer kernels (EDIT_PEER_CTAS env overrides)
   int peer_tile = kPeerTileVec;  // vectors per TMA tile (EDIT_PEER_TILE env; must match on all ranks)
+  bool dev_xchg = true;          // scalar chain over NVLink mailboxes (EDIT_XCHG=nccl: NCCL gathers)
   bool ef_direct = false;        // L2 evict_first streaming for edit_layer_sync / edit_sync_round
   bool ef_sched = false;         // ... for the prefetch scheduler (a forward runs concurrently)
   // scheduler (co-resident) mode: at most sched_ctas CTAs per streaming kernel, each small
@@ -182,6 +188,12 @@ struct edit_sync {
   bool poisoned = false;
   int64_t launches = 0;
 };
+
+extern "C" {
+static edit_status_t exchange_ipc(edit_sync_t h, void* const* ptrs, const size_t* bytes, int L, ncclComm_t comm,
+                                  int P, int me, cudaStream_t st, std::vector<std::vector<void*>>& out,
+                                  std::vector<void*>& opened);
+}
 
 namespace {
 
@@ -274,6 +286,7 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
   INIT_CUDA(cudaSetDevice(cfg->device));
   INIT_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
   h->peer_ctas = h->num_sms;
+  if (const char* e = getenv("EDIT_XCHG")) h->dev_xchg = strcmp(e, "nccl") != 0;
   if (const char* e = getenv("EDIT_PEER_TILE")) {
     const int v = atoi(e);
     if (v >= 32 && v <= 4096 && (v & 31) == 0) h->peer_tile = v;
@@ -348,6 +361,19 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
     // sync group (row): same shard index m, ordered by n; shard group (column): same n.
     INIT_NCCL(ncclCommSplit(ln.global, h->shard_idx, h->sync_idx, &ln.sync, nullptr));
     INIT_NCCL(ncclCommSplit(ln.global, h->sync_idx, h->shard_idx, &ln.shard, nullptr));
+    if (h->dev_xchg) {
+      INIT_CUDA(cudaMalloc(reinterpret_cast<void**>(&ln.mailbox), align_up(mailbox_bytes(K), 256)));
+      INIT_CUDA(cudaMemset(ln.mailbox, 0, align_up(mailbox_bytes(K), 256)));
+      INIT_CUDA(cudaMalloc(reinterpret_cast<void**>(&ln.xerr), sizeof(int)));
+      INIT_CUDA(cudaMemset(ln.xerr, 0, sizeof(int)));
+      INIT_CUDA(cudaDeviceSynchronize());
+      void* mine = ln.mailbox;
+      size_t mb = mailbox_bytes(K);
+      std::vector<std::vector<void*>> boxes;
+      edit_status_t rc = exchange_ipc(h, &mine, &mb, 1, ln.global, K, cfg->rank, ln.stream, boxes, ln.opened);
+      if (rc != EDIT_OK) return bail(rc);
+      for (int r = 0; r < K; ++r) ln.mp.box[r] = static_cast<unsigned long long*>(boxes[0][r]);
+    }
     if (h->peer) {
       const Slicing sl = slicing_of(max_numel, h->N, 0, h->peer_tile);
       INIT_CUDA(cudaMalloc(&ln.Lown, align_up((size_t)std::max<int64_t>(max_numel, 8) * esz, 256)));
@@ -440,7 +466,12 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
   // module norms of every replica on every rank: one K-scalar gather (R6)
   const double* parts = &scr->send1;
   if (h->K > 1) {
-    NCCL_TRY(h, ncclAllGather(&scr->send1, scr->recv1, 1, ncclFloat64, ln.global, st));
+    if (ln.mailbox) {
+      launched += launch_xchg(ln.mp, h->K, h->cfg.rank, 0, ++ln.seq[0], &scr->send1, scr->recv1, ln.xerr, st);
+      CUDA_TRY(h, cudaGetLastError());
+    } else {
+      NCCL_TRY(h, ncclAllGather(&scr->send1, scr->recv1, 1, ncclFloat64, ln.global, st));
+    }
     parts = scr->recv1;
   }
   DecideArgs d{};
@@ -488,7 +519,12 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
     // ||Dbar||^2 of the module = sum over every slice of every shard: one K-scalar gather
     // (also the barrier after which every member's D slice is complete)
-    NCCL_TRY(h, ncclAllGather(&scr->send2, scr->recv2, 1, ncclFloat64, ln.global, st));
+    if (ln.mailbox) {
+      launched += launch_xchg(ln.mp, h->K, h->cfg.rank, 1, ++ln.seq[1], &scr->send2, scr->recv2, ln.xerr, st);
+      CUDA_TRY(h, cudaGetLastError());
+    } else {
+      NCCL_TRY(h, ncclAllGather(&scr->send2, scr->recv2, 1, ncclFloat64, ln.global, st));
+    }
     if (ev) CUDA_TRY(h, cudaEventRecord(ev[4], st));
     u.gparts = scr->recv2;
     u.n_gparts = h->K;
@@ -880,6 +916,14 @@ edit_status_t edit_sync_stats(edit_sync_t h, int32_t layer, edit_layer_stats_t* 
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   CUDA_TRY(h, cudaEventSynchronize(h->done[layer]));
   for (Lane& ln : h->lanes) {
+    if (ln.xerr) {
+      int e = 0;
+      CUDA_TRY(h, cudaMemcpy(&e, ln.xerr, sizeof e, cudaMemcpyDeviceToHost));
+      if (e) {
+        h->poisoned = true;
+        return fail(EDIT_ERR_STATE, "device scalar exchange timed out (a peer rank stopped syncing)");
+      }
+    }
     if (!ln.global) continue;
     ncclResult_t async_err = ncclSuccess;
     NCCL_TRY(h, ncclCommGetAsyncError(ln.global, &async_err));
@@ -965,7 +1009,7 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
   edit_status_t st = EDIT_OK;
   cudaSetDevice(h->cfg.device);
   if (!h->poisoned) cudaDeviceSynchronize();
-  if ((h->peer || !h->reg_gather.empty()) && h->ready && !h->poisoned && !h->lanes.empty() &&
+  if ((h->peer || !h->reg_gather.empty() || h->dev_xchg) && h->ready && !h->poisoned && !h->lanes.empty() &&
       h->lanes[0].global) {
     // barrier: no member may free its IPC-exported buffers while a peer still reads them
     double* tmpd = nullptr;
@@ -986,6 +1030,8 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
     if (ln.Lown) cudaFree(ln.Lown);
     if (ln.Down) cudaFree(ln.Down);
     if (ln.S) cudaFree(ln.S);
+    if (ln.mailbox) cudaFree(ln.mailbox);
+    if (ln.xerr) cudaFree(ln.xerr);
     if (ln.shard) ncclCommDestroy(ln.shard);
     if (ln.sync) ncclCommDestroy(ln.sync);
     if (ln.global) ncclCommDestroy(ln.global);

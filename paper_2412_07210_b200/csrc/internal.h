@@ -107,6 +107,19 @@ inline Slicing slicing_of(int64_t n, int N, int me, int tile = kPeerTileVec) {
   return s;
 }
 
+// Device-side scalar exchange over NVLink (replaces the tiny NCCL all-gathers of the scalar
+// chain): every rank's mailbox, mapped in every rank through CUDA IPC.
+// Slot layout: box[((phase * 2 + (seq & 1)) * K + src) * 2 + {0: value bits, 1: seq}].
+constexpr int kXchgPhases = 2;
+struct MailPtrs {
+  unsigned long long* box[kMaxRanks];
+};
+inline size_t mailbox_bytes(int K) { return sizeof(unsigned long long) * 2 * 2 * kXchgPhases * (size_t)K; }
+// out[r] = rank r's *src for r < K.  One CTA; spins (bounded: ~10 s, then *err = 1) only in
+// this kernel, never in the big streaming kernels -> no cross-lane starvation.
+int launch_xchg(const MailPtrs& mp, int K, int me, int phase, unsigned long long seq, const double* src,
+                double* out, int* err, cudaStream_t st);
+
 // Launchers (kernels.cu).  Each returns the number of kernels launched.
 // cta_parts: grid_of(n, kVecReduce) fp64 slots for the per-CTA partials.
 // ef: stream with an L2 evict_first policy (device_common.cuh).  cap > 0: at most `cap` CTAs

@@ -336,6 +336,41 @@ __global__ void __launch_bounds__(kThreads) warm_ag_kernel(const __grid_constant
   }
 }
 
+// ------------------------------------------------------------------------------ scalar exchange
+// Publish this rank's scalar into every rank's mailbox (value, then seq with release
+// semantics at system scope), then wait for all K senders in its own mailbox (acquire).
+// Slots alternate by seq parity: a rank can only write seq+2 into a slot after the reader
+// published seq+1, i.e. after it finished reading seq -- no slot is overwritten early.
+__global__ void xchg_kernel(const __grid_constant__ MailPtrs mp, int K, int me, int phase,
+                            unsigned long long seq, const double* src, double* out, int* err) {
+  const int t = threadIdx.x;
+  const int base = (phase * 2 + (int)(seq & 1)) * K;
+  if (t < K) {
+    const double v = *src;
+    unsigned long long* slot = mp.box[t] + 2 * (base + me);
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(slot), "l"((unsigned long long)__double_as_longlong(v))
+                 : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot + 1), "l"(seq) : "memory");
+  }
+  if (t < K) {
+    unsigned long long* slot = mp.box[me] + 2 * (base + t);
+    unsigned long long s = 0, t0, now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(s) : "l"(slot + 1) : "memory");
+      if (s == seq) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > 10000000000ull) {  // 10 s: a peer is gone; fail loudly instead of hanging
+        atomicExch(err, 1);
+        break;
+      }
+    }
+    unsigned long long vb;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(vb) : "l"(slot) : "memory");
+    out[t] = __longlong_as_double((long long)vb);
+  }
+}
+
 int default_smem_budget() {
   static int b = [] {
     const char* e = getenv("EDIT_PEER_SMEM_KB");  // shared-memory ring per CTA (default 200 KB)
@@ -418,6 +453,12 @@ int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const S
     if (ef) ag_go<float, true>(grid, r, st, a, pp, sl);
     else ag_go<float, false>(grid, r, st, a, pp, sl);
   }
+  return 1;
+}
+
+int launch_xchg(const MailPtrs& mp, int K, int me, int phase, unsigned long long seq, const double* src,
+                double* out, int* err, cudaStream_t st) {
+  xchg_kernel<<<1, 64, 0, st>>>(mp, K, me, phase, seq, src, out, err);
   return 1;
 }
 
