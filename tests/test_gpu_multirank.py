@@ -36,7 +36,22 @@ GATHER_CASES = [("2x1", "bf16", "ragged"), ("2x2", "f32", "toy"), ("4x1", "bf16"
                 ("2x2", "bf16", "rollback"), ("2x4", "bf16", "ragged"), ("4x2", "f32", "toy")]
 
 
+def _core_cases(mesh):
+    """The default subset (every feature once per mesh); EDIT_TEST_FULL=1 runs every case."""
+    M, N = (int(x) for x in mesh.split("x"))
+    c = [("bf16", "ragged", "peer", "unit"), ("f32", "toy", "nccl", "unit"), ("bf16", "nan", "peer", "round"),
+         ("f32", "toy_clip", "peer", "unit")]
+    if N > 1:
+        c += [("bf16", "ragged", "peer", "reg"), ("bf16", "warm", "peer", "unit"), ("bf16", "rollback", "nccl", "round")]
+    if M > 1:
+        c += [("bf16", "ragged", "peer", "gather")]
+    return c
+
+
 def _mesh_cases():
+    if not os.environ.get("EDIT_TEST_FULL"):
+        meshes = sorted({m for m, *_ in UNIT_CASES + ROUND_CASES + REG_CASES + WARM_CASES + GATHER_CASES})
+        return {m: _core_cases(m) for m in meshes}
     by_mesh = defaultdict(list)
     for algo in ALGOS:
         for mesh, dt, cfg in UNIT_CASES:
