@@ -207,7 +207,8 @@ def run_case(mesh, dtype_s, config, algo="peer", api="unit"):
             if config == "toy_clip":
                 assert out.beta < 1.0
             if config == "nan" and i == 0:
-                assert out.anomalous[N - 1] and not out.rollback
+                # the replica with a NaN param is excluded; alone (N == 1) that is a rollback
+                assert out.anomalous[N - 1] and out.rollback == (N == 1)
         print(f"PARITY OK {config} {mesh} {dtype_s} {algo} {api}: {len(units)} units", flush=True)
     s.close()
     dist.barrier(device_ids=[local_rank])
