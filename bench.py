@@ -358,6 +358,28 @@ def main() -> None:
         b_nvl = 6.0 * (N - 1) / N if b_l == 2 else 8.0 * (N - 1) / N  # bytes the peer path moves
     t_roof_nom = max(P_r * b_hbm / (NOMINAL_HBM_GBS * 1e9), P_r * (8.0 * (N - 1) / N) / (NOMINAL_NVL_GBS * 1e9)) * 1e3
     t_roof_meas = max(P_r * b_hbm / (hbm_peak * 1e9), P_r * (8.0 * (N - 1) / N) / (MEASURED_NVL_GBS * 1e9)) * 1e3
+    # the bytes THIS dataflow must move per param (not the algorithmic minimum), bf16 local:
+    # N == 1: 6 + 20 = 26; peer path: 6 (+2 staging copy unless registered) + RS (2 + 8/N) +
+    # AG 22 in HBM and 6(N-1)/N over NVLink; the NCCL path is not modelled
+    design = None
+    if N == 1:
+        d_hbm, d_nvl = (b_l + 4) + (16 + 2 * b_l), 0.0                      # K1 + K4
+    elif peer:
+        # K1 (+ staging copy) + RS (anchor + local slices, served peer reads, Dbar slice) +
+        # AG (Dbar own + served, anchor, momentum in; momentum, anchor, local out)
+        d_hbm = (b_l + 4) + (0 if registered else b_l) + (b_l + 8.0 / N) + (20 + b_l)
+        d_nvl = (b_l + 4) * (N - 1) / N
+    else:
+        d_hbm = d_nvl = None
+    if d_hbm is not None:
+        nvl_bidir = 673.0  # measured: two GPUs pulling from each other (profiles/r1_a2a_peer_pull_2gpu.txt)
+        t_bound = max(P_r * d_hbm / (hbm_peak * 1e9), P_r * d_nvl / (nvl_bidir * 1e9)) * 1e3
+        design = {"hbm_B_per_param": d_hbm, "nvlink_B_per_param_per_dir": d_nvl,
+                  "hbm_achieved_GBps": P_r * d_hbm / (ms_per_step * 1e-3) / 1e9,
+                  "nvlink_achieved_GBps": P_r * d_nvl / (ms_per_step * 1e-3) / 1e9,
+                  "t_bound_ms": t_bound, "frac": t_bound / ms_per_step,
+                  "peaks": f"HBM {hbm_peak} GB/s (MEASURED_PEAKS), NVLink {nvl_bidir} GB/s per direction "
+                           "bidirectional (measured)"}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -550,6 +572,7 @@ def main() -> None:
                 "pg_norm": {"bytes_per_param": k1_B, "achieved": k1_iso, "peak": hbm_peak,
                             "frac": (k1_iso / hbm_peak) if k1_iso else None},
                 "phases_ms_per_round": {k: v / 2 for k, v in iso_ms.items()}},
+            "design_bound": design,
             "sync_roofline": {"t_roof_ms_nominal": t_roof_nom, "frac_nominal": t_roof_nom / ms_per_step,
                               "t_roof_ms_measured": t_roof_meas, "frac_measured": t_roof_meas / ms_per_step,
                               "bound": "hbm" if N == 1 else "nvlink", "hbm_B_per_param": b_hbm,
