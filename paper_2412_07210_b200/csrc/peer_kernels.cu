@@ -30,7 +30,10 @@ namespace edit {
 namespace {
 using namespace dev;
 
-constexpr int kConsumerWarps = 8;
+#ifndef EDIT_CONSUMER_WARPS
+#define EDIT_CONSUMER_WARPS 8
+#endif
+constexpr int kConsumerWarps = EDIT_CONSUMER_WARPS;
 constexpr int kPeerThreads = 32 * (1 + kConsumerWarps);  // warp 0 = producer
 constexpr int kSmemBudget = 200 * 1024;
 
@@ -235,22 +238,31 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
       const int s = it % K, use = it / K;
       mbar_wait(&bars.full[s], use & 1);
       const float* st = reinterpret_cast<const float*>(smem + (size_t)s * stage_bytes);
-      for (int v = t; v < nv; v += 32 * kConsumerWarps) {
-        float d[8], a[8], m[8];
-        load8(st + 8 * v, d);
-        load8(st + V * 8 + 8 * v, a);
-        load8(st + V * 16 + 8 * v, m);
+      constexpr int NT = 32 * kConsumerWarps, CU = EDIT_CONSUMER_UNROLL;
+      for (int v = t; v < nv; v += CU * NT) {
+        float d[CU][8], a[CU][8], m[CU][8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float g = beta * d[k];             // Eq. 5
-          m[k] = fmaf(mu, m[k], g);                // m' = mu m + g
-          a[k] = a[k] - nu * fmaf(mu, m[k], g);    // a' = a - nu (g + mu m')
-        }
-        const int64_t i = v0 + v;
-        store8<kEF>(mom + 8 * i, m, pol);
-        store8<kEF>(anchor + 8 * i, a, pol);
-        store8<kEF>(local + 8 * i, a, pol);
-        if (kG) gather_store8_t<kEF, T>(p, 8 * i, a, pol);
+        for (int c = 0; c < CU; ++c)  // all shared-memory loads of the CU vectors first
+          if (v + c * NT < nv) {
+            load8(st + 8 * (v + c * NT), d[c]);
+            load8(st + V * 8 + 8 * (v + c * NT), a[c]);
+            load8(st + V * 16 + 8 * (v + c * NT), m[c]);
+          }
+#pragma unroll
+        for (int c = 0; c < CU; ++c)
+          if (v + c * NT < nv) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const float g = beta * d[c][k];                // Eq. 5
+              m[c][k] = fmaf(mu, m[c][k], g);                // m' = mu m + g
+              a[c][k] = a[c][k] - nu * fmaf(mu, m[c][k], g);  // a' = a - nu (g + mu m')
+            }
+            const int64_t i = v0 + v + c * NT;
+            store8<kEF>(mom + 8 * i, m[c], pol);
+            store8<kEF>(anchor + 8 * i, a[c], pol);
+            store8<kEF>(local + 8 * i, a[c], pol);
+            if (kG) gather_store8_t<kEF, T>(p, 8 * i, a[c], pol);
+          }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.empty[s]);
