@@ -34,6 +34,9 @@ using namespace dev;
 #define EDIT_CONSUMER_WARPS 8
 #endif
 constexpr int kConsumerWarps = EDIT_CONSUMER_WARPS;
+#ifndef EDIT_CONSUMER_UNROLL
+#define EDIT_CONSUMER_UNROLL 1  // measured neutral (tools/peer_kbench.cu, 8/16 warps x 1/2)
+#endif
 constexpr int kPeerThreads = 32 * (1 + kConsumerWarps);  // warp 0 = producer
 constexpr int kSmemBudget = 200 * 1024;
 
