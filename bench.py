@@ -385,7 +385,7 @@ def main() -> None:
     if os.path.exists(tpath):
         with open(tpath) as f:
             tinfo = json.load(f)
-        key = f"outer_update_{args.dtype}_{'S' if N > 1 else 'local'}"
+        key = (f"ag_update_{args.dtype}" if peer else f"outer_update_{args.dtype}_{'S' if N > 1 else 'local'}")
         if key in tinfo:
             traffic = tinfo[key]["dram_bytes_per_elem"] * k4_elems / k4_launches
 

@@ -23,7 +23,8 @@ SCALE = {"us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1.0, "Gbyte": 1e9, "Mbyte": 1e
 
 
 def key_of(name: str) -> str:
-    m = re.search(r"(pg_norm_kernel|outer_update_kernel|sumsq_kernel|decide_kernel)<?([^>]*)>?", name)
+    m = re.search(r"(pg_norm_kernel|outer_update_kernel|sumsq_kernel|decide_kernel|ag_update_tma_kernel|rs_tma_kernel)"
+                  r"<?([^>]*)>?", name)
     if not m:
         return name[:40]
     base = m.group(1).replace("_kernel", "")
@@ -33,6 +34,8 @@ def key_of(name: str) -> str:
     flag = parts[1] if len(parts) > 1 else ""
     if base == "outer_update":
         return f"outer_update_{dt}_{'S' if flag in ('1', 'true') else 'local'}"
+    if base in ("ag_update_tma", "rs_tma"):
+        return f"{base.replace('_tma', '')}_{dt}"
     if base == "pg_norm":
         return f"pg_norm_{dt}_{'S' if flag in ('1', 'true') else 'noS'}"
     return base
