@@ -201,7 +201,9 @@ def main() -> None:
     ap.add_argument("--mesh", default=None, help="MxN shard x sync mesh (default 1xN)")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--algo", default="peer", choices=["peer", "nccl"], help="N > 1 exchange of Eq. 3")
-    ap.add_argument("--e2e-units", default="1,2,3,4,5,6", help="unit indices timed through the host-buffer API")
+    ap.add_argument("--e2e-units", default=None,
+                    help="unit indices timed through the host-buffer API (default 1..6, or 1..3 at >= 4 GPUs "
+                         "to bound the pinned host memory of the node)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=4_000_000)
@@ -512,7 +514,8 @@ def main() -> None:
     # local/anchor/momentum and D2H of the three results inside the timed region)
     e2e = None
     if not args.no_e2e:
-        idx = [int(x) for x in args.e2e_units.split(",") if x.strip()]
+        spec = args.e2e_units or ("1,2,3,4,5,6" if world <= 2 else "1,2,3")
+        idx = [int(x) for x in spec.split(",") if x.strip()]
         h_loc = [locs[i].cpu().pin_memory() for i in idx]
         h_anc = [anchors[i].cpu().pin_memory() for i in idx]
         h_mom = [moms[i].cpu().pin_memory() for i in idx]
