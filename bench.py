@@ -115,8 +115,12 @@ class Clocks:
         mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        pw = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
+        capped = sum(1 for r in rows if r[8].lower() == "active")
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows),
+                "power_w": statistics.median(pw) if pw else None,
+                "power_cap_frac": capped / len(rows)}
 
 
 def oracle_cpu_baseline(model: str, dtype, target_s: float = 12.0) -> dict:
@@ -207,8 +211,13 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=4_000_000)
-    ap.add_argument("--overlap-tokens", type=int, default=8192,
-                    help="tokens/GPU of the synthetic forward for the prefetch-overlap measurement (0 = skip)")
+    ap.add_argument("--overlap-tokens", default="8192,65536",
+                    help="tokens/GPU of the synthetic forward(s) for the prefetch-overlap measurement, comma "
+                         "list (0 = skip); 8,192 = SURVEY 8d default, 65,536 = the paper's 1024 seqs x 4096 / 64")
+    ap.add_argument("--partition", default="0,16",
+                    help="scheduler partition modes to measure (comma list of SM counts; 0 = full grids)")
+    ap.add_argument("--full-units", type=int, default=2,
+                    help="partition mode: units before this index keep full grids (embedding + first layer)")
     ap.add_argument("--overlap-steps", type=int, default=3)
     ap.add_argument("--warmup-allreduce", action="store_true", help="NEXT-3 measurement (N > 1)")
     ap.add_argument("--gather", action="store_true", help="NEXT-2 fused shard all-gather measurement (M > 1)")
@@ -391,11 +400,21 @@ def main() -> None:
         if key in tinfo:
             traffic = tinfo[key]["dram_bytes_per_elem"] * k4_elems / k4_launches
 
-    # a8: layer-wise prefetch -- hidden fraction h = 1 - (t_fwd+sync - t_fwd) / t_sync
+    # a8: layer-wise prefetch -- hidden fraction h = 1 - (t_fwd+sync - t_fwd) / t_sync,
+    # t_sync = the full-speed round alone; swept over forward sizes and partition modes
     overlap = None
-    if args.overlap_tokens > 0:
+    tokens_list = [int(x) for x in str(args.overlap_tokens).split(",") if int(x) > 0]
+    parts = [int(x) for x in str(args.partition).split(",")]
+    if tokens_list:
         from synth.forward import SyntheticForward
-        fwd = SyntheticForward(args.model, units, args.overlap_tokens, dev)
+
+        def timed_clk(fn, nsteps, redraw_first=True):
+            c = Clocks(local_rank)
+            with c:
+                t = timed(fn, nsteps, redraw_first)
+            k = c.summary()
+            return t, {"sm_mhz": k["sm_mhz"], "power_w": k.get("power_w"),
+                       "power_cap_frac": k.get("power_cap_frac"), "samples": k["samples"]}
 
         def timed(fn, nsteps, redraw_first=True):
             ts = []
@@ -414,29 +433,64 @@ def main() -> None:
                     ts.append(t)
             return sum(ts) / len(ts)
 
-        def forward_only():
+        t_sync_alone, clk_sync = timed_clk(run_round, args.overlap_steps)
+
+        def sched_only():                       # the scheduled round with no forward
+            sync.begin_round(locs, anchors, moms, 1, stream)
             for u in range(len(units)):
-                fwd.unit(u, locs[u])
+                sync.acquire(u, stream)
+            sync.end_round(stream)
 
-        def fwd_and_sync(depth):
-            def run():
-                sync.begin_round(locs, anchors, moms, depth, stream)
+        t_sync_sched = {}
+        for sms in parts:                       # the partitioned sync alone, per SM count
+            sync.set_partition(sms, args.full_units)
+            t, k = timed_clk(sched_only, args.overlap_steps)
+            t_sync_sched[str(sms)] = {"ms": t, "clocks": k}
+        sync.set_partition(0, args.full_units)
+        runs = []
+        for tokens in tokens_list:
+            fwd = SyntheticForward(args.model, units, tokens, dev)
+
+            def forward_only():
                 for u in range(len(units)):
-                    sync.acquire(u, stream)
                     fwd.unit(u, locs[u])
-                sync.end_round(stream)
-            return run
 
-        t_fwd = timed(forward_only, args.overlap_steps, redraw_first=False)
-        t_sync_alone = timed(run_round, args.overlap_steps)
-        overlap = {"tokens_per_gpu": args.overlap_tokens, "t_fwd_ms": t_fwd, "t_sync_ms": t_sync_alone,
-                   "fwd_tflops": fwd.flops_per_round() / (t_fwd * 1e-3) / 1e12, "by_depth": {}}
-        for depth in (1, 2):
-            t_both = timed(fwd_and_sync(depth), args.overlap_steps)
-            overlap["by_depth"][str(depth)] = {"t_fwd_plus_sync_ms": t_both,
-                                               "hidden_fraction": 1.0 - (t_both - t_fwd) / t_sync_alone}
-        overlap["note"] = ("synthetic forward (bf16 GEMMs of each unit, weights = the synced local) on the "
-                           "compute stream; syncs on the library's side stream; acquire(u) before forward(u)")
+            def fwd_and_sync(depth):
+                def run():
+                    sync.begin_round(locs, anchors, moms, depth, stream)
+                    for u in range(len(units)):
+                        sync.acquire(u, stream)
+                        fwd.unit(u, locs[u])
+                    sync.end_round(stream)
+                return run
+
+            t_fwd, clk_fwd = timed_clk(forward_only, args.overlap_steps, redraw_first=False)
+            for sms in parts:
+                sync.set_partition(sms, args.full_units)
+                for depth in (1, 2):
+                    t_both, clk_both = timed_clk(fwd_and_sync(depth), args.overlap_steps)
+                    runs.append({"tokens_per_gpu": tokens, "partition_sms": sms, "depth": depth,
+                                 "t_fwd_ms": t_fwd, "t_fwd_plus_sync_ms": t_both,
+                                 "clocks_fwd": clk_fwd, "clocks_fwd_plus_sync": clk_both,
+                                 "fwd_tflops": fwd.flops_per_round() / (t_fwd * 1e-3) / 1e12,
+                                 "hidden_fraction": 1.0 - (t_both - t_fwd) / t_sync_alone})
+            sync.set_partition(0, args.full_units)
+            del fwd
+            torch.cuda.empty_cache()
+        best = {}
+        for r in runs:
+            k = r["tokens_per_gpu"]
+            if k not in best or r["hidden_fraction"] > best[k]["hidden_fraction"]:
+                best[k] = r
+        head = best[tokens_list[0]]
+        overlap = {"tokens_per_gpu": head["tokens_per_gpu"], "t_sync_ms": t_sync_alone, "clocks_sync": clk_sync,
+                   "t_sync_sched_alone_ms_by_partition": t_sync_sched,
+                   "t_fwd_ms": head["t_fwd_ms"], "best": {str(k): v for k, v in best.items()}, "runs": runs,
+                   "full_units": args.full_units,
+                   "note": ("synthetic forward (bf16 GEMMs of each unit, weights = the synced local) on the "
+                            "compute stream; syncs on the library's side streams; acquire(u) before forward(u); "
+                            "partition_sms > 0: edit_sched_set_partition (units >= full_units on that many "
+                            "persistent TMA CTAs, one per SM); h = 1 - (t_fwd+sync - t_fwd) / t_sync_alone")}
 
     # NEXT-3: warm-up gradient all-reduce (mean over the sync group) of a full set of bf16
     # gradient shards, library path vs torch.distributed/NCCL all_reduce on the same group

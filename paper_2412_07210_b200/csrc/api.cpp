@@ -152,6 +152,11 @@ struct edit_sync {
   // (default 0 = full grids: measured, capping does not buy overlap on B200 -- DESIGN.md 7)
   int sched_ctas = 0;
   int sched_smem_kb = 18;
+  // partition mode (edit_sched_set_partition): scheduled units u >= sched_full_units run
+  // as persistent TMA pipelines on sched_part CTAs (one per SM), lanes at high priority
+  int sched_part = 0;
+  int sched_full_units = 2;
+  int lane_prio = 0;             // priority the lanes were created with (env default)
   bool ready = false;            // init completed (destroy may then barrier with the peers)
   char* ws = nullptr;
   LayerScratch* scratch = nullptr;
@@ -341,6 +346,7 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
     if (!strcmp(e, "high")) prio = prio_hi;
     else if (!strcmp(e, "normal")) prio = 0;
   }
+  h->lane_prio = prio;
   h->lanes.resize(nlanes);
   h->peer = h->N > 1 && cfg->algo == EDIT_ALGO_PEER;
   int64_t max_numel = 0;
@@ -436,6 +442,7 @@ struct Mode {
   int cap;        // max CTAs of the LDG streaming kernels (0 = full grid)
   int peer_ctas;  // persistent grid of the TMA peer kernels
   int smem_kb;    // shared-memory ring of the TMA peer kernels (0 = default)
+  int part = 0;   // > 0: partition mode, K1 / K4 / peer kernels on <= part persistent CTAs
 };
 
 static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* local, float* anchor, float* momentum,
@@ -457,7 +464,9 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
   PeerPtrs pp = ln.pp;
   if (direct)
     for (int j = 0; j < N; ++j) pp.L[j] = h->reg_peer[layer][j];
-  if (h->peer && !direct)
+  if (mode.part > 0 && !S && (!h->peer || direct))
+    launched += launch_pg_norm_tma(dt, local, anchor, n, scr, h->part1[layer], mode.part, st);
+  else if (h->peer && !direct)
     launched += launch_pg_norm_copy(dt, local, anchor, ln.Lown, n, scr, h->part1[layer], ef, mode.cap, st);
   else
     launched += launch_pg_norm(dt, local, anchor, S, n, scr, h->part1[layer], ef, mode.cap, st);
@@ -550,7 +559,10 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
     u.gparts = &scr->gsq;
     u.n_gparts = 1;
   }
-  if (!h->peer) launched += launch_update(dt, u, ef, mode.cap, st);
+  if (!h->peer) {
+    if (mode.part > 0 && !u.dbar && !gathered) launched += launch_update_tma(dt, u, mode.part, st);
+    else launched += launch_update(dt, u, ef, mode.cap, st);
+  }
   CUDA_TRY(h, cudaGetLastError());
   if (gathered) {
     // every member of the shard group has stored its shard into every gathered module once
@@ -834,9 +846,16 @@ edit_status_t edit_sync_host_wait(edit_sync_t h, void* stream) {
 static edit_status_t sched_enqueue_next(edit_sync_t h) {
   const int u = h->sched_next_sync++;
   Lane& ln = h->lanes[u % h->lanes.size()];
-  return sync_unit(h, ln, u, h->sched_local[u], h->sched_anchor[u], h->sched_mom[u], ln.stream,
-                   Mode{h->ef_sched, h->sched_ctas, h->sched_ctas > 0 ? h->sched_ctas : h->peer_ctas,
-                        h->sched_ctas > 0 ? h->sched_smem_kb : 0});
+  Mode mode{h->ef_sched, h->sched_ctas, h->sched_ctas > 0 ? h->sched_ctas : h->peer_ctas,
+            h->sched_ctas > 0 ? h->sched_smem_kb : 0};
+  if (h->sched_part > 0 && u >= h->sched_full_units) {
+    // partition mode: persistent TMA pipelines with full rings on sched_part CTAs
+    mode.cap = 0;
+    mode.peer_ctas = h->sched_part;
+    mode.smem_kb = 0;
+    mode.part = h->sched_part;
+  }
+  return sync_unit(h, ln, u, h->sched_local[u], h->sched_anchor[u], h->sched_mom[u], ln.stream, mode);
 }
 
 edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* const* anchors,
@@ -906,6 +925,33 @@ edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream) {
     CUDA_TRY(h, cudaStreamWaitEvent(cs, ln.tail, 0));
   }
   h->sched_active = false;
+  return EDIT_OK;
+}
+
+edit_status_t edit_sched_set_partition(edit_sync_t h, int32_t sms, int32_t full_units) {
+  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
+  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  if (h->sched_active) return fail(EDIT_ERR_INVALID_ARG, "a scheduled round is active");
+  if (sms < 0 || sms > h->num_sms || full_units < 0)
+    return fail(EDIT_ERR_INVALID_ARG, "sms must be in [0, #SMs], full_units >= 0");
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  int prio_lo = 0, prio_hi = 0;
+  CUDA_TRY(h, cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  // partition mode: the lanes' persistent CTAs should take each SM a forward CTA releases,
+  // so the lanes run at the highest priority; otherwise back to the priority of init
+  const int prio = sms > 0 ? prio_hi : h->lane_prio;
+  for (Lane& ln : h->lanes) {
+    int cur = 0;
+    CUDA_TRY(h, cudaStreamGetPriority(ln.stream, &cur));
+    if (cur == prio) continue;
+    // a lane's stream orders its buffers and communicators: drain it, then replace it
+    CUDA_TRY(h, cudaStreamSynchronize(ln.stream));
+    CUDA_TRY(h, cudaStreamDestroy(ln.stream));
+    ln.stream = nullptr;
+    CUDA_TRY(h, cudaStreamCreateWithPriority(&ln.stream, cudaStreamNonBlocking, prio));
+  }
+  h->sched_part = sms;
+  h->sched_full_units = full_units;
   return EDIT_OK;
 }
 

@@ -140,6 +140,12 @@ int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anc
 // AG + update: Dbar pulled from each slice's owner, then the K4 math on the whole shard.
 int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl, int max_ctas,
                      bool ef, int smem_kb, cudaStream_t st);
+// Partition mode of the prefetch scheduler (peer_kernels.cu): K1 (no S, no copy) and the
+// N == 1 K4 as persistent TMA pipelines on <= max_ctas CTAs, each with the full ~200 KB
+// ring (one CTA per SM, no GEMM CTA beside it).
+int launch_pg_norm_tma(int dtype, const void* local, const float* anchor, int64_t n, LayerScratch* scr,
+                       double* cta_parts, int max_ctas, cudaStream_t st);
+int launch_update_tma(int dtype, const UpdateArgs& a, int max_ctas, cudaStream_t st);
 inline int64_t rs_partial_slots(int64_t, int) { return kMaxPeerCtas; }
 // Warm-up gradient all-reduce (mean) over the sync row, peer path (peer_kernels.cu).
 int launch_warm_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, void* Dmine, cudaStream_t st);

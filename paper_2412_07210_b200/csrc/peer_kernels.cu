@@ -286,6 +286,177 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
   }
 }
 
+// ------------------------------------------------------------------------------ partition mode
+// The prefetch scheduler's partition mode (a8): while a forward runs on the compute
+// stream, a unit's K1 and (N == 1) K4 run as persistent TMA pipelines on a FEW CTAs, each
+// holding the whole ~200 KB ring -- so no GEMM CTA (213 KB) can share its SM and the forward
+// keeps the other SMs undisturbed.  Per-SM bandwidth comes from the bulk-copy ring depth
+// rather than from thread count.  Same math and reduction structure as kernels.cu's K1/K4
+// (fixed tile -> CTA map for a given grid, fp32 per-thread sums, fp64 CTA tree, partials
+// added in CTA order by the last CTA): deterministic for a given grid.
+
+// K1 (Alg. 2 l.442-443): partial ||anchor - local||^2 of the shard -> scr->send1.
+template <typename T>
+__global__ void __launch_bounds__(kPeerThreads) pg_norm_tma_kernel(const T* __restrict__ local,
+                                                                   const float* __restrict__ anchor, int64_t n,
+                                                                   LayerScratch* __restrict__ scr,
+                                                                   double* __restrict__ cta_parts, int K, int V) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ RingBars bars;
+  const int lbytes = (int)sizeof(T);
+  const int64_t n8 = n >> 3;
+  const int64_t ntiles = (n8 + V - 1) / V;
+  const int stage_bytes = V * 8 * (4 + lbytes);  // [anchor V*8 f32][local V*8 T]
+  ring_init(&bars, K);
+  float acc = 0.f;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      int it = 0;
+      for (int64_t q = blockIdx.x; q < ntiles; q += gridDim.x, ++it) {
+        const int s = it % K, use = it / K;
+        if (use > 0) mbar_wait(&bars.empty[s], (use - 1) & 1);
+        const int64_t v0 = q * V;
+        const int nv = (int)min((int64_t)V, n8 - v0);
+        char* st = smem + (size_t)s * stage_bytes;
+        mbar_arrive_expect_tx(&bars.full[s], (uint32_t)(nv * 8 * (4 + lbytes)));
+        tma_load_1d(st, anchor + 8 * v0, nv * 32, &bars.full[s]);
+        tma_load_1d(st + V * 32, local + 8 * v0, (uint32_t)(nv * 8 * lbytes), &bars.full[s]);
+      }
+    }
+  } else {  // consumers
+    const int t = threadIdx.x - 32;
+    int it = 0;
+    for (int64_t q = blockIdx.x; q < ntiles; q += gridDim.x, ++it) {
+      const int s = it % K, use = it / K;
+      mbar_wait(&bars.full[s], use & 1);
+      const int nv = (int)min((int64_t)V, n8 - q * V);
+      const char* st = smem + (size_t)s * stage_bytes;
+      for (int v = t; v < nv; v += 32 * kConsumerWarps) {
+        float a[8], l[8];
+        load8(reinterpret_cast<const float*>(st) + 8 * v, a);
+        load8(reinterpret_cast<const T*>(st + V * 32) + 8 * v, l);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float d = a[k] - l[k];
+          acc = fmaf(d, d, acc);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.empty[s]);
+    }
+  }
+  double accd = (double)acc;
+  if (blockIdx.x == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + (n & 7)) {  // ragged tail
+    const int64_t k = 8 * n8 + (threadIdx.x - 32);
+    const float d = anchor[k] - load1(local + k);
+    accd += (double)(d * d);
+  }
+  accd = block_sum_n<kPeerThreads>(accd);
+  finish_partials_n<kPeerThreads>(accd, cta_parts, &scr->counter1, &scr->send1);
+}
+
+// K4 at N == 1 (Eq. 4-5, Alg. 2 l.449, l.454-455): Dbar = Delta = anchor - local, beta from
+// the module norm; m = mu m + beta Dbar; a = a - nu (beta Dbar + mu m); local = rne(a).
+// Tiles are walked from the unit's end (K1 streamed it forward: its tail is still in L2).
+template <typename T>
+__global__ void __launch_bounds__(kPeerThreads) update_tma_kernel(UpdateArgs p, int K, int V) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ RingBars bars;
+  __shared__ float s_beta;
+  __shared__ int s_rollback;
+  T* __restrict__ local = static_cast<T*>(p.local);
+  float* __restrict__ anchor = p.anchor;
+  float* __restrict__ mom = p.momentum;
+  if (threadIdx.x == 0) {  // Eq. 4 once per CTA (fp64)
+    double gsq = 0.0;
+    for (int i = 0; i < p.n_gparts; ++i) gsq += p.gparts[i];
+    const double gbar = sqrt(gsq);
+    double beta_d = p.phi / (gbar + p.eps);
+    beta_d = beta_d < 1.0 ? beta_d : 1.0;
+    if (p.flags & EDIT_NO_GC) beta_d = 1.0;
+    const int rb = *p.rollback;
+    if (blockIdx.x == 0) {
+      p.rec->G_bar = rb ? 0.0 : gbar;
+      p.rec->beta = rb ? 1.0 : beta_d;
+      p.rec->rollback = rb;
+      p.rec->round += 1;
+    }
+    s_beta = (float)beta_d;
+    s_rollback = rb;
+  }
+  ring_init(&bars, K);  // (contains __syncthreads)
+  const float beta = s_beta, mu = p.mu, nu = p.nu;
+  const int lbytes = (int)sizeof(T);
+  const int64_t n8 = p.n >> 3;
+  const int64_t ntiles = (n8 + V - 1) / V;
+  const int stage_bytes = V * 8 * (8 + lbytes);  // [anchor V*8 f32][mom V*8 f32][local V*8 T]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (s_rollback) {  // Alg. 2 l.449: local = rne(anchor) (R14)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += stride) {
+      float a[8];
+      load8(anchor + 8 * i, a);
+      store8(local + 8 * i, a);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (p.n & 7)) store1(local + 8 * n8 + threadIdx.x, anchor[8 * n8 + threadIdx.x]);
+    return;
+  }
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      int it = 0;
+      for (int64_t q = blockIdx.x; q < ntiles; q += gridDim.x, ++it) {
+        const int s = it % K, use = it / K;
+        if (use > 0) mbar_wait(&bars.empty[s], (use - 1) & 1);
+        const int64_t v0 = (ntiles - 1 - q) * V;
+        const int nv = (int)min((int64_t)V, n8 - v0);
+        char* st = smem + (size_t)s * stage_bytes;
+        mbar_arrive_expect_tx(&bars.full[s], (uint32_t)(nv * 8 * (8 + lbytes)));
+        tma_load_1d(st, anchor + 8 * v0, nv * 32, &bars.full[s]);
+        tma_load_1d(st + V * 32, mom + 8 * v0, nv * 32, &bars.full[s]);
+        tma_load_1d(st + V * 64, local + 8 * v0, (uint32_t)(nv * 8 * lbytes), &bars.full[s]);
+      }
+    }
+  } else {  // consumers
+    const int t = threadIdx.x - 32;
+    int it = 0;
+    for (int64_t q = blockIdx.x; q < ntiles; q += gridDim.x, ++it) {
+      const int s = it % K, use = it / K;
+      mbar_wait(&bars.full[s], use & 1);
+      const int64_t v0 = (ntiles - 1 - q) * V;
+      const int nv = (int)min((int64_t)V, n8 - v0);
+      const char* st = smem + (size_t)s * stage_bytes;
+      for (int v = t; v < nv; v += 32 * kConsumerWarps) {
+        float a[8], m[8], l[8];
+        load8(reinterpret_cast<const float*>(st) + 8 * v, a);
+        load8(reinterpret_cast<const float*>(st + V * 32) + 8 * v, m);
+        load8(reinterpret_cast<const T*>(st + V * 64) + 8 * v, l);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float g = beta * (a[k] - l[k]);     // Eq. 5, Dbar = Delta at N == 1
+          m[k] = fmaf(mu, m[k], g);                 // m' = mu m + g
+          a[k] = a[k] - nu * fmaf(mu, m[k], g);     // a' = a - nu (g + mu m')
+        }
+        const int64_t i = v0 + v;
+        store8(mom + 8 * i, m);
+        store8(anchor + 8 * i, a);
+        store8(local + 8 * i, a);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.empty[s]);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + (p.n & 7)) {  // ragged tail
+    const int64_t k = 8 * n8 + (threadIdx.x - 32);
+    const float g = beta * (anchor[k] - load1(local + k));
+    const float m1 = fmaf(mu, mom[k], g);
+    const float a1 = anchor[k] - nu * fmaf(mu, m1, g);
+    mom[k] = m1;
+    anchor[k] = a1;
+    store1(local + k, a1);
+  }
+}
+
 // ------------------------------------------------------------------------------ warm-up
 // Alg. 1 l.422-424: during the warm-up the sync group all-reduces the gradients
 // (mean, R-warm).  Same two-kernel shape as the sync's exchange, with uniform weights and no
@@ -467,6 +638,42 @@ int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const S
   } else {
     if (ef) ag_go<float, true>(grid, r, st, a, pp, sl);
     else ag_go<float, false>(grid, r, st, a, pp, sl);
+  }
+  return 1;
+}
+
+template <typename T>
+void pg_norm_tma_go(unsigned grid, const Ring& r, cudaStream_t st, const void* local, const float* anchor, int64_t n,
+                    LayerScratch* scr, double* cta_parts) {
+  set_smem(pg_norm_tma_kernel<T>, r.K * r.stage_bytes);
+  pg_norm_tma_kernel<T><<<grid, kPeerThreads, r.K * r.stage_bytes, st>>>(static_cast<const T*>(local), anchor, n,
+                                                                         scr, cta_parts, r.K, r.V);
+}
+
+int launch_pg_norm_tma(int dtype, const void* local, const float* anchor, int64_t n, LayerScratch* scr,
+                       double* cta_parts, int max_ctas, cudaStream_t st) {
+  const int esz = dtype == EDIT_BF16 ? 2 : 4;
+  const Ring r = ring_for(kPeerTileVec, 8 * (4 + esz), 0);
+  const int64_t ntiles = ((n >> 3) + r.V - 1) / r.V;
+  // never more CTAs than the unit's partial slots (grid_of(n, kVecReduce), the full-grid K1's)
+  const int64_t g = std::min<int64_t>({ntiles, (int64_t)max_ctas, grid_of(n, kVecReduce)});
+  const unsigned grid = (unsigned)std::max<int64_t>(1, g);
+  if (dtype == EDIT_BF16) pg_norm_tma_go<__nv_bfloat16>(grid, r, st, local, anchor, n, scr, cta_parts);
+  else pg_norm_tma_go<float>(grid, r, st, local, anchor, n, scr, cta_parts);
+  return 1;
+}
+
+int launch_update_tma(int dtype, const UpdateArgs& a, int max_ctas, cudaStream_t st) {
+  const int esz = dtype == EDIT_BF16 ? 2 : 4;
+  const Ring r = ring_for(kPeerTileVec, 8 * (8 + esz), 0);
+  const int64_t ntiles = ((a.n >> 3) + r.V - 1) / r.V;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, max_ctas));
+  if (dtype == EDIT_BF16) {
+    set_smem(update_tma_kernel<__nv_bfloat16>, r.K * r.stage_bytes);
+    update_tma_kernel<__nv_bfloat16><<<grid, kPeerThreads, r.K * r.stage_bytes, st>>>(a, r.K, r.V);
+  } else {
+    set_smem(update_tma_kernel<float>, r.K * r.stage_bytes);
+    update_tma_kernel<float><<<grid, kPeerThreads, r.K * r.stage_bytes, st>>>(a, r.K, r.V);
   }
   return 1;
 }

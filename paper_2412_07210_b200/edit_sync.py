@@ -25,7 +25,7 @@ NO_AE, NO_WA, NO_GC = 1, 2, 4
 EXPORTED = ("edit_sync_get_unique_id", "edit_sync_workspace_bytes", "edit_sync_init", "edit_layer_sync",
             "edit_layer_sync_host", "edit_sync_host_wait", "edit_sync_round", "edit_sync_register_locals",
             "edit_warmup_allreduce", "edit_sync_register_gather", "edit_sched_begin_round", "edit_sched_acquire",
-            "edit_sched_end_round",
+            "edit_sched_end_round", "edit_sched_set_partition",
             "edit_sync_stats", "edit_sync_get_state", "edit_sync_set_state", "edit_sync_kernel_launches",
             "edit_sync_set_profiling", "edit_sync_profile_collect", "edit_trigger_create", "edit_trigger_sync_now",
             "edit_trigger_in_warmup", "edit_trigger_mark_synced", "edit_trigger_syncs", "edit_trigger_destroy",
@@ -89,6 +89,7 @@ def load_library() -> ctypes.CDLL:
     lib.edit_sched_begin_round.argtypes, lib.edit_sched_begin_round.restype = [P, P, P, P, I32, P], S
     lib.edit_sched_acquire.argtypes, lib.edit_sched_acquire.restype = [P, I32, P], S
     lib.edit_sched_end_round.argtypes, lib.edit_sched_end_round.restype = [P, P], S
+    lib.edit_sched_set_partition.argtypes, lib.edit_sched_set_partition.restype = [P, I32, I32], S
     lib.edit_sync_stats.argtypes = [P, I32, ctypes.POINTER(LayerStatsC)]
     lib.edit_sync_stats.restype = S
     lib.edit_sync_get_state.argtypes = [P, P, ctypes.POINTER(ctypes.c_size_t)]
@@ -246,6 +247,11 @@ class EditSync:
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         _check(self._lib.edit_sched_end_round(self._h, st.cuda_stream))
         self._round_refs = None
+
+    def set_partition(self, sms: int, full_units: int = 2) -> None:
+        """Scheduler partition mode (edit_sched_set_partition): units >= full_units sync on at
+        most `sms` persistent TMA CTAs (one per SM) while the forward keeps the other SMs."""
+        _check(self._lib.edit_sched_set_partition(self._h, int(sms), int(full_units)))
 
     def _check_round(self, locals_, anchors, momenta):
         L = self.num_layers

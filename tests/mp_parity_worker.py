@@ -69,7 +69,8 @@ def warm_check(units, M, N, m_idx, n_idx, rank, world, dtype, dtype_s, dev, s, m
 
 def run_case(mesh, dtype_s, config, algo="peer", api="unit"):
     # api -- unit: edit_layer_sync x L; round: edit_sync_round; reg: registered locals + round;
-    # gather: fused shard all-gather + round
+    # gather: fused shard all-gather + round; sched: prefetch scheduler (depth 1);
+    # schedpart: registered locals + scheduler in partition mode (8 CTAs, unit 0 full grid)
     M, N = (int(x) for x in mesh.split("x"))
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     assert world == M * N
@@ -138,7 +139,16 @@ def run_case(mesh, dtype_s, config, algo="peer", api="unit"):
     if api == "gather":                # NEXT-2: fused write-back -> shard-group all-gather
         full = [torch.zeros(M * n_, dtype=dtype, device=dev) for n_ in numel]
         s.register_gather(full)
-    if api in ("round", "reg", "gather"):
+    if api in ("sched", "schedpart"):  # a8 prefetch scheduler; schedpart: partition mode
+        if api == "schedpart":
+            s.register_locals(loc)
+            s.set_partition(8, 1)
+        stream = torch.cuda.current_stream(dev)
+        s.begin_round(loc, anc, mom, 1, stream)
+        for i in range(len(units)):
+            s.acquire(i, stream)
+        s.end_round(stream)
+    elif api in ("round", "reg", "gather"):
         if api == "reg":
             s.register_locals(loc)     # peer path reads the members' locals directly
         s.sync_round(loc, anc, mom)

@@ -6,6 +6,7 @@ compares every rank's outputs with the fp64 oracle for the whole M x N mesh and 
 cross-rank invariants.  Cases = (dtype, config, exchange algo, API):
   unit   edit_layer_sync per unit           round  edit_sync_round (2 lanes)
   reg    registered locals + round (peer)   gather fused shard all-gather + round (NEXT-2)
+  sched  prefetch scheduler (a8)            schedpart  scheduler in partition mode (8 CTAs)
 configs: ragged units, toy (BASELINE configs[0]: 4 x 64K fp32, replica 1 planted x4),
 toy_clip, rollback (every replica anomalous), nan (one replica with a NaN param),
 llama350m_sample, warm (NEXT-3 warm-up gradient all-reduce)."""
@@ -41,6 +42,7 @@ def _core_cases(mesh):
     M, N = (int(x) for x in mesh.split("x"))
     c = [("bf16", "ragged", "peer", "unit"), ("f32", "toy", "nccl", "unit"), ("bf16", "nan", "peer", "round"),
          ("f32", "toy_clip", "peer", "unit")]
+    c += [("bf16", "ragged", "peer", "schedpart"), ("bf16", "toy", "nccl", "sched")]
     if N > 1:
         c += [("bf16", "ragged", "peer", "reg"), ("bf16", "warm", "peer", "unit"), ("bf16", "rollback", "nccl", "round")]
     if M > 1:
@@ -64,6 +66,8 @@ def _mesh_cases():
             by_mesh[mesh].append((dt, cfg, algo, "gather"))
     for mesh, dt, cfg in REG_CASES:
         by_mesh[mesh].append((dt, cfg, "peer", "reg"))
+        by_mesh[mesh].append((dt, cfg, "peer", "schedpart"))
+        by_mesh[mesh].append((dt, cfg, "nccl", "sched"))
     return dict(sorted(by_mesh.items()))
 
 

@@ -228,6 +228,42 @@ def test_prefetch_scheduler_round_matches_oracle_and_orders_forward(depth):
         parity.assert_local_close(parity.to_oracle_local(c.local[i]), loc[0, 0], "sched local")
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("sms,full_units", [(1, 0), (8, 1), (148, 2)])
+def test_prefetch_scheduler_partition_mode_matches_oracle(dtype, sms, full_units):
+    # edit_sched_set_partition: units >= full_units sync through the persistent TMA K1/K4 on
+    # <= sms CTAs; same results as the oracle (R17), forward ordering kept, rollback exact
+    units = [synth.Unit(f"u{i}", n, ()) for i, n in enumerate([3_000_017, 7, 4096 * 37 + 3, 1_000_000, 65_536])]
+    c = Case(units, DTYPES[dtype], plant={3: 4.0})
+    mu = np.array([synth.ema_seed(u, 0, c.recipe)[0] for u in units])
+    c.seed_ema(mu, 0.1 * mu, c.recipe.ema_warmup_rounds)   # unit 3 planted x4: flagged -> rollback
+    c.sync.set_partition(sms, full_units)
+    stream = torch.cuda.current_stream(DEV)
+    seen = []
+    c.sync.begin_round(c.local, c.anchor, c.mom, 1, stream)
+    for i in range(len(units)):
+        c.sync.acquire(i, stream)
+        seen.append(c.local[i].float().sum())
+        torch.cuda._sleep(100_000)
+    c.sync.end_round(stream)
+    torch.cuda.synchronize()
+    for i in range(len(units)):
+        assert torch.equal(seen[i], c.local[i].float().sum()), f"forward of unit {i} did not see the synced params"
+        loc, anc, mom, ema, out = oracle.sync_unit(c.cfg, c.o_local[i][None, None], c.o_anchor[i][None],
+                                                   c.o_mom[i][None], c.o_ema[i])
+        tag = f"partition sms={sms} unit {i}"
+        parity.assert_outcome(c.sync.stats(i), out, ema, tag)
+        parity.assert_f32_close(c.anchor[i].cpu().numpy(), anc[0], tag + " anchor")
+        parity.assert_f32_close(c.mom[i].cpu().numpy(), mom[0], tag + " momentum")
+        parity.assert_local_close(parity.to_oracle_local(c.local[i]), loc[0, 0], tag + " local")
+        assert torch.equal(c.local[i], c.anchor[i].to(DTYPES[dtype])), tag
+        if i == 3:
+            assert out.rollback and np.array_equal(c.anchor[i].cpu().numpy(), c.o_anchor[i])
+    c.sync.set_partition(0, 2)                               # back to full grids
+    with pytest.raises(Exception):
+        c.sync.set_partition(-1, 0)
+
+
 def test_prefetch_scheduler_argument_errors():
     from paper_2412_07210_b200 import EditSyncError
     units = [synth.Unit("a", 1000, ()), synth.Unit("b", 2000, ())]
