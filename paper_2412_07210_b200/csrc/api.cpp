@@ -157,6 +157,10 @@ struct edit_sync {
   int sched_part = 0;
   int sched_full_units = 2;
   int lane_prio = 0;             // priority the lanes were created with (env default)
+  // gate (EDIT_SCHED_GATE=1): the sync of unit u+depth starts only when the forward of unit
+  // u may start (an event on the compute stream at acquire(u)), not as soon as its lane frees
+  bool sched_gate = false;
+  std::vector<cudaEvent_t> gate_ev;
   bool ready = false;            // init completed (destroy may then barrier with the peers)
   char* ws = nullptr;
   LayerScratch* scratch = nullptr;
@@ -329,6 +333,9 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
 
   h->done.assign(cfg->num_layers, nullptr);
   for (auto& e : h->done) INIT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  h->gate_ev.assign(cfg->num_layers, nullptr);
+  for (auto& e : h->gate_ev) INIT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (const char* e = getenv("EDIT_SCHED_GATE")) h->sched_gate = atoi(e) != 0;
   INIT_CUDA(cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming));
 
   int nlanes = 2;  // EDIT_LANES (1..4) -- must be equal on every rank
@@ -843,9 +850,13 @@ edit_status_t edit_sync_host_wait(edit_sync_t h, void* stream) {
   return EDIT_OK;
 }
 
-static edit_status_t sched_enqueue_next(edit_sync_t h) {
+static edit_status_t sched_enqueue_next(edit_sync_t h, cudaStream_t gate = nullptr) {
   const int u = h->sched_next_sync++;
   Lane& ln = h->lanes[u % h->lanes.size()];
+  if (gate && h->sched_gate) {
+    CUDA_TRY(h, cudaEventRecord(h->gate_ev[u], gate));
+    CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->gate_ev[u], 0));
+  }
   Mode mode{h->ef_sched, h->sched_ctas, h->sched_ctas > 0 ? h->sched_ctas : h->peer_ctas,
             h->sched_ctas > 0 ? h->sched_smem_kb : 0};
   if (h->sched_part > 0 && u >= h->sched_full_units) {
@@ -903,7 +914,7 @@ edit_status_t edit_sched_acquire(edit_sync_t h, int32_t layer, void* compute_str
   CUDA_TRY(h, cudaStreamWaitEvent(static_cast<cudaStream_t>(compute_stream), h->done[layer], 0));
   h->sched_next_acquire = layer + 1;
   if (h->sched_next_sync < L && h->sched_next_sync <= layer + h->sched_depth) {
-    edit_status_t rc = sched_enqueue_next(h);
+    edit_status_t rc = sched_enqueue_next(h, static_cast<cudaStream_t>(compute_stream));
     if (rc != EDIT_OK) return rc;
   }
   return EDIT_OK;
@@ -1087,6 +1098,8 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
   if (h->fork) cudaEventDestroy(h->fork);
   if (h->warm_dev) cudaFree(h->warm_dev);
   for (auto e : h->done)
+    if (e) cudaEventDestroy(e);
+  for (auto e : h->gate_ev)
     if (e) cudaEventDestroy(e);
   for (auto e : h->prof)
     if (e) cudaEventDestroy(e);

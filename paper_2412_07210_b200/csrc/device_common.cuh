@@ -72,6 +72,32 @@ __device__ __forceinline__ void store8(__nv_bfloat16* __restrict__ p, const floa
   }
   stg16<kEF>(p, make_uint4(w[0], w[1], w[2], w[3]), pol);
 }
+// 4 elements: 16 B (fp32) / 8 B (bf16) per thread, consecutive threads at consecutive
+// addresses -- conflict-free shared-memory reads and fully coalesced global stores (the
+// partition-mode kernels, where per-SM datapath bandwidth is the limit: tools/sm_stream_bench.cu)
+__device__ __forceinline__ void load4(const float* __restrict__ p, float (&v)[4]) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+}
+__device__ __forceinline__ void load4(const __nv_bfloat16* __restrict__ p, float (&v)[4]) {
+  const uint2 r = *reinterpret_cast<const uint2*>(p);
+  v[0] = __uint_as_float(r.x << 16); v[1] = __uint_as_float(r.x & 0xffff0000u);
+  v[2] = __uint_as_float(r.y << 16); v[3] = __uint_as_float(r.y & 0xffff0000u);
+}
+template <bool kEF = false>
+__device__ __forceinline__ void store4(float* __restrict__ p, const float (&v)[4], uint64_t pol = 0) {
+  stg16<kEF>(p, make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3])),
+             pol);
+}
+template <bool kEF = false>
+__device__ __forceinline__ void store4(__nv_bfloat16* __restrict__ p, const float (&v)[4], uint64_t pol = 0) {
+  __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]), h1 = __floats2bfloat162_rn(v[2], v[3]);  // RNE (R16)
+  const uint32_t x = *reinterpret_cast<uint32_t*>(&h0), y = *reinterpret_cast<uint32_t*>(&h1);
+  if (kEF)
+    asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1,%2}, %3;" ::"l"(p), "r"(x), "r"(y), "l"(pol) : "memory");
+  else
+    *reinterpret_cast<uint2*>(p) = make_uint2(x, y);
+}
 __device__ __forceinline__ float load1(const float* p) { return *p; }
 __device__ __forceinline__ float load1(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 __device__ __forceinline__ void store1(float* p, float v) { *p = v; }
@@ -91,6 +117,19 @@ __device__ __forceinline__ void gather_store8_t(const UpdateArgs& p, int64_t k, 
     for (int q = 0; q < p.gather_M; ++q)
 #pragma unroll
       for (int j = 0; j < 8; ++j) store1(static_cast<T*>(p.gather[q]) + p.gather_off + k + j, v[j]);
+  }
+}
+// 4-element variant (slot aligned for a 4-element store iff gather_off % 4 == 0)
+template <bool kEF, typename T>
+__device__ __forceinline__ void gather_store4_t(const UpdateArgs& p, int64_t k, const float (&v)[4], uint64_t pol) {
+  if ((p.gather_off & 3) == 0) {
+#pragma unroll
+    for (int q = 0; q < EDIT_MAX_SHARD; ++q)
+      if (q < p.gather_M) store4<kEF>(static_cast<T*>(p.gather[q]) + p.gather_off + k, v, pol);
+  } else {
+    for (int q = 0; q < p.gather_M; ++q)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) store1(static_cast<T*>(p.gather[q]) + p.gather_off + k + j, v[j]);
   }
 }
 template <typename T>

@@ -13,8 +13,8 @@
 //
 // Both are persistent, warp-specialised TMA pipelines: one producer thread streams tiles
 // (local HBM and peers alike) with 1-D bulk copies (cp.async.bulk ... complete_tx) into a
-// ring of shared-memory stages; 8 consumer warps compute from shared memory and store with
-// 16-byte STG.  Measured on B200 (profiles/r1_peer_bench_2gpu.txt): 16-32 CTAs of bulk
+// ring of shared-memory stages; 8 consumer warps compute from shared memory (4-element units:
+// conflict-free LDS) and store with coalesced STG.  Measured on B200 (profiles/r1_peer_bench_2gpu.txt): 16-32 CTAs of bulk
 // copies already pull ~780 GB/s from a peer, where plain LDG needs the whole GPU.
 #include <cuda_bf16.h>
 #include <math.h>
@@ -34,9 +34,6 @@ using namespace dev;
 #define EDIT_CONSUMER_WARPS 8
 #endif
 constexpr int kConsumerWarps = EDIT_CONSUMER_WARPS;
-#ifndef EDIT_CONSUMER_UNROLL
-#define EDIT_CONSUMER_UNROLL 1  // measured neutral (tools/peer_kbench.cu, 8/16 warps x 1/2)
-#endif
 constexpr int kPeerThreads = 32 * (1 + kConsumerWarps);  // warp 0 = producer
 constexpr int kSmemBudget = 200 * 1024;
 
@@ -113,22 +110,22 @@ __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_const
         const int64_t v0 = s0 + q * V;
         const int nv = (int)min((int64_t)V, s1 - v0);
         const char* st = smem + (size_t)s * stage_bytes;
-        for (int v = t; v < nv; v += 32 * kConsumerWarps) {
-          float a[8], d[8];
-          load8(reinterpret_cast<const float*>(st) + 8 * v, a);
+        for (int v = t; v < 2 * nv; v += 32 * kConsumerWarps) {  // 4-element units
+          float a[4], d[4];
+          load4(reinterpret_cast<const float*>(st) + 4 * v, a);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) d[k] = 0.f;
+          for (int k = 0; k < 4; ++k) d[k] = 0.f;
 #pragma unroll
           for (int j = 0; j < EDIT_MAX_SYNC; ++j) {
             if (j >= N || w[j] == 0.f) continue;
-            float l[8];
-            load8(reinterpret_cast<const T*>(st + V * 32 + j * V * 8 * lbytes) + 8 * v, l);
+            float l[4];
+            load4(reinterpret_cast<const T*>(st + V * 32 + j * V * 8 * lbytes) + 4 * v, l);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) d[k] = fmaf(w[j], a[k] - l[k], d[k]);
+            for (int k = 0; k < 4; ++k) d[k] = fmaf(w[j], a[k] - l[k], d[k]);
           }
 #pragma unroll
-          for (int k = 0; k < 8; ++k) acc = fmaf(d[k], d[k], acc);
-          store8<kEF>(Dmine + 8 * (v0 - s0 + v), d, pol);
+          for (int k = 0; k < 4; ++k) acc = fmaf(d[k], d[k], acc);
+          store4<kEF>(Dmine + 8 * (v0 - s0) + 4 * v, d, pol);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.empty[s]);
@@ -241,31 +238,25 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
       const int s = it % K, use = it / K;
       mbar_wait(&bars.full[s], use & 1);
       const float* st = reinterpret_cast<const float*>(smem + (size_t)s * stage_bytes);
-      constexpr int NT = 32 * kConsumerWarps, CU = EDIT_CONSUMER_UNROLL;
-      for (int v = t; v < nv; v += CU * NT) {
-        float d[CU][8], a[CU][8], m[CU][8];
+      // 4-element units, consecutive threads on consecutive 16 B: conflict-free shared-memory
+      // reads, fully coalesced stores (tools/sm_stream_bench.cu)
+      const int n4 = 2 * nv;
+      for (int v = t; v < n4; v += 32 * kConsumerWarps) {
+        float d[4], a[4], m[4];
+        load4(st + 4 * v, d);
+        load4(st + V * 8 + 4 * v, a);
+        load4(st + V * 16 + 4 * v, m);
 #pragma unroll
-        for (int c = 0; c < CU; ++c)  // all shared-memory loads of the CU vectors first
-          if (v + c * NT < nv) {
-            load8(st + 8 * (v + c * NT), d[c]);
-            load8(st + V * 8 + 8 * (v + c * NT), a[c]);
-            load8(st + V * 16 + 8 * (v + c * NT), m[c]);
-          }
-#pragma unroll
-        for (int c = 0; c < CU; ++c)
-          if (v + c * NT < nv) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const float g = beta * d[c][k];                // Eq. 5
-              m[c][k] = fmaf(mu, m[c][k], g);                // m' = mu m + g
-              a[c][k] = a[c][k] - nu * fmaf(mu, m[c][k], g);  // a' = a - nu (g + mu m')
-            }
-            const int64_t i = v0 + v + c * NT;
-            store8<kEF>(mom + 8 * i, m[c], pol);
-            store8<kEF>(anchor + 8 * i, a[c], pol);
-            store8<kEF>(local + 8 * i, a[c], pol);
-            if (kG) gather_store8_t<kEF, T>(p, 8 * i, a[c], pol);
-          }
+        for (int k = 0; k < 4; ++k) {
+          const float g = beta * d[k];                // Eq. 5
+          m[k] = fmaf(mu, m[k], g);                   // m' = mu m + g
+          a[k] = a[k] - nu * fmaf(mu, m[k], g);       // a' = a - nu (g + mu m')
+        }
+        const int64_t i = 8 * v0 + 4 * v;             // first element of the unit
+        store4<kEF>(mom + i, m, pol);
+        store4<kEF>(anchor + i, a, pol);
+        store4<kEF>(local + i, a, pol);
+        if (kG) gather_store4_t<kEF, T>(p, i, a, pol);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.empty[s]);
@@ -330,14 +321,14 @@ __global__ void __launch_bounds__(kPeerThreads) pg_norm_tma_kernel(const T* __re
     for (int64_t q = blockIdx.x; q < ntiles; q += gridDim.x, ++it) {
       const int s = it % K, use = it / K;
       mbar_wait(&bars.full[s], use & 1);
-      const int nv = (int)min((int64_t)V, n8 - q * V);
+      const int n4 = 2 * (int)min((int64_t)V, n8 - q * V);  // 4-element units of the tile
       const char* st = smem + (size_t)s * stage_bytes;
-      for (int v = t; v < nv; v += 32 * kConsumerWarps) {
-        float a[8], l[8];
-        load8(reinterpret_cast<const float*>(st) + 8 * v, a);
-        load8(reinterpret_cast<const T*>(st + V * 32) + 8 * v, l);
+      for (int v = t; v < n4; v += 32 * kConsumerWarps) {
+        float a[4], l[4];
+        load4(reinterpret_cast<const float*>(st) + 4 * v, a);
+        load4(reinterpret_cast<const T*>(st + V * 32) + 4 * v, l);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < 4; ++k) {
           const float d = a[k] - l[k];
           acc = fmaf(d, d, acc);
         }
@@ -424,23 +415,23 @@ __global__ void __launch_bounds__(kPeerThreads) update_tma_kernel(UpdateArgs p, 
       const int s = it % K, use = it / K;
       mbar_wait(&bars.full[s], use & 1);
       const int64_t v0 = (ntiles - 1 - q) * V;
-      const int nv = (int)min((int64_t)V, n8 - v0);
+      const int n4 = 2 * (int)min((int64_t)V, n8 - v0);  // 4-element units of the tile
       const char* st = smem + (size_t)s * stage_bytes;
-      for (int v = t; v < nv; v += 32 * kConsumerWarps) {
-        float a[8], m[8], l[8];
-        load8(reinterpret_cast<const float*>(st) + 8 * v, a);
-        load8(reinterpret_cast<const float*>(st + V * 32) + 8 * v, m);
-        load8(reinterpret_cast<const T*>(st + V * 64) + 8 * v, l);
+      for (int v = t; v < n4; v += 32 * kConsumerWarps) {
+        float a[4], m[4], l[4];
+        load4(reinterpret_cast<const float*>(st) + 4 * v, a);
+        load4(reinterpret_cast<const float*>(st + V * 32) + 4 * v, m);
+        load4(reinterpret_cast<const T*>(st + V * 64) + 4 * v, l);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < 4; ++k) {
           const float g = beta * (a[k] - l[k]);     // Eq. 5, Dbar = Delta at N == 1
           m[k] = fmaf(mu, m[k], g);                 // m' = mu m + g
           a[k] = a[k] - nu * fmaf(mu, m[k], g);     // a' = a - nu (g + mu m')
         }
-        const int64_t i = v0 + v;
-        store8(mom + 8 * i, m);
-        store8(anchor + 8 * i, a);
-        store8(local + 8 * i, a);
+        const int64_t i = 8 * v0 + 4 * v;           // first element of the unit
+        store4(mom + i, m);
+        store4(anchor + i, a);
+        store4(local + i, a);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.empty[s]);
@@ -653,7 +644,7 @@ void pg_norm_tma_go(unsigned grid, const Ring& r, cudaStream_t st, const void* l
 int launch_pg_norm_tma(int dtype, const void* local, const float* anchor, int64_t n, LayerScratch* scr,
                        double* cta_parts, int max_ctas, cudaStream_t st) {
   const int esz = dtype == EDIT_BF16 ? 2 : 4;
-  const Ring r = ring_for(kPeerTileVec, 8 * (4 + esz), 0);
+  const Ring r = ring_for(2 * kPeerTileVec, 8 * (4 + esz), 0);  // bf16: 1024-vector tiles x 4 stages
   const int64_t ntiles = ((n >> 3) + r.V - 1) / r.V;
   // never more CTAs than the unit's partial slots (grid_of(n, kVecReduce), the full-grid K1's)
   const int64_t g = std::min<int64_t>({ntiles, (int64_t)max_ctas, grid_of(n, kVecReduce)});
