@@ -223,6 +223,10 @@ def main() -> None:
     ap.add_argument("--gather", action="store_true", help="NEXT-2 fused shard all-gather measurement (M > 1)")
     ap.add_argument("--no-register", action="store_true",
                     help="peer path: do not register the locals for direct IPC reads (stage a copy)")
+    ap.add_argument("--anomaly-rate", type=float, default=0.0,
+                    help="probability that a (unit, replica) is planted anomalous in a round (SURVEY 8d: 3B config)")
+    ap.add_argument("--anomaly-sweep", default=None,
+                    help="comma list of anomaly rates timed after the main loop (e.g. 0,0.125,0.25,0.5,1)")
     ap.add_argument("--sequential", action="store_true",
                     help="time per-unit edit_layer_sync calls on one stream instead of edit_sync_round")
     args = ap.parse_args()
@@ -269,10 +273,17 @@ def main() -> None:
     if registered:
         sync.register_locals(locs)   # members read each other's locals directly (no staging copy)
 
+    planted = {"replicas": 0, "rounds": 0}
+
     def redraw(step: int) -> None:
-        # "tau inner steps" of every worker, outside the timed region
+        # "tau inner steps" of every worker, outside the timed region; --anomaly-rate r plants
+        # anomalous replicas (x4 displacement) per (unit, replica, round) with probability r
+        plants = synth.anomaly_plants(len(units), N, args.anomaly_rate, step)
+        planted["replicas"] += len(plants)
+        planted["rounds"] += 1
         for i, u in enumerate(units):
-            locs[i].copy_(synth.shard_local(u, i, M, m_idx, n_idx, anchors[i], dtype, dev, round_salt=step))
+            locs[i].copy_(synth.shard_local(u, i, M, m_idx, n_idx, anchors[i], dtype, dev,
+                                            plant=plants.get((i, n_idx), 1.0), round_salt=step))
 
     stream = torch.cuda.current_stream(dev)
 
@@ -317,6 +328,35 @@ def main() -> None:
             step_ms.append(max_over_ranks(t, world, dev))
     launches = sync.kernel_launches - launches0
     clk = clocks.summary()
+    # SURVEY 8d (3B config): the same timed round at several anomaly rates; throughput should
+    # not depend on the rate except through the cheaper rollback write (every replica flagged)
+    anomaly_sweep = None
+    if args.anomaly_sweep:
+        anomaly_sweep = []
+        rate0 = args.anomaly_rate
+        for ri, rate in enumerate(float(x) for x in args.anomaly_sweep.split(",")):
+            args.anomaly_rate = rate
+            ts, fl, rb = [], 0, 0
+            for s in range(args.steps + 1):      # first round untimed
+                redraw(20000 + 100 * ri + s)
+                barrier()
+                torch.cuda.synchronize()
+                ev0.record(stream)
+                run_round()
+                ev1.record(stream)
+                torch.cuda.synchronize()
+                if s > 0:
+                    ts.append(max_over_ranks(ev0.elapsed_time(ev1), world, dev))
+                    for i in range(len(units)):
+                        st_i = sync.stats(i)
+                        fl += int(sum(st_i.anomalous[:N]))
+                        rb += int(st_i.rollback)
+            ms = sum(ts) / len(ts)
+            anomaly_sweep.append({"rate": rate, "ms_per_round": ms,
+                                  "value_GBps": world * 4.0 * P_r / (ms * 1e-3) / 1e9,
+                                  "flagged_per_round": fl / len(ts), "rollbacks_per_round": rb / len(ts),
+                                  "units_x_replicas": len(units) * N})
+        args.anomaly_rate = rate0
     # the same kernels once more, isolated: per-unit calls on one stream (no lane overlap),
     # outside the timed region -- each kernel's own duration for the isolated roofline
     iso_ms = {k: 0.0 for k in sync.PHASES}
@@ -336,6 +376,10 @@ def main() -> None:
     # every unit's outcome of the last round (checks nothing rolled back unexpectedly)
     rollbacks = sum(int(sync.stats(i).rollback) for i in range(len(units)))
     betas = [sync.stats(i).beta for i in (0, 1, len(units) - 1)]
+    flagged = sum(int(sum(sync.stats(i).anomalous[:N])) for i in range(len(units)))
+    anomaly = {"rate": args.anomaly_rate, "planted_replicas_per_round": planted["replicas"] / max(1, planted["rounds"]),
+               "flagged_last_round": flagged, "rollbacks_last_round": rollbacks,
+               "units_x_replicas": len(units) * N}
 
     total_ms = sum(step_ms)
     ms_per_step = total_ms / len(step_ms)
@@ -612,7 +656,8 @@ def main() -> None:
                        "api": "edit_layer_sync x L (sequential)" if args.sequential else
                        f"edit_sync_round ({os.environ.get('EDIT_LANES', '2')} lanes)",
                        "l2": "inputs (%.1f GB/rank) larger than L2" % (P_r * (b_l + 8) / 1e9),
-                       "inner_steps": "locals redrawn as cast(anchor - D) between steps, outside the timed region"},
+                       "inner_steps": "locals redrawn as cast(anchor - D) between steps, outside the timed region",
+                       "anomaly_rate": args.anomaly_rate},
             "roofline": {"bound": k4_bound, "kernel": k4_name, "achieved": k4_achieved, "peak": k4_peak,
                          "unit": "GB/s", "frac": (k4_achieved / k4_peak) if k4_achieved else None,
                          "traffic": traffic if k4_bound == "hbm" else None,
@@ -639,7 +684,8 @@ def main() -> None:
                                       "the peer path moves (b_l+4)(N-1)/N B/param, below the fp32 bus convention"},
             "phases_ms_per_step": {k: v / args.steps for k, v in phase_ms.items()},
             "per_gpu_GBps": bytes_per_rank_round / (ms_per_step * 1e-3) / 1e9,
-            "rollbacks_last_round": rollbacks, "beta_sample": betas,
+            "rollbacks_last_round": rollbacks, "beta_sample": betas, "anomaly": anomaly,
+            "anomaly_sweep": anomaly_sweep,
             "gpu_launches": launches, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "overlap": overlap,
             "warmup_allreduce": warm, "fused_gather": gather,
         }

@@ -37,7 +37,7 @@ LLAMA = {
 N_LAYERS = 32
 VOCAB = 79800
 
-KIND_ANCHOR, KIND_MOMENTUM, KIND_COMMON, KIND_REPLICA = 0, 1, 2, 3
+KIND_ANCHOR, KIND_MOMENTUM, KIND_COMMON, KIND_REPLICA, KIND_ANOMALY = 0, 1, 2, 3, 4
 
 
 def seed_of(kind: int, u: int, m: int, n: int) -> int:
@@ -129,6 +129,23 @@ def shard_local(unit: Unit, u: int, M: int, m: int, n: int, anchor: torch.Tensor
     disp[valid:] = 0.0
     out = anchor.to(torch.float32) - disp
     return out.to(dtype)
+
+
+def anomaly_plants(num_units: int, N: int, rate: float, round_salt: int = 0, factor: float = 4.0) -> dict:
+    """Planted anomalies for an anomaly-rate run: replica n of unit u is
+    planted (its displacement x factor, z ~ 30) with probability `rate`, one Bernoulli draw per
+    (unit, replica, round) from a CPU generator seeded by (KIND_ANOMALY, u, n, round) -- the
+    same decisions on every rank.  Returns {(u, n): factor}."""
+    out = {}
+    if rate <= 0.0:
+        return out
+    for u in range(num_units):
+        for n in range(N):
+            g = torch.Generator()
+            g.manual_seed(seed_of(KIND_ANOMALY, u, 0, n) + 7919 * round_salt)
+            if torch.rand((), generator=g).item() < rate:
+                out[(u, n)] = factor
+    return out
 
 
 def ema_seed(unit: Unit, n: int, recipe: Recipe = Recipe()) -> tuple[float, float, int]:
