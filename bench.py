@@ -654,7 +654,7 @@ def main() -> None:
                        "exchange": (args.algo + (" (registered locals)" if registered else "") if N > 1
                                     else "none (N = 1)"),
                        "api": "edit_layer_sync x L (sequential)" if args.sequential else
-                       f"edit_sync_round ({os.environ.get('EDIT_LANES', '2')} lanes)",
+                       f"edit_sync_round ({os.environ.get('EDIT_LANES', '4')} lanes)",
                        "l2": "inputs (%.1f GB/rank) larger than L2" % (P_r * (b_l + 8) / 1e9),
                        "inner_steps": "locals redrawn as cast(anchor - D) between steps, outside the timed region",
                        "anomaly_rate": args.anomaly_rate},

@@ -168,7 +168,7 @@ edit_status_t edit_sync_register_gather(edit_sync_t h, void* const* full_bufs);
 
 /* One full sync round: every unit 0..L-1 (arrays of L device pointers), equivalent to
  * calling edit_layer_sync for u = 0..L-1 in order but pipelined: units are dealt
- * round-robin over the library's lanes (EDIT_LANES, default 2; each lane = an internal
+ * round-robin over the library's lanes (EDIT_LANES, default 4; each lane = an internal
  * stream + its own NCCL communicators + exchange buffers), so unit u+1's norm pass and
  * scalar gathers overlap unit u's exchange and update.  Starts after the work already on
  * `stream`; `stream` waits for the whole round.  Same results, bit for bit, as the

@@ -338,10 +338,12 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
   if (const char* e = getenv("EDIT_SCHED_GATE")) h->sched_gate = atoi(e) != 0;
   INIT_CUDA(cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming));
 
-  int nlanes = 2;  // EDIT_LANES (1..4) -- must be equal on every rank
+  // EDIT_LANES (1..8) -- must be equal on every rank.  4: measured 350M 1x2 3.27 -> 2.78 ms,
+  // 1B 7.90 -> 7.21 ms, 7B 43.0 -> 42.5 ms vs 2 lanes (profiles/r1_lanes_2gpu.txt)
+  int nlanes = 4;
   if (const char* e = getenv("EDIT_LANES")) {
     const int v = atoi(e);
-    if (v >= 1 && v <= 4) nlanes = v;
+    if (v >= 1 && v <= 8) nlanes = v;
   }
   int prio_lo = 0, prio_hi = 0;
   INIT_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
