@@ -214,7 +214,7 @@ def main() -> None:
     ap.add_argument("--overlap-tokens", default="8192,65536",
                     help="tokens/GPU of the synthetic forward(s) for the prefetch-overlap measurement, comma "
                          "list (0 = skip); 8,192 = SURVEY 8d default, 65,536 = the paper's 1024 seqs x 4096 / 64")
-    ap.add_argument("--partition", default="0,16",
+    ap.add_argument("--partition", default="0,32",
                     help="scheduler partition modes to measure (comma list of SM counts; 0 = full grids)")
     ap.add_argument("--full-units", type=int, default=2,
                     help="partition mode: units before this index keep full grids (embedding + first layer)")
@@ -654,7 +654,7 @@ def main() -> None:
                        "exchange": (args.algo + (" (registered locals)" if registered else "") if N > 1
                                     else "none (N = 1)"),
                        "api": "edit_layer_sync x L (sequential)" if args.sequential else
-                       f"edit_sync_round ({os.environ.get('EDIT_LANES', '4')} lanes)",
+                       f"edit_sync_round ({os.environ.get('EDIT_LANES', '4' if N > 1 else '2')} lanes)",
                        "l2": "inputs (%.1f GB/rank) larger than L2" % (P_r * (b_l + 8) / 1e9),
                        "inner_steps": "locals redrawn as cast(anchor - D) between steps, outside the timed region",
                        "anomaly_rate": args.anomaly_rate},

@@ -168,8 +168,8 @@ edit_status_t edit_sync_register_gather(edit_sync_t h, void* const* full_bufs);
 
 /* One full sync round: every unit 0..L-1 (arrays of L device pointers), equivalent to
  * calling edit_layer_sync for u = 0..L-1 in order but pipelined: units are dealt
- * round-robin over the library's lanes (EDIT_LANES, default 4; each lane = an internal
- * stream + its own NCCL communicators + exchange buffers), so unit u+1's norm pass and
+ * round-robin over the library's lanes (EDIT_LANES; default 4 for N > 1, 2 for N == 1;
+ * each lane = an internal stream + its own NCCL communicators + exchange buffers), so unit u+1's norm pass and
  * scalar gathers overlap unit u's exchange and update.  Starts after the work already on
  * `stream`; `stream` waits for the whole round.  Same results, bit for bit, as the
  * sequential calls (every unit's arithmetic and reduction order is unchanged). */
@@ -208,8 +208,9 @@ edit_status_t edit_sched_acquire(edit_sync_t h, int32_t layer, void* compute_str
 edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream);
 /* Partition mode of the scheduler (how the overlap of P:70 is obtained on one GPU whose
  * forward is tensor-bound on every SM).  sms > 0: the syncs of units u >= full_units run as
- * persistent TMA pipelines on at most `sms` CTAs, each holding a ~200 KB shared-memory ring
- * so that it owns its SM; the concurrent forward keeps the other SMs.  The side streams are
+ * persistent TMA pipelines on about `sms` SMs in total (each lane's kernels get
+ * ceil(sms / lanes) CTAs; the lanes run concurrently), each CTA holding a ~200 KB
+ * shared-memory ring so that it owns its SM; the concurrent forward keeps the other SMs.  The side streams are
  * switched to the highest stream priority (so a freed SM goes to a sync CTA first).  Units
  * u < full_units (the ones a forward reaches before its first GEMM, e.g. the embedding: 2)
  * keep full grids.  sms == 0 restores the default (full grids, init priority).

@@ -338,9 +338,11 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
   if (const char* e = getenv("EDIT_SCHED_GATE")) h->sched_gate = atoi(e) != 0;
   INIT_CUDA(cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming));
 
-  // EDIT_LANES (1..8) -- must be equal on every rank.  4: measured 350M 1x2 3.27 -> 2.78 ms,
-  // 1B 7.90 -> 7.21 ms, 7B 43.0 -> 42.5 ms vs 2 lanes (profiles/r1_lanes_2gpu.txt)
-  int nlanes = 4;
+  // EDIT_LANES (1..8) -- must be equal on every rank.  Lanes hide the latency of the scalar
+  // chain of the exchange: N > 1 -> 4 (measured 350M 1x2 3.27 -> 2.78 ms, 1B 7.90 -> 7.21 ms,
+  // 7B 43.0 -> 42.5 ms vs 2 lanes, profiles/r1_lanes_2gpu.txt); N == 1 -> 2 (no exchange;
+  // 7B 1x1 27.0 ms with 2 or 4 lanes)
+  int nlanes = h->N > 1 ? 4 : 2;
   if (const char* e = getenv("EDIT_LANES")) {
     const int v = atoi(e);
     if (v >= 1 && v <= 8) nlanes = v;
@@ -862,11 +864,14 @@ static edit_status_t sched_enqueue_next(edit_sync_t h, cudaStream_t gate = nullp
   Mode mode{h->ef_sched, h->sched_ctas, h->sched_ctas > 0 ? h->sched_ctas : h->peer_ctas,
             h->sched_ctas > 0 ? h->sched_smem_kb : 0};
   if (h->sched_part > 0 && u >= h->sched_full_units) {
-    // partition mode: persistent TMA pipelines with full rings on sched_part CTAs
+    // partition mode: persistent TMA pipelines with full rings; the lanes run concurrently,
+    // so each lane's kernels get an equal share of the sched_part SMs
+    const int nl = (int)h->lanes.size();
+    const int per = std::max(1, (h->sched_part + nl - 1) / nl);
     mode.cap = 0;
-    mode.peer_ctas = h->sched_part;
+    mode.peer_ctas = per;
     mode.smem_kb = 0;
-    mode.part = h->sched_part;
+    mode.part = per;
   }
   return sync_unit(h, ln, u, h->sched_local[u], h->sched_anchor[u], h->sched_mom[u], ln.stream, mode);
 }
