@@ -123,6 +123,17 @@ class Clocks:
                 "power_cap_frac": capped / len(rows)}
 
 
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def oracle_cpu_baseline(model: str, dtype, target_s: float = 12.0) -> dict:
     """The oracle (as it stands) on this host's cores, on a bounded sample of the workload:
     whole decoder-unit shards of the 1 x 1 mesh (layer 0, 1, ...) until ~target_s of CPU work."""
@@ -147,7 +158,26 @@ def oracle_cpu_baseline(model: str, dtype, target_s: float = 12.0) -> dict:
         done.append(u.name)
         if total_t >= target_s or len(done) >= 8:
             break
-    return {"value": 4.0 * total_n / total_t / 1e9, "unit": "GB/s", "cores": oracle.get_threads(), "kind": "oracle",
+    # the same oracle on ONE thread (threads = 1 and os.cpu_count()), on a 16M-param
+    # prefix of the first sampled unit (timing only; a prefix is a smaller unit of the same kind)
+    cores = oracle.get_threads()
+    u = units[1]
+    sub = min(u.numel, 16_000_000)
+    a = synth.shard_anchor(u, 1, 1, 0, dev)
+    m = synth.shard_momentum(u, 1, 1, 0, dev)
+    l = synth.shard_local(u, 1, 1, 0, 0, a, dtype, dev)
+    L1 = parity.to_oracle_local(l)[None, None, :sub].copy()
+    A1, M1 = a.cpu().numpy()[None, :sub].copy(), m.cpu().numpy()[None, :sub].copy()
+    del a, m, l
+    oracle.set_threads(1)
+    t0 = time.perf_counter()
+    oracle.sync_unit(oracle.Config(), L1, A1, M1, [oracle.Ema()])
+    t1 = time.perf_counter() - t0
+    oracle.set_threads(cores)
+    one = {"value": 4.0 * sub / t1 / 1e9, "unit": "GB/s", "cores": 1,
+           "sample": f"{sub} params (prefix of {u.name}), {t1:.1f} s on 1 thread"}
+    return {"value": 4.0 * total_n / total_t / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "threads_1": one, "host_cpu": _cpu_model(),
             "sample": f"1 sync of the Llama-{model} shards {done[0]}..{done[-1]} ({len(done)} decoder units, "
                       f"{total_n} params, 1x1 mesh, {'bf16' if dtype == torch.bfloat16 else 'f32'} local): "
                       f"{total_t:.1f} s on {oracle.get_threads()} threads; fp32 pseudo-gradient bytes / s"}

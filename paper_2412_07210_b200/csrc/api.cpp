@@ -483,19 +483,10 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
     launched += launch_pg_norm(dt, local, anchor, S, n, scr, h->part1[layer], ef, mode.cap, st);
   CUDA_TRY(h, cudaGetLastError());
   if (ev) CUDA_TRY(h, cudaEventRecord(ev[1], st));
-  // module norms of every replica on every rank: one K-scalar gather (R6)
-  const double* parts = &scr->send1;
-  if (h->K > 1) {
-    if (ln.mailbox) {
-      launched += launch_xchg(ln.mp, h->K, h->cfg.rank, 0, ++ln.seq[0], &scr->send1, scr->recv1, ln.xerr, st);
-      CUDA_TRY(h, cudaGetLastError());
-    } else {
-      NCCL_TRY(h, ncclAllGather(&scr->send1, scr->recv1, 1, ncclFloat64, ln.global, st));
-    }
-    parts = scr->recv1;
-  }
+  // module norms of every replica on every rank: one K-scalar gather (R6),
+  // then K2 on the gathered norms (fused into the mailbox exchange kernel when K > 1)
   DecideArgs d{};
-  d.parts = parts;
+  d.parts = h->K > 1 ? scr->recv1 : &scr->send1;
   d.M = M;
   d.N = N;
   d.my_n = h->sync_idx;
@@ -509,8 +500,14 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
   d.delta = h->cfg.anomaly_threshold;
   d.warmup = h->cfg.ema_warmup_rounds;
   d.flags = h->cfg.flags;
-  launched += launch_decide(d, st);
-  CUDA_TRY(h, cudaGetLastError());
+  if (h->K > 1 && ln.mailbox) {
+    launched += launch_xchg(ln.mp, h->K, h->cfg.rank, 0, ++ln.seq[0], &scr->send1, scr->recv1, ln.xerr, st, &d);
+    CUDA_TRY(h, cudaGetLastError());
+  } else {
+    if (h->K > 1) NCCL_TRY(h, ncclAllGather(&scr->send1, scr->recv1, 1, ncclFloat64, ln.global, st));
+    launched += launch_decide(d, st);
+    CUDA_TRY(h, cudaGetLastError());
+  }
   if (ev) CUDA_TRY(h, cudaEventRecord(ev[2], st));
 
   UpdateArgs u{};

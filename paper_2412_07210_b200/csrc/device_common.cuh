@@ -137,6 +137,75 @@ __device__ __forceinline__ void gather_store1_t(const UpdateArgs& p, int64_t k, 
   for (int q = 0; q < p.gather_M; ++q) store1(static_cast<T*>(p.gather[q]) + p.gather_off + k, v);
 }
 
+// ---------------------------------------------------------------- K2 (scalar chain)
+// K2 body (one thread): Alg. 2 l.443-451 on the gathered scalars, identically on every rank
+// (R6).  Used by decide_kernel and, fused after the exchange, by xchg_kernel (phase 0).
+static __device__ __noinline__ void decide_body(const DecideArgs& p) {
+  double G[EDIT_MAX_SYNC];
+  const int M = p.M, N = p.N;
+  edit_layer_stats_t* rec = p.rec;
+  for (int n = 0; n < N; ++n) {
+    double s = 0.0;
+    for (int m = 0; m < M; ++m) s += p.parts[n * M + m];  // module-level norm (R5)
+    G[n] = sqrt(s);
+  }
+  // IsAnomaly (R7-R10) with the pre-update EMA, then Eq. 1 for finite G.
+  for (int n = 0; n < N; ++n) {
+    edit_ema_t e = p.ema[n];
+    double z = nan("");
+    bool flagged = !isfinite(G[n]);  // R9: always excluded
+    if (!flagged && !(p.flags & EDIT_NO_AE) && e.count >= p.warmup && e.sigma > 0.0) {
+      z = (G[n] - e.mu) / e.sigma;
+      flagged = z > p.delta;
+    }
+    rec->z[n] = z;
+    rec->anomalous[n] = flagged ? 1 : 0;
+    if (flagged) {
+      G[n] = INFINITY;  // Alg. 2 l.445; Eq. 1 skipped
+    } else {
+      const double mu_new = p.alpha * G[n] + (1.0 - p.alpha) * e.mu;
+      const double dev = G[n] - mu_new;
+      e.sigma = sqrt((1.0 - p.alpha) * e.sigma * e.sigma + p.alpha * dev * dev);
+      e.mu = mu_new;
+      e.count += 1;
+      p.ema[n] = e;
+    }
+    rec->G[n] = G[n];
+    rec->ema_mu[n] = e.mu;
+    rec->ema_sigma[n] = e.sigma;
+    rec->ema_count[n] = e.count;
+  }
+  // gamma == 0 <=> no finite G (R11); Eq. 2 with exp(G_min) cancelled.
+  int nfinite = 0;
+  double gmin = INFINITY;
+  for (int n = 0; n < N; ++n)
+    if (isfinite(G[n])) {
+      ++nfinite;
+      gmin = fmin(gmin, G[n]);
+    }
+  double w[EDIT_MAX_SYNC];
+  double gamma = 0.0;
+  for (int n = 0; n < N; ++n) {
+    if (!isfinite(G[n])) w[n] = 0.0;
+    else w[n] = (p.flags & EDIT_NO_WA) ? 1.0 : exp(-(G[n] - gmin));
+    gamma += w[n];
+  }
+  const int rollback = nfinite == 0;
+  for (int n = 0; n < N; ++n) {
+    w[n] = rollback ? 0.0 : w[n] / gamma;
+    rec->w[n] = w[n];
+  }
+  for (int n = N; n < EDIT_MAX_SYNC; ++n) {
+    rec->G[n] = 0.0; rec->z[n] = 0.0; rec->w[n] = 0.0; rec->anomalous[n] = 0;
+  }
+  rec->num_sync = N;
+  *p.w_out = (float)w[p.my_n];
+  if (p.w_all_out)
+    for (int n = 0; n < EDIT_MAX_SYNC; ++n) p.w_all_out[n] = n < N ? (float)w[n] : 0.f;
+  *p.rollback_out = rollback;
+  *p.gsq_out = rollback ? 0.0 : G[p.my_n] * G[p.my_n];  // N == 1: G_bar = G
+}
+
 // ---------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -117,8 +117,9 @@ struct MailPtrs {
 inline size_t mailbox_bytes(int K) { return sizeof(unsigned long long) * 2 * 2 * kXchgPhases * (size_t)K; }
 // out[r] = rank r's *src for r < K.  One CTA; spins (bounded: ~10 s, then *err = 1) only in
 // this kernel, never in the big streaming kernels -> no cross-lane starvation.
+// dec != nullptr: K2 (decide) runs in the same kernel right after the gather.
 int launch_xchg(const MailPtrs& mp, int K, int me, int phase, unsigned long long seq, const double* src,
-                double* out, int* err, cudaStream_t st);
+                double* out, int* err, cudaStream_t st, const DecideArgs* dec = nullptr);
 
 // Launchers (kernels.cu).  Each returns the number of kernels launched.
 // cta_parts: grid_of(n, kVecReduce) fp64 slots for the per-CTA partials.

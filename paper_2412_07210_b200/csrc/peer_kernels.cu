@@ -518,8 +518,11 @@ __global__ void __launch_bounds__(kThreads) warm_ag_kernel(const __grid_constant
 // semantics at system scope), then wait for all K senders in its own mailbox (acquire).
 // Slots alternate by seq parity: a rank can only write seq+2 into a slot after the reader
 // published seq+1, i.e. after it finished reading seq -- no slot is overwritten early.
+// with_decide: K2 (decide_body) runs right after the gather in the same 1-CTA kernel (the
+// phase-0 exchange feeds it), saving one dependent launch per unit.
 __global__ void xchg_kernel(const __grid_constant__ MailPtrs mp, int K, int me, int phase,
-                            unsigned long long seq, const double* src, double* out, int* err) {
+                            unsigned long long seq, const double* src, double* out, int* err,
+                            const __grid_constant__ DecideArgs dec, int with_decide) {
   const int t = threadIdx.x;
   const int base = (phase * 2 + (int)(seq & 1)) * K;
   if (t < K) {
@@ -545,6 +548,10 @@ __global__ void xchg_kernel(const __grid_constant__ MailPtrs mp, int K, int me, 
     unsigned long long vb;
     asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(vb) : "l"(slot) : "memory");
     out[t] = __longlong_as_double((long long)vb);
+  }
+  if (with_decide) {
+    __syncthreads();  // out[0..K) written by threads 0..K-1 of this CTA
+    if (t == 0) decide_body(dec);
   }
 }
 
@@ -670,8 +677,10 @@ int launch_update_tma(int dtype, const UpdateArgs& a, int max_ctas, cudaStream_t
 }
 
 int launch_xchg(const MailPtrs& mp, int K, int me, int phase, unsigned long long seq, const double* src,
-                double* out, int* err, cudaStream_t st) {
-  xchg_kernel<<<1, 64, 0, st>>>(mp, K, me, phase, seq, src, out, err);
+                double* out, int* err, cudaStream_t st, const DecideArgs* dec) {
+  DecideArgs d{};
+  if (dec) d = *dec;
+  xchg_kernel<<<1, 64, 0, st>>>(mp, K, me, phase, seq, src, out, err, d, dec ? 1 : 0);
   return 1;
 }
 
