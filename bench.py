@@ -337,6 +337,7 @@ def main() -> None:
     sync.set_profiling(True)
     step_ms = []
     phase_ms = {k: 0.0 for k in sync.PHASES}
+    phase_busy_ms = {k: 0.0 for k in sync.PHASES}
     k4_elems = 0
     launches0 = sync.kernel_launches
     clocks = Clocks(local_rank)
@@ -354,6 +355,8 @@ def main() -> None:
             prof = sync.profile_collect()
             for k, v in prof["ms"].items():
                 phase_ms[k] += v
+            for k, v in prof["busy_ms"].items():
+                phase_busy_ms[k] += v
             k4_elems += prof["elements"]
             step_ms.append(max_over_ranks(t, world, dev))
     launches = sync.kernel_launches - launches0
@@ -435,7 +438,12 @@ def main() -> None:
         k4_bound, k4_peak, k4_B = "nvlink", MEASURED_NVL_GBS, k4_nvl_B
     else:
         k4_bound, k4_peak, k4_B = "hbm", hbm_peak, k4_hbm_B
-    k4_achieved = k4_B * k4_elems / (k4_ms * 1e-3) / 1e9 if k4_ms > 0 else None
+    # live achieved = the dominant kernel's algorithmic bytes over the time its launches were
+    # running (union of the units' intervals: with several lanes, launches of different units
+    # overlap, and the per-launch sum would count shared time twice)
+    k4_busy = phase_busy_ms["outer_update"]
+    k4_achieved = k4_B * k4_elems / (k4_busy * 1e-3) / 1e9 if k4_busy > 0 else None
+    k4_achieved_sum = k4_B * k4_elems / (k4_ms * 1e-3) / 1e9 if k4_ms > 0 else None
     k4_iso = k4_B * iso_elems / (iso_ms["outer_update"] * 1e-3) / 1e9 if iso_ms["outer_update"] > 0 else None
     k1_B = (2 * b_l + 4) if (peer and not registered) else (b_l + 4 + (4 if (N > 1 and not peer) else 0))
     k1_iso = k1_B * iso_elems / (iso_ms["pg_norm"] * 1e-3) / 1e9 if iso_ms["pg_norm"] > 0 else None
@@ -695,7 +703,11 @@ def main() -> None:
                          "peak_source": ("MEASURED_PEAKS.json hbm_gbs (measured)" if "_fallback" not in peaks
                                          else "fallback 6650 GB/s") if k4_bound == "hbm" else
                          "B200_PROFILING.md measured peer copy 770 GB/s per direction",
-                         "hbm_achieved_GBps": (k4_hbm_B * k4_elems / (k4_ms * 1e-3) / 1e9) if k4_ms > 0 else None},
+                         "hbm_achieved_GBps": (k4_hbm_B * k4_elems / (k4_busy * 1e-3) / 1e9) if k4_busy > 0 else None,
+                         "timing": "CUDA events around every launch on its lane stream, union of the launches' "
+                                   "intervals over the timed region",
+                         "busy_ms_per_step": k4_busy / args.steps, "launch_sum_ms_per_step": k4_ms / args.steps,
+                         "achieved_per_launch_sum": k4_achieved_sum},
             "roofline_isolated": {
                 "note": "same kernels, per-unit calls on one stream (no lane overlap), 2 rounds outside the timed "
                         "region; achieved = algorithmic bytes / the kernel's own CUDA-event time",
@@ -713,6 +725,7 @@ def main() -> None:
                               "note": "T_roof per BASELINE.md: max(P_r*(16+2b_l)/HBM, P_r*8(N-1)/N/NVLink); "
                                       "the peer path moves (b_l+4)(N-1)/N B/param, below the fp32 bus convention"},
             "phases_ms_per_step": {k: v / args.steps for k, v in phase_ms.items()},
+            "phases_busy_ms_per_step": {k: v / args.steps for k, v in phase_busy_ms.items()},
             "per_gpu_GBps": bytes_per_rank_round / (ms_per_step * 1e-3) / 1e9,
             "rollbacks_last_round": rollbacks, "beta_sample": betas, "anomaly": anomaly,
             "anomaly_sweep": anomaly_sweep,

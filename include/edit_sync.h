@@ -242,15 +242,17 @@ edit_status_t edit_sync_stats(edit_sync_t h, int32_t layer, edit_layer_stats_t* 
 edit_status_t edit_sync_get_state(edit_sync_t h, void* host_buf, size_t* bytes);
 edit_status_t edit_sync_set_state(edit_sync_t h, const void* host_buf, size_t bytes);
 
-/* Phase timing with CUDA events on the caller's stream (bench evidence, off by default).
- * Phases: 0 = K1 pg_norm, 1 = norm gather + K2 decide, 2 = weighted all-reduce (N > 1),
- * 3 = K3 + G_bar gather (N > 1), 4 = K4 outer_update.  collect() blocks until every unit
- * synced since the last collect has completed and returns the per-phase sums (ms) over
- * those syncs, plus the number of syncs and of elements the K4 launches processed. */
+/* Phase timing with CUDA events on the stream each unit runs on (bench evidence, off by
+ * default).  Phases: 0 = K1 pg_norm, 1 = norm gather + K2 decide, 2 = weighted all-reduce /
+ * peer RS (N > 1), 3 = K3 / Dbar-norm gather (N > 1), 4 = K4 outer_update / peer AG+update.
+ * collect() blocks until every unit synced since the last collect has completed and returns
+ * the per-phase sums (ms) over those syncs; busy_ms (nullable) = per phase, the union of the
+ * units' intervals (units on different lanes overlap: the time the phase's kernels were
+ * running at all); plus the number of syncs and of elements the K4 launches processed. */
 #define EDIT_NUM_PHASES 5
 edit_status_t edit_sync_set_profiling(edit_sync_t h, int32_t enable);
-edit_status_t edit_sync_profile_collect(edit_sync_t h, double phase_ms[EDIT_NUM_PHASES], int64_t* syncs,
-                                        int64_t* elements);
+edit_status_t edit_sync_profile_collect(edit_sync_t h, double phase_ms[EDIT_NUM_PHASES],
+                                        double busy_ms[EDIT_NUM_PHASES], int64_t* syncs, int64_t* elements);
 
 /* Number of kernels the library launched so far on this handle (bench evidence). */
 int64_t edit_sync_kernel_launches(edit_sync_t h);

@@ -1036,27 +1036,58 @@ edit_status_t edit_sync_set_profiling(edit_sync_t h, int32_t enable) {
   return EDIT_OK;
 }
 
-edit_status_t edit_sync_profile_collect(edit_sync_t h, double phase_ms[EDIT_NUM_PHASES], int64_t* syncs,
-                                        int64_t* elements) {
+edit_status_t edit_sync_profile_collect(edit_sync_t h, double phase_ms[EDIT_NUM_PHASES], double busy_ms[EDIT_NUM_PHASES],
+                                        int64_t* syncs, int64_t* elements) {
   if (!h || !phase_ms) return fail(EDIT_ERR_INVALID_ARG, "null argument");
   if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
   for (int p = 0; p < EDIT_NUM_PHASES; ++p) phase_ms[p] = 0.0;
   int64_t elems = 0;
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  // per phase: the [start, end) interval of every unit, in ms from the first unit's start
+  std::vector<std::vector<std::pair<double, double>>> iv(EDIT_NUM_PHASES);
+  cudaEvent_t ref = nullptr;
   for (int32_t layer : h->pending) {
     cudaEvent_t* ev = &h->prof[(size_t)layer * (EDIT_NUM_PHASES + 1)];
     CUDA_TRY(h, cudaEventSynchronize(ev[EDIT_NUM_PHASES]));
+    if (!ref) ref = ev[0];
     // N == 1 records no events for the empty phases 2 and 3 (no all-reduce, no K3)
     const int seq[6] = {0, 1, 2, 3, 4, 5}, seq1[4] = {0, 1, 2, 5};
     const int* q = h->N > 1 ? seq : seq1;
     const int nq = h->N > 1 ? 6 : 4;
     for (int k = 0; k + 1 < nq; ++k) {
-      float ms = 0.f;
+      float ms = 0.f, t0 = 0.f, t1 = 0.f;
       CUDA_TRY(h, cudaEventElapsedTime(&ms, ev[q[k]], ev[q[k + 1]]));
-      phase_ms[q[k + 1] == 5 ? 4 : q[k]] += ms;
+      const int ph = q[k + 1] == 5 ? 4 : q[k];
+      phase_ms[ph] += ms;
+      if (busy_ms) {
+        CUDA_TRY(h, cudaEventElapsedTime(&t0, ref, ev[q[k]]));
+        CUDA_TRY(h, cudaEventElapsedTime(&t1, ref, ev[q[k + 1]]));
+        iv[ph].emplace_back(t0, t1);
+      }
     }
     elems += h->numel[layer];
   }
+  // busy time of a phase = the union of its units' intervals (units on different lanes
+  // overlap, so the plain sum over-counts the time the phase's kernels occupied the GPU)
+  if (busy_ms)
+    for (int p = 0; p < EDIT_NUM_PHASES; ++p) {
+      auto& v = iv[p];
+      std::sort(v.begin(), v.end());
+      double total = 0.0, lo = 0.0, hi = 0.0;
+      bool open = false;
+      for (const auto& x : v) {
+        if (!open || x.first > hi) {
+          if (open) total += hi - lo;
+          lo = x.first;
+          hi = x.second;
+          open = true;
+        } else if (x.second > hi) {
+          hi = x.second;
+        }
+      }
+      if (open) total += hi - lo;
+      busy_ms[p] = total;
+    }
   if (syncs) *syncs = (int64_t)h->pending.size();
   if (elements) *elements = elems;
   h->pending.clear();

@@ -96,8 +96,8 @@ def load_library() -> ctypes.CDLL:
     lib.edit_sync_get_state.restype = S
     lib.edit_sync_set_state.argtypes, lib.edit_sync_set_state.restype = [P, P, ctypes.c_size_t], S
     lib.edit_sync_set_profiling.argtypes, lib.edit_sync_set_profiling.restype = [P, I32], S
-    lib.edit_sync_profile_collect.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64),
-                                              ctypes.POINTER(I64)]
+    lib.edit_sync_profile_collect.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                              ctypes.POINTER(I64), ctypes.POINTER(I64)]
     lib.edit_sync_profile_collect.restype = S
     lib.edit_sync_kernel_launches.argtypes, lib.edit_sync_kernel_launches.restype = [P], I64
     lib.edit_sync_destroy.argtypes, lib.edit_sync_destroy.restype = [P], S
@@ -343,11 +343,14 @@ class EditSync:
         _check(self._lib.edit_sync_set_profiling(self._h, 1 if enable else 0))
 
     def profile_collect(self) -> dict:
-        """Per-phase CUDA-event ms summed over the syncs since the last collect."""
+        """Per-phase CUDA-event ms summed over the syncs since the last collect, and per-phase
+        busy ms (union of the units' intervals: overlapping lanes counted once)."""
         ms = (ctypes.c_double * len(self.PHASES))()
+        busy = (ctypes.c_double * len(self.PHASES))()
         syncs, elems = ctypes.c_int64(), ctypes.c_int64()
-        _check(self._lib.edit_sync_profile_collect(self._h, ms, ctypes.byref(syncs), ctypes.byref(elems)))
-        return {"ms": dict(zip(self.PHASES, list(ms))), "syncs": syncs.value, "elements": elems.value}
+        _check(self._lib.edit_sync_profile_collect(self._h, ms, busy, ctypes.byref(syncs), ctypes.byref(elems)))
+        return {"ms": dict(zip(self.PHASES, list(ms))), "busy_ms": dict(zip(self.PHASES, list(busy))),
+                "syncs": syncs.value, "elements": elems.value}
 
     @property
     def kernel_launches(self) -> int:
