@@ -679,11 +679,15 @@ def main() -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_cpu_baseline(args.model, dtype)
+        # labelled extrapolation (by parameter count) of one full round of this config
+        cpu["extrapolated_full_round_s"] = 4.0 * P_r / (cpu["value"] * 1e9)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "ms_per_step_median": statistics.median(step_ms), "ms_per_step_min": min(step_ms),
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"llama-{args.model}-shaped shards, {M}x{N} shard x sync mesh, full sync round "
                                    f"of {len(units)} units ({P_r} params/rank), {args.dtype} local + f32 "
