@@ -431,6 +431,80 @@ __global__ void __launch_bounds__(1024) k1_ldg4(const __nv_bfloat16* local, cons
   if (acc == 1234.5f) out[0] = acc;
 }
 
+// 4-element layout + TMA bulk STORES: results written in place into the stage (conflict-free
+// 16-B / 8-B shared stores), one elected consumer thread stores the tile with cp.async.bulk
+// (fewer, wider write requests than 16-B STG), the stage is released once the stores READ it.
+template <int CWn>
+__global__ void __launch_bounds__(32 * (1 + CWn)) k4_tma4_bulk(__nv_bfloat16* local, float* anchor, float* mom,
+                                                              int64_t n8, int K, int V) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ uint64_t full[MAXK], empty[MAXK];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < K; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const float beta = 0.5f, mu = 0.85f, nu = 0.8f;
+  const int64_t nt = (n8 + V - 1) / V;
+  const int sb = V * 80;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t q = blockIdx.x; q < nt; q += gridDim.x, ++it) {
+        const int s = it % K, use = it / K;
+        if (use) mbar_wait(&empty[s], (use - 1) & 1);
+        const int64_t v0 = q * V;
+        const int nv = (int)min((int64_t)V, n8 - v0);
+        char* st = smem + (size_t)s * sb;
+        mbar_expect_tx(&full[s], nv * 80);
+        tma_load(st, anchor + 8 * v0, nv * 32, &full[s]);
+        tma_load(st + V * 32, mom + 8 * v0, nv * 32, &full[s]);
+        tma_load(st + V * 64, local + 8 * v0, nv * 16, &full[s]);
+      }
+    }
+  } else {
+    const int t = threadIdx.x - 32;
+    int it = 0, prev = -1;
+    for (int64_t q = blockIdx.x; q < nt; q += gridDim.x, ++it) {
+      const int s = it % K, use = it / K;
+      mbar_wait(&full[s], use & 1);
+      const int64_t v0 = q * V;
+      const int nv = (int)min((int64_t)V, n8 - v0);
+      char* st = smem + (size_t)s * sb;
+      for (int v = t; v < 2 * nv; v += 32 * CWn) {
+        float4* ap = reinterpret_cast<float4*>(st) + v;
+        float4* mp = reinterpret_cast<float4*>(st + V * 32) + v;
+        __nv_bfloat16* lp = reinterpret_cast<__nv_bfloat16*>(st + V * 64) + 4 * v;
+        float4 a = *ap, m = *mp;
+        float l[4];
+        ld4h(lp, l);
+        float g;
+        g = beta * (a.x - l[0]); m.x = fmaf(mu, m.x, g); a.x = a.x - nu * fmaf(mu, m.x, g);
+        g = beta * (a.y - l[1]); m.y = fmaf(mu, m.y, g); a.y = a.y - nu * fmaf(mu, m.y, g);
+        g = beta * (a.z - l[2]); m.z = fmaf(mu, m.z, g); a.z = a.z - nu * fmaf(mu, m.z, g);
+        g = beta * (a.w - l[3]); m.w = fmaf(mu, m.w, g); a.w = a.w - nu * fmaf(mu, m.w, g);
+        *ap = a;
+        *mp = m;
+        const float o[4] = {a.x, a.y, a.z, a.w};
+        st4h(lp, o);
+      }
+      fence_async_smem();
+      named_bar(1, 32 * CWn);
+      if (t == 0) {
+        tma_store(anchor + 8 * v0, st, nv * 32);
+        tma_store(mom + 8 * v0, st + V * 32, nv * 32);
+        tma_store(local + 8 * v0, st + V * 64, nv * 16);
+        bulk_commit();
+        bulk_wait_read<1>();
+        if (prev >= 0) mbar_arrive(&empty[prev]);
+      }
+      prev = s;
+    }
+    if (t == 0) bulk_wait_all();
+  }
+}
+
 int main(int argc, char** argv) {
   const int64_t n = argc > 1 ? atoll(argv[1]) : 202383360;  // a 7B decoder unit
   const int64_t n8 = n / 8;
@@ -472,6 +546,7 @@ int main(int argc, char** argv) {
     CK(cudaFuncSetAttribute(k4_tma4<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, K4 * V * 80));
     CK(cudaFuncSetAttribute(k1_tma4<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, K1 * V * 48));
     CK(cudaFuncSetAttribute(k4_tma4<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, K4 * V * 80));
+    CK(cudaFuncSetAttribute(k4_tma4_bulk<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, K4 * V * 80));
     for (int g : grids) {
       const float a1 = timeit([&] { k1_tma<<<g, NT, K1 * V * 48>>>(local, anchor, n8, out, K1, V); });
       const float b1 = timeit([&] { k1_tma4<8><<<g, 288, K1 * V * 48>>>(local, anchor, n8, out, K1, V); });
@@ -480,6 +555,8 @@ int main(int argc, char** argv) {
       const float b4 = timeit([&] { k4_tma4<8><<<g, 288, K4 * V * 80>>>(local, anchor, mom, n8, K4, V); });
       const float c4 = timeit([&] { k4_tma4<16><<<g, 544, K4 * V * 80>>>(local, anchor, mom, n8, K4, V); });
       auto ps = [&](double bpp, float ms) { return bpp * n / ms / 1e6 / g; };
+      const float d4 = timeit([&] { k4_tma4_bulk<8><<<g, 288, K4 * V * 80>>>(local, anchor, mom, n8, K4, V); });
+      printf("V %4d grid %3d | K4 v4 + TMA bulk store %5.1f GB/s/SM\n", V, g, ps(20, d4));
       printf("V %4d K1st %d K4st %d grid %3d | GB/s/SM  K1: v8 %5.1f  v4w8 %5.1f  v4w16 %5.1f | K4: v8 %5.1f  v4w8 %5.1f  "
              "v4w16 %5.1f | total@grid K1 %6.0f K4 %6.0f\n",
              V, K1, K4, g, ps(6, a1), ps(6, b1), ps(6, c1), ps(20, a4), ps(20, b4), ps(20, c4),
