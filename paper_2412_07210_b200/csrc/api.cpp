@@ -131,7 +131,18 @@ struct Lane {
   unsigned long long* mailbox = nullptr;
   MailPtrs mp{};
   unsigned long long seq[kXchgPhases] = {0, 0};
+  unsigned long long* dseq = nullptr;  // graph mode: device-side sequence counters [kXchgPhases]
   int* xerr = nullptr;
+};
+
+// EDIT_GRAPH=1: edit_sync_round captures the round once per set of buffer pointers into a
+// CUDA graph and replays it (measured boundary cost of dependent kernels: plain 3.7-4.1 us,
+// graph 0.6-1.4 us, profiles/r1_pdl_graph_launch_gaps.txt).  Requires the mailbox sequence
+// numbers on the device (Lane::dseq); must be equal on every rank.
+struct RoundGraph {
+  std::vector<uintptr_t> key;  // the 3L buffer pointers
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;        // kernels per replay
 };
 
 struct edit_sync {
@@ -170,6 +181,8 @@ struct edit_sync {
   cudaEvent_t fork = nullptr;     // round API / scheduler: "the caller's inputs are ready"
   // profiling: EDIT_NUM_PHASES + 1 timing events per unit, and the units pending collection
   bool profiling = false;
+  bool graph = false;               // EDIT_GRAPH=1 (round replay from CUDA graphs)
+  std::vector<RoundGraph> graphs;   // small cache, most recent last
   std::vector<cudaEvent_t> prof;
   std::vector<int32_t> pending;
   // host-buffer variant: two device staging slots + copy-in / copy-out streams
@@ -296,6 +309,7 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
   INIT_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
   h->peer_ctas = h->num_sms;
   if (const char* e = getenv("EDIT_XCHG")) h->dev_xchg = strcmp(e, "nccl") != 0;
+  if (const char* e = getenv("EDIT_GRAPH")) h->graph = atoi(e) != 0;
   if (const char* e = getenv("EDIT_PEER_TILE")) {
     const int v = atoi(e);
     if (v >= 32 && v <= 4096 && (v & 31) == 0) h->peer_tile = v;
@@ -383,6 +397,10 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
       INIT_CUDA(cudaMemset(ln.mailbox, 0, align_up(mailbox_bytes(K), 256)));
       INIT_CUDA(cudaMalloc(reinterpret_cast<void**>(&ln.xerr), sizeof(int)));
       INIT_CUDA(cudaMemset(ln.xerr, 0, sizeof(int)));
+      if (h->graph) {
+        INIT_CUDA(cudaMalloc(reinterpret_cast<void**>(&ln.dseq), sizeof(unsigned long long) * kXchgPhases));
+        INIT_CUDA(cudaMemset(ln.dseq, 0, sizeof(unsigned long long) * kXchgPhases));
+      }
       INIT_CUDA(cudaDeviceSynchronize());
       void* mine = ln.mailbox;
       size_t mb = mailbox_bytes(K);
@@ -456,6 +474,16 @@ struct Mode {
   int part = 0;   // > 0: partition mode, K1 / K4 / peer kernels on <= part persistent CTAs
 };
 
+// cudaEventRecord that stays a real (external) event record when `st` is being captured into
+// a CUDA graph (EDIT_GRAPH=1): the round's done / profiling events are read by the host later.
+static cudaError_t record_event(cudaEvent_t ev, cudaStream_t st) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  const cudaError_t e = cudaStreamIsCapturing(st, &cap);
+  if (e != cudaSuccess) return e;
+  return cap == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal)
+                                              : cudaEventRecord(ev, st);
+}
+
 static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* local, float* anchor, float* momentum,
                                cudaStream_t st, const Mode& mode) {
   const bool ef = mode.ef;
@@ -467,7 +495,7 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
 
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   cudaEvent_t* ev = h->profiling ? &h->prof[(size_t)layer * (EDIT_NUM_PHASES + 1)] : nullptr;
-  if (ev) CUDA_TRY(h, cudaEventRecord(ev[0], st));
+  if (ev) CUDA_TRY(h, record_event(ev[0], st));
   // K1: Delta and its shard norm (Alg. 2 l.442-443)
   float* S = (N > 1 && !h->peer) ? ln.S : nullptr;
   // peer path: read the members' registered locals directly, else stage a copy of ours
@@ -482,7 +510,7 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
   else
     launched += launch_pg_norm(dt, local, anchor, S, n, scr, h->part1[layer], ef, mode.cap, st);
   CUDA_TRY(h, cudaGetLastError());
-  if (ev) CUDA_TRY(h, cudaEventRecord(ev[1], st));
+  if (ev) CUDA_TRY(h, record_event(ev[1], st));
   // module norms of every replica on every rank: one K-scalar gather (R6),
   // then K2 on the gathered norms (fused into the mailbox exchange kernel when K > 1)
   DecideArgs d{};
@@ -501,14 +529,15 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
   d.warmup = h->cfg.ema_warmup_rounds;
   d.flags = h->cfg.flags;
   if (h->K > 1 && ln.mailbox) {
-    launched += launch_xchg(ln.mp, h->K, h->cfg.rank, 0, ++ln.seq[0], &scr->send1, scr->recv1, ln.xerr, st, &d);
+    launched += launch_xchg(ln.mp, h->K, h->cfg.rank, 0, ++ln.seq[0], &scr->send1, scr->recv1, ln.xerr, st, &d,
+                            ln.dseq);
     CUDA_TRY(h, cudaGetLastError());
   } else {
     if (h->K > 1) NCCL_TRY(h, ncclAllGather(&scr->send1, scr->recv1, 1, ncclFloat64, ln.global, st));
     launched += launch_decide(d, st);
     CUDA_TRY(h, cudaGetLastError());
   }
-  if (ev) CUDA_TRY(h, cudaEventRecord(ev[2], st));
+  if (ev) CUDA_TRY(h, record_event(ev[2], st));
 
   UpdateArgs u{};
   u.local = local;
@@ -533,23 +562,24 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
     const Slicing sl = slicing_of(n, N, h->sync_idx, h->peer_tile);
     launched += launch_rs(dt, pp, sl, anchor, ln.Down, scr, h->part2[layer], mode.peer_ctas, ef, mode.smem_kb, st);
     CUDA_TRY(h, cudaGetLastError());
-    if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
+    if (ev) CUDA_TRY(h, record_event(ev[3], st));
     // ||Dbar||^2 of the module = sum over every slice of every shard: one K-scalar gather
     // (also the barrier after which every member's D slice is complete)
     if (ln.mailbox) {
-      launched += launch_xchg(ln.mp, h->K, h->cfg.rank, 1, ++ln.seq[1], &scr->send2, scr->recv2, ln.xerr, st);
+      launched += launch_xchg(ln.mp, h->K, h->cfg.rank, 1, ++ln.seq[1], &scr->send2, scr->recv2, ln.xerr, st,
+                              nullptr, ln.dseq);
       CUDA_TRY(h, cudaGetLastError());
     } else {
       NCCL_TRY(h, ncclAllGather(&scr->send2, scr->recv2, 1, ncclFloat64, ln.global, st));
     }
-    if (ev) CUDA_TRY(h, cudaEventRecord(ev[4], st));
+    if (ev) CUDA_TRY(h, record_event(ev[4], st));
     u.gparts = scr->recv2;
     u.n_gparts = h->K;
     launched += launch_ag_update(dt, u, pp, sl, mode.peer_ctas, ef, mode.smem_kb, st);
   } else if (N > 1) {
     // Eq. 3: Dbar = sum_n w_n Delta_n, the weight applied inside NCCL (PreMulSum)
     NCCL_TRY(h, ncclAllReduce(S, S, (size_t)n, ncclFloat32, ln.ops[layer], ln.sync, st));
-    if (ev) CUDA_TRY(h, cudaEventRecord(ev[3], st));
+    if (ev) CUDA_TRY(h, record_event(ev[3], st));
     launched += launch_sumsq(S, n, scr, h->part2[layer], ef, mode.cap, st);
     CUDA_TRY(h, cudaGetLastError());
     if (M > 1) {
@@ -561,7 +591,7 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
       u.n_gparts = 1;
     }
     u.dbar = S;
-    if (ev) CUDA_TRY(h, cudaEventRecord(ev[4], st));
+    if (ev) CUDA_TRY(h, record_event(ev[4], st));
   } else {
     u.dbar = nullptr;  // Dbar = Delta, G_bar = G (module level)
     u.gparts = &scr->gsq;
@@ -579,10 +609,10 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
     NCCL_TRY(h, ncclAllGather(gd, gd + 1, 1, ncclFloat64, ln.shard, st));
   }
   if (ev) {
-    CUDA_TRY(h, cudaEventRecord(ev[5], st));
+    CUDA_TRY(h, record_event(ev[5], st));
     h->pending.push_back(layer);
   }
-  CUDA_TRY(h, cudaEventRecord(h->done[layer], st));
+  CUDA_TRY(h, record_event(h->done[layer], st));  // read by edit_sync_stats / acquire
   h->launches += launched;
   return EDIT_OK;
 }
@@ -739,19 +769,63 @@ edit_status_t edit_sync_round(edit_sync_t h, void* const* locals, float* const* 
   }
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
-  CUDA_TRY(h, cudaEventRecord(h->fork, cs));
+  const bool use_graph = h->graph && (h->K == 1 || h->lanes[0].dseq != nullptr);
+  std::vector<uintptr_t> key;
+  if (use_graph) {
+    key.reserve(3 * (size_t)L);
+    for (int u = 0; u < L; ++u) {
+      key.push_back(reinterpret_cast<uintptr_t>(locals[u]));
+      key.push_back(reinterpret_cast<uintptr_t>(anchors[u]));
+      key.push_back(reinterpret_cast<uintptr_t>(momenta[u]));
+    }
+    key.push_back(h->profiling ? 1u : 0u);  // a profiled capture holds the phase events
+    for (const RoundGraph& g : h->graphs)
+      if (g.key == key) {
+        CUDA_TRY(h, cudaGraphLaunch(g.exec, cs));
+        h->launches += g.launches;
+        if (h->profiling)
+          for (int u = 0; u < L; ++u) h->pending.push_back(u);
+        return EDIT_OK;
+      }
+    CUDA_TRY(h, cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+  }
+  const int64_t launches0 = h->launches;
+  edit_status_t rc = EDIT_OK;
   const int nl = (int)h->lanes.size();
-  for (Lane& ln : h->lanes) CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->fork, 0));
-  for (int u = 0; u < L; ++u) {
+  if (cudaEventRecord(h->fork, cs) != cudaSuccess) rc = fail(EDIT_ERR_CUDA, "fork record");
+  for (Lane& ln : h->lanes)
+    if (rc == EDIT_OK && cudaStreamWaitEvent(ln.stream, h->fork, 0) != cudaSuccess) rc = fail(EDIT_ERR_CUDA, "fork wait");
+  for (int u = 0; u < L && rc == EDIT_OK; ++u) {
     Lane& ln = h->lanes[u % nl];
-    edit_status_t rc = sync_unit(h, ln, u, locals[u], anchors[u], momenta[u], ln.stream,
-                                 Mode{h->ef_direct, 0, h->peer_ctas, 0});
-    if (rc != EDIT_OK) return rc;
+    rc = sync_unit(h, ln, u, locals[u], anchors[u], momenta[u], ln.stream, Mode{h->ef_direct, 0, h->peer_ctas, 0});
   }
   for (Lane& ln : h->lanes) {
-    CUDA_TRY(h, cudaEventRecord(ln.tail, ln.stream));
-    CUDA_TRY(h, cudaStreamWaitEvent(cs, ln.tail, 0));
+    if (rc != EDIT_OK) break;
+    if (cudaEventRecord(ln.tail, ln.stream) != cudaSuccess || cudaStreamWaitEvent(cs, ln.tail, 0) != cudaSuccess)
+      rc = fail(EDIT_ERR_CUDA, "join");
   }
+  if (!use_graph) return rc;
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
+  if (rc != EDIT_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  CUDA_TRY(h, ec);
+  RoundGraph g;
+  g.key = std::move(key);
+  g.launches = h->launches - launches0;
+  const cudaError_t ei = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  CUDA_TRY(h, ei);
+  h->launches = launches0;  // capture launched nothing; the replay below does
+  if (h->graphs.size() >= 4) {
+    cudaGraphExecDestroy(h->graphs.front().exec);
+    h->graphs.erase(h->graphs.begin());
+  }
+  h->graphs.push_back(std::move(g));
+  CUDA_TRY(h, cudaGraphLaunch(h->graphs.back().exec, cs));
+  h->launches += h->graphs.back().launches;
   return EDIT_OK;
 }
 
@@ -1123,6 +1197,7 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
     if (ln.Down) cudaFree(ln.Down);
     if (ln.S) cudaFree(ln.S);
     if (ln.mailbox) cudaFree(ln.mailbox);
+    if (ln.dseq) cudaFree(ln.dseq);
     if (ln.xerr) cudaFree(ln.xerr);
     if (ln.shard) ncclCommDestroy(ln.shard);
     if (ln.sync) ncclCommDestroy(ln.sync);
@@ -1130,6 +1205,9 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
     if (ln.tail) cudaEventDestroy(ln.tail);
     if (ln.stream) cudaStreamDestroy(ln.stream);
   }
+  for (RoundGraph& g : h->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  h->graphs.clear();
   if (h->fork) cudaEventDestroy(h->fork);
   if (h->warm_dev) cudaFree(h->warm_dev);
   for (auto e : h->done)

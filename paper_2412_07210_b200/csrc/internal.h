@@ -118,8 +118,11 @@ inline size_t mailbox_bytes(int K) { return sizeof(unsigned long long) * 2 * 2 *
 // out[r] = rank r's *src for r < K.  One CTA; spins (bounded: ~10 s, then *err = 1) only in
 // this kernel, never in the big streaming kernels -> no cross-lane starvation.
 // dec != nullptr: K2 (decide) runs in the same kernel right after the gather.
+// dseq != nullptr: seq comes from (and advances) the lane's device counter dseq[phase]
+// (graph-replayable); else the host-passed seq.
 int launch_xchg(const MailPtrs& mp, int K, int me, int phase, unsigned long long seq, const double* src,
-                double* out, int* err, cudaStream_t st, const DecideArgs* dec = nullptr);
+                double* out, int* err, cudaStream_t st, const DecideArgs* dec = nullptr,
+                unsigned long long* dseq = nullptr);
 
 // Launchers (kernels.cu).  Each returns the number of kernels launched.
 // cta_parts: grid_of(n, kVecReduce) fp64 slots for the per-CTA partials.

@@ -520,10 +520,22 @@ __global__ void __launch_bounds__(kThreads) warm_ag_kernel(const __grid_constant
 // published seq+1, i.e. after it finished reading seq -- no slot is overwritten early.
 // with_decide: K2 (decide_body) runs right after the gather in the same 1-CTA kernel (the
 // phase-0 exchange feeds it), saving one dependent launch per unit.
+// dseq != nullptr: the sequence number is this lane's device counter for the phase, incremented
+// here (so a captured CUDA graph can be replayed: every replay takes the next number; only this
+// 1-CTA kernel on the lane's stream touches the counter); else the host-passed seq.
 __global__ void xchg_kernel(const __grid_constant__ MailPtrs mp, int K, int me, int phase,
-                            unsigned long long seq, const double* src, double* out, int* err,
-                            const __grid_constant__ DecideArgs dec, int with_decide) {
+                            unsigned long long seq_arg, unsigned long long* dseq, const double* src, double* out,
+                            int* err, const __grid_constant__ DecideArgs dec, int with_decide) {
   const int t = threadIdx.x;
+  __shared__ unsigned long long s_seq;
+  if (dseq) {
+    if (t == 0) {
+      s_seq = dseq[phase] + 1;
+      dseq[phase] = s_seq;
+    }
+    __syncthreads();
+  }
+  const unsigned long long seq = dseq ? s_seq : seq_arg;
   const int base = (phase * 2 + (int)(seq & 1)) * K;
   if (t < K) {
     const double v = *src;
@@ -677,10 +689,10 @@ int launch_update_tma(int dtype, const UpdateArgs& a, int max_ctas, cudaStream_t
 }
 
 int launch_xchg(const MailPtrs& mp, int K, int me, int phase, unsigned long long seq, const double* src,
-                double* out, int* err, cudaStream_t st, const DecideArgs* dec) {
+                double* out, int* err, cudaStream_t st, const DecideArgs* dec, unsigned long long* dseq) {
   DecideArgs d{};
   if (dec) d = *dec;
-  xchg_kernel<<<1, 64, 0, st>>>(mp, K, me, phase, seq, src, out, err, d, dec ? 1 : 0);
+  xchg_kernel<<<1, 64, 0, st>>>(mp, K, me, phase, seq, dseq, src, out, err, d, dec ? 1 : 0);
   return 1;
 }
 

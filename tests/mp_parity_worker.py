@@ -70,7 +70,8 @@ def warm_check(units, M, N, m_idx, n_idx, rank, world, dtype, dtype_s, dev, s, m
 def run_case(mesh, dtype_s, config, algo="peer", api="unit"):
     # api -- unit: edit_layer_sync x L; round: edit_sync_round; reg: registered locals + round;
     # gather: fused shard all-gather + round; sched: prefetch scheduler (depth 1);
-    # schedpart: registered locals + scheduler in partition mode (8 CTAs, unit 0 full grid)
+    # schedpart: registered locals + scheduler in partition mode (8 CTAs, unit 0 full grid);
+    # graph: EDIT_GRAPH=1 round captured into a CUDA graph, the checked round is a replay
     M, N = (int(x) for x in mesh.split("x"))
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     assert world == M * N
@@ -109,10 +110,13 @@ def run_case(mesh, dtype_s, config, algo="peer", api="unit"):
         raise SystemExit(f"unknown config {config}")
     numel = [synth.shard_numel(u.numel, M) for u in units]
     uid = broadcast_unique_id()
+    if api == "graph":
+        os.environ["EDIT_GRAPH"] = "1"   # read at init: device-side mailbox sequence numbers
     s = EditSync(numel, shard_dim=M, sync_dim=N, rank=rank, device=dev, param_dtype=dtype,
                  outer_lr=cfg.outer_lr, outer_momentum=cfg.outer_momentum, clip_threshold=cfg.clip_threshold,
                  clip_eps=cfg.clip_eps, anomaly_threshold=cfg.anomaly_threshold, ema_alpha=cfg.ema_alpha,
                  ema_warmup_rounds=cfg.ema_warmup_rounds, flags=cfg.flags, unique_id=uid, algo=algo)
+    os.environ.pop("EDIT_GRAPH", None)
     ema0 = [[oracle.Ema() for _ in range(N)] for _ in units]
     if seed_ema:
         mu = np.array([[synth.ema_seed(u, n, recipe)[0] for n in range(N)] for u in units])
@@ -148,6 +152,15 @@ def run_case(mesh, dtype_s, config, algo="peer", api="unit"):
         for i in range(len(units)):
             s.acquire(i, stream)
         s.end_round(stream)
+    elif api == "graph":               # EDIT_GRAPH=1: captured round, then a REPLAY is checked
+        saved = [x.clone() for x in loc + anc + mom]
+        state0 = s.get_state()
+        s.sync_round(loc, anc, mom)    # capture + first launch (results discarded)
+        torch.cuda.synchronize()
+        for x, y in zip(loc + anc + mom, saved):
+            x.copy_(y)                 # same buffers -> the next call replays the graph
+        s.set_state(state0)
+        s.sync_round(loc, anc, mom)
     elif api in ("round", "reg", "gather"):
         if api == "reg":
             s.register_locals(loc)     # peer path reads the members' locals directly

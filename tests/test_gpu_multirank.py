@@ -7,6 +7,7 @@ cross-rank invariants.  Cases = (dtype, config, exchange algo, API):
   unit   edit_layer_sync per unit           round  edit_sync_round (2 lanes)
   reg    registered locals + round (peer)   gather fused shard all-gather + round (NEXT-2)
   sched  prefetch scheduler (a8)            schedpart  scheduler in partition mode (8 CTAs)
+  graph  EDIT_GRAPH=1 round (captured CUDA graph; the checked round is a replay)
 configs: ragged units, toy (BASELINE configs[0]: 4 x 64K fp32, replica 1 planted x4),
 toy_clip, rollback (every replica anomalous), nan (one replica with a NaN param),
 llama350m_sample, warm (NEXT-3 warm-up gradient all-reduce)."""
@@ -42,7 +43,7 @@ def _core_cases(mesh):
     M, N = (int(x) for x in mesh.split("x"))
     c = [("bf16", "ragged", "peer", "unit"), ("f32", "toy", "nccl", "unit"), ("bf16", "nan", "peer", "round"),
          ("f32", "toy_clip", "peer", "unit")]
-    c += [("bf16", "ragged", "peer", "schedpart"), ("bf16", "toy", "nccl", "sched")]
+    c += [("bf16", "ragged", "peer", "schedpart"), ("bf16", "toy", "nccl", "sched"), ("bf16", "ragged", "peer", "graph")]
     if N > 1:
         c += [("bf16", "ragged", "peer", "reg"), ("bf16", "warm", "peer", "unit"), ("bf16", "rollback", "nccl", "round")]
     if M > 1:
@@ -68,6 +69,8 @@ def _mesh_cases():
         by_mesh[mesh].append((dt, cfg, "peer", "reg"))
         by_mesh[mesh].append((dt, cfg, "peer", "schedpart"))
         by_mesh[mesh].append((dt, cfg, "nccl", "sched"))
+        by_mesh[mesh].append((dt, cfg, "peer", "graph"))
+        by_mesh[mesh].append((dt, cfg, "nccl", "graph"))
     return dict(sorted(by_mesh.items()))
 
 

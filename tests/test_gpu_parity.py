@@ -301,6 +301,43 @@ def test_round_api_matches_oracle_and_sequential_bitwise(dtype):
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_round_api_graph_replay_matches_oracle(dtype, monkeypatch):
+    # EDIT_GRAPH=1: the round is captured once per buffer set and replayed; three rounds on the
+    # same buffers (two replays) plus one on new buffers (a second capture) == oracle, and the
+    # first round == the non-graph path bit for bit
+    units = [synth.Unit(f"u{i}", n, ()) for i, n in enumerate([1_000_003, 65_536, 7, 2_000_000])]
+    monkeypatch.setenv("EDIT_GRAPH", "1")
+    c = Case(units, DTYPES[dtype])
+    monkeypatch.delenv("EDIT_GRAPH")
+    ref = Case(units, DTYPES[dtype])
+    ref.sync.sync_round(ref.local, ref.anchor, ref.mom)
+    for r in range(4):
+        if r > 0:
+            for i, u in enumerate(units):   # next round from the oracle's state, in place
+                c.anchor[i].copy_(torch.from_numpy(c.o_anchor[i]))
+                c.mom[i].copy_(torch.from_numpy(c.o_mom[i]))
+                c.local[i].copy_(synth.shard_local(u, i, 1, 0, 0, c.anchor[i], c.dtype, DEV, c.recipe, 1.0, r))
+                c.o_local[i] = parity.to_oracle_local(c.local[i])
+        if r == 3:                          # new buffers -> a second captured graph
+            c.local = [x.clone() for x in c.local]
+        c.sync.sync_round(c.local, c.anchor, c.mom)
+        torch.cuda.synchronize()
+        for i in range(len(units)):
+            if r == 0:
+                assert torch.equal(c.local[i], ref.local[i]) and torch.equal(c.anchor[i], ref.anchor[i])
+                assert torch.equal(c.mom[i], ref.mom[i])
+            loc, anc, mom, ema, out = oracle.sync_unit(c.cfg, c.o_local[i][None, None], c.o_anchor[i][None],
+                                                       c.o_mom[i][None], c.o_ema[i])
+            c.o_anchor[i], c.o_mom[i], c.o_local[i], c.o_ema[i] = anc[0], mom[0], loc[0, 0], ema
+            tag = f"graph round {r} unit {i}"
+            parity.assert_outcome(c.sync.stats(i), out, ema, tag)
+            parity.assert_f32_close(c.anchor[i].cpu().numpy(), anc[0], tag + " anchor")
+            parity.assert_f32_close(c.mom[i].cpu().numpy(), mom[0], tag + " momentum")
+            parity.assert_local_close(parity.to_oracle_local(c.local[i]), loc[0, 0], tag + " local")
+            assert c.sync.stats(i).round == r + 1
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
 @pytest.mark.parametrize("numel", [1, 9, 1000, 65_543, 2_000_001])
 def test_no_writes_outside_the_shards(dtype, numel):
     # guard zones around every buffer (compute-sanitizer is closed on this pool): the sync
