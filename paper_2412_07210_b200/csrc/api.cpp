@@ -182,6 +182,7 @@ struct edit_sync {
   // profiling: EDIT_NUM_PHASES + 1 timing events per unit, and the units pending collection
   bool profiling = false;
   bool graph = false;               // EDIT_GRAPH=1 (round replay from CUDA graphs)
+  cudaStream_t cap_stream = nullptr;  // the capture origin (the caller's stream may be the legacy one)
   std::vector<RoundGraph> graphs;   // small cache, most recent last
   std::vector<cudaEvent_t> prof;
   std::vector<int32_t> pending;
@@ -787,12 +788,16 @@ edit_status_t edit_sync_round(edit_sync_t h, void* const* locals, float* const* 
           for (int u = 0; u < L; ++u) h->pending.push_back(u);
         return EDIT_OK;
       }
-    CUDA_TRY(h, cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+    // capture on a library stream (the caller's may be the legacy default stream, which
+    // cannot be captured); the graph is then launched on the caller's stream
+    if (!h->cap_stream) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    CUDA_TRY(h, cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeRelaxed));
   }
+  cudaStream_t origin = use_graph ? h->cap_stream : cs;
   const int64_t launches0 = h->launches;
   edit_status_t rc = EDIT_OK;
   const int nl = (int)h->lanes.size();
-  if (cudaEventRecord(h->fork, cs) != cudaSuccess) rc = fail(EDIT_ERR_CUDA, "fork record");
+  if (cudaEventRecord(h->fork, origin) != cudaSuccess) rc = fail(EDIT_ERR_CUDA, "fork record");
   for (Lane& ln : h->lanes)
     if (rc == EDIT_OK && cudaStreamWaitEvent(ln.stream, h->fork, 0) != cudaSuccess) rc = fail(EDIT_ERR_CUDA, "fork wait");
   for (int u = 0; u < L && rc == EDIT_OK; ++u) {
@@ -801,12 +806,12 @@ edit_status_t edit_sync_round(edit_sync_t h, void* const* locals, float* const* 
   }
   for (Lane& ln : h->lanes) {
     if (rc != EDIT_OK) break;
-    if (cudaEventRecord(ln.tail, ln.stream) != cudaSuccess || cudaStreamWaitEvent(cs, ln.tail, 0) != cudaSuccess)
+    if (cudaEventRecord(ln.tail, ln.stream) != cudaSuccess || cudaStreamWaitEvent(origin, ln.tail, 0) != cudaSuccess)
       rc = fail(EDIT_ERR_CUDA, "join");
   }
   if (!use_graph) return rc;
   cudaGraph_t graph = nullptr;
-  const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
+  const cudaError_t ec = cudaStreamEndCapture(h->cap_stream, &graph);
   if (rc != EDIT_OK) {
     if (graph) cudaGraphDestroy(graph);
     return rc;
@@ -1208,6 +1213,7 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
   for (RoundGraph& g : h->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   h->graphs.clear();
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   if (h->fork) cudaEventDestroy(h->fork);
   if (h->warm_dev) cudaFree(h->warm_dev);
   for (auto e : h->done)
