@@ -1180,6 +1180,12 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
   edit_status_t st = EDIT_OK;
   cudaSetDevice(h->cfg.device);
   if (!h->poisoned) cudaDeviceSynchronize();
+  // captured rounds first: a graph holding NCCL collectives references the communicators,
+  // which must outlive it (the NCCL-exchange graph case once stalled in teardown with the
+  // graphs destroyed after the comms)
+  for (RoundGraph& g : h->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  h->graphs.clear();
   if ((h->peer || !h->reg_gather.empty() || h->dev_xchg) && h->ready && !h->poisoned && !h->lanes.empty() &&
       h->lanes[0].global) {
     // barrier: no member may free its IPC-exported buffers while a peer still reads them
@@ -1210,9 +1216,6 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
     if (ln.tail) cudaEventDestroy(ln.tail);
     if (ln.stream) cudaStreamDestroy(ln.stream);
   }
-  for (RoundGraph& g : h->graphs)
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-  h->graphs.clear();
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   if (h->fork) cudaEventDestroy(h->fork);
   if (h->warm_dev) cudaFree(h->warm_dev);
