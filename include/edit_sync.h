@@ -172,7 +172,10 @@ edit_status_t edit_sync_register_gather(edit_sync_t h, void* const* full_bufs);
  * each lane = an internal stream + its own NCCL communicators + exchange buffers), so unit u+1's norm pass and
  * scalar gathers overlap unit u's exchange and update.  Starts after the work already on
  * `stream`; `stream` waits for the whole round.  Same results, bit for bit, as the
- * sequential calls (every unit's arithmetic and reduction order is unchanged). */
+ * sequential calls (every unit's arithmetic and reduction order is unchanged).
+ * EDIT_GRAPH=1 in the environment at init (equal on every rank; opt-in): the round is
+ * captured into a CUDA graph on the first call with a given set of 3L pointers and replayed
+ * on later calls with the same set (up to 4 sets cached); same results. */
 edit_status_t edit_sync_round(edit_sync_t h, void* const* locals, float* const* anchors, float* const* momenta,
                               void* stream);
 
