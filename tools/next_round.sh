@@ -15,4 +15,3 @@ for m in 350M 1B; do
 done
 EDIT_TEST_FULL=1 timeout 2400 python -m pytest tests/test_gpu_multirank.py -x -q > gpurun_out/nr_multirank_full.log 2>&1
 tail -1 gpurun_out/nr_multirank_full.log
-python tools/ov_table.py gpurun_out/nr_*graph*.json 2>/dev/null | head -0
