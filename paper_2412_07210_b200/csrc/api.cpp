@@ -26,9 +26,28 @@ typedef int CUresult_t;  // CUresult (driver API) without including cuda.h
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3 (ranges for nsys; no-ops without a tool)
+
 #include "internal.h"
 
 using namespace edit;
+
+namespace {
+// EDIT_NVTX=1: one NVTX range per enqueued unit sync and per round (host-side enqueue spans;
+// nsys correlates the CUDA launches inside them).  Scoped: popped on every return path.
+struct NvtxRange {
+  bool on;
+  NvtxRange(bool enable, const char* fmt, int arg) : on(enable) {
+    if (!on) return;
+    char name[64];
+    snprintf(name, sizeof name, fmt, arg);
+    nvtxRangePushA(name);
+  }
+  ~NvtxRange() {
+    if (on) nvtxRangePop();
+  }
+};
+}  // namespace
 
 namespace {
 
@@ -182,6 +201,7 @@ struct edit_sync {
   // profiling: EDIT_NUM_PHASES + 1 timing events per unit, and the units pending collection
   bool profiling = false;
   bool graph = false;               // EDIT_GRAPH=1 (round replay from CUDA graphs)
+  bool nvtx = false;                // EDIT_NVTX=1 (NVTX ranges per unit / round)
   cudaStream_t cap_stream = nullptr;  // the capture origin (the caller's stream may be the legacy one)
   std::vector<RoundGraph> graphs;   // small cache, most recent last
   std::vector<cudaEvent_t> prof;
@@ -311,6 +331,7 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
   h->peer_ctas = h->num_sms;
   if (const char* e = getenv("EDIT_XCHG")) h->dev_xchg = strcmp(e, "nccl") != 0;
   if (const char* e = getenv("EDIT_GRAPH")) h->graph = atoi(e) != 0;
+  if (const char* e = getenv("EDIT_NVTX")) h->nvtx = atoi(e) != 0;
   if (const char* e = getenv("EDIT_PEER_TILE")) {
     const int v = atoi(e);
     if (v >= 32 && v <= 4096 && (v & 31) == 0) h->peer_tile = v;
@@ -493,6 +514,7 @@ static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* loc
   LayerScratch* scr = &h->scratch[layer];
   const int M = h->M, N = h->N;
   int launched = 0;
+  const NvtxRange range(h->nvtx, "edit_sync unit %d", layer);
 
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   cudaEvent_t* ev = h->profiling ? &h->prof[(size_t)layer * (EDIT_NUM_PHASES + 1)] : nullptr;
@@ -769,6 +791,7 @@ edit_status_t edit_sync_round(edit_sync_t h, void* const* locals, float* const* 
     if (rc != EDIT_OK) return rc;
   }
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  const NvtxRange range(h->nvtx, "edit_sync_round (%d units)", L);
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   const bool use_graph = h->graph && (h->K == 1 || h->lanes[0].dseq != nullptr);
   std::vector<uintptr_t> key;
