@@ -25,8 +25,10 @@ def _rand_mesh(M, N, numel, seed, bf16=False, scale=2e-3):
 
 
 def _as_f64(locals_):
+    # widen with torch (independent of the oracle's own oracle_bf16_to_f64, which is pinned
+    # separately against torch over all 65,536 bit patterns in test_oracle_pins.py)
     if locals_.dtype == np.uint16:
-        return oracle.bf16_bits_to_f64(locals_).reshape(locals_.shape)
+        return torch.from_numpy(locals_.view(np.int16).copy()).view(torch.bfloat16).to(torch.float64).numpy()
     return locals_.astype(np.float64)
 
 

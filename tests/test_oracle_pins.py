@@ -179,6 +179,35 @@ def test_bf16_rounding_vs_torch():
     assert np.isnan(oracle.bf16_bits_to_f64(oracle.f32_to_bf16_bits(np.array([np.nan], np.float32))))[0]
 
 
+def test_bf16_widening_vs_torch_all_patterns():
+    # oracle_bf16_to_f64 (the oracle's only way to read a bf16 local) against torch's
+    # bf16 -> fp64 conversion over every one of the 65,536 bit patterns (NaNs: both NaN)
+    bits = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    ours = oracle.bf16_bits_to_f64(bits)
+    ref = torch.from_numpy(bits.view(np.int16).copy()).view(torch.bfloat16).to(torch.float64).numpy()
+    nan = np.isnan(ref)
+    assert (np.isnan(ours) == nan).all()
+    np.testing.assert_array_equal(ours[~nan], ref[~nan])
+    # signed zeros and infinities keep their sign
+    np.testing.assert_array_equal(np.signbit(ours[~nan]), np.signbit(ref[~nan]))
+
+
+def test_bf16_sync_unit_reads_locals_like_torch():
+    # a whole Sync() with bf16 locals against one computed from torch-widened locals in plain
+    # numpy: NO_AE|NO_WA|NO_GC, nu = 1, mu = 0 -> anchor' = mean_n local_n (R1), so every bit
+    # of the widening shows up in the result
+    rng = np.random.default_rng(41)
+    M, N, numel = 2, 3, 4099
+    anchors = rng.normal(0, 0.02, (M, numel)).astype(np.float32)
+    loc32 = (anchors[:, None, :] - rng.normal(0, 2e-3, (M, N, numel))).astype(np.float32)
+    loc = torch.from_numpy(loc32).to(torch.bfloat16)
+    bits = loc.view(torch.int16).numpy().view(np.uint16)
+    cfg = oracle.Config(outer_lr=1.0, outer_momentum=0.0, flags=oracle.NO_AE | oracle.NO_WA | oracle.NO_GC)
+    _, anc, _, _, _ = oracle.sync_unit(cfg, bits, anchors, np.zeros_like(anchors), [oracle.Ema()] * N)
+    ref = loc.to(torch.float64).numpy().mean(axis=1)
+    np.testing.assert_allclose(anc, ref.astype(np.float32), rtol=0, atol=2e-9)
+
+
 # ----------------------------------------------------- App. C worked example
 def test_appc_worked_example_primitives(golden):
     c = golden("appc_worked_example.json")
@@ -230,6 +259,7 @@ def test_allreduce_mean_vs_numpy_and_identical_inputs():
     same = np.repeat(g[:1], 4, axis=0)                     # identical inputs -> that input
     np.testing.assert_array_equal(oracle.allreduce_mean(same), g[0])
     gb = oracle.f32_to_bf16_bits(g).reshape(g.shape)
-    ref = torch.from_numpy(oracle.bf16_bits_to_f64(gb).reshape(g.shape).mean(0).astype(np.float32)).to(
+    gw = torch.from_numpy(gb.view(np.int16).copy()).view(torch.bfloat16).to(torch.float64).numpy()  # torch widening
+    ref = torch.from_numpy(gw.mean(0).astype(np.float32)).to(
         torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
     np.testing.assert_array_equal(oracle.allreduce_mean(gb), ref)
