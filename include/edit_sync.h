@@ -25,6 +25,17 @@
  * host except edit_sync_stats / get_state / set_state / destroy and init.
  * There is no CPU fallback: without a CUDA device every call that needs one
  * returns EDIT_ERR_CUDA.
+ *
+ * Cross-rank exchange (N > 1 or M > 1, default): the K-scalar gathers of the module norms and
+ * of the ||Dbar|| partials run over NVLink mailboxes inside the LAST CTA of the producing
+ * kernel (K1, the reduce-scatter), so a unit is 3 dependent kernels on the peer path and 2 at
+ * N == 1.  A rank that waits longer than EDIT_XCHG_TIMEOUT_S seconds (default 600; 0 = wait
+ * forever, as NCCL does) for a peer marks its handle failed: from then on every exchange of
+ * the handle returns at once without publishing, no kernel of an affected unit writes any
+ * buffer (no update from stale peer data), the peers in turn time out the same way, and
+ * every later call on the handle returns EDIT_ERR_STATE (polled from mapped host memory, no
+ * device sync).  The state is then that of the last unit that completed everywhere: restore
+ * from a checkpoint.
  */
 #ifndef EDIT_SYNC_H_
 #define EDIT_SYNC_H_
@@ -128,7 +139,16 @@ edit_status_t edit_sync_workspace_bytes(const edit_sync_config_t* cfg, size_t* b
  * [0, 1); phi <= 0; eps <= 0; alpha outside (0, 1]; delta <= 0; W < 0),
  * creates the NCCL comms (global, sync = row, shard = column) and zeroes the
  * EMA state (mu = sigma = 0, count = 0; R8).  The workspace stays owned by the
- * caller and must outlive the handle. */
+ * caller and must outlive the handle.
+ * Every rank must agree on the settings that fix slice layout, lane mapping and the exchange
+ * protocol (EDIT_LANES, EDIT_PEER_TILE, EDIT_XCHG, EDIT_GRAPH, algo, the units, dtype,
+ * flags): init all-gathers a digest of them and fails with EDIT_ERR_INVALID_ARG on a mismatch.
+ * EMA warm-up (R8, PAPER P:98 gives no initialisation): with mu = sigma = 0 and the paper's
+ * alpha = 0.02, mu reaches only ~18 % of a constant G after W = 10 rounds, so z stays near 2
+ * at the end of the warm-up and a ~1.35x rise of G then flags every replica (a rollback
+ * whose skipped Eq. 1 update freezes the EMA).  Callers should either seed the EMA with
+ * edit_sync_set_state (e.g. mu = G of the first sync, sigma = 0.1 mu, count = W) or use a
+ * warm-up of about 3 / alpha rounds. */
 edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDIT_UNIQUE_ID_BYTES],
                              void* workspace, size_t workspace_bytes, edit_sync_t* out);
 
@@ -141,7 +161,15 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
  * and the zero-padded shard tail must be zero.  Every rank must call this for
  * every unit in the same order (collective).  Enqueues only: no host sync, no
  * data-dependent host branch (the rollback branch is taken on the device).
- * EDIT_ERR_INVALID_ARG: null handle/pointer, layer outside [0, L), misalignment. */
+ * Stream order: any stream may be passed, a different one per call.  The call runs on
+ * `stream` after (i) the work already enqueued there, (ii) the previous sync of the same unit
+ * and (iii) the previous user of the exchange buffers of lane 0 (which every per-unit call
+ * shares), whatever streams those ran on (internal events) -- so calls on different streams
+ * or host threads cannot race on the library's buffers.  The ORDER of the calls (the host
+ * order in which they were made) must still be the same on every rank: it fixes the pairing
+ * of the exchanges across ranks; calls from several host threads must be serialised.
+ * EDIT_ERR_INVALID_ARG: null handle/pointer, layer outside [0, L), misalignment.
+ * EDIT_ERR_STATE: the handle is poisoned (CUDA/NCCL error, or an exchange timed out). */
 edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* anchor, float* momentum,
                               void* stream);
 
@@ -260,7 +288,11 @@ edit_status_t edit_sync_profile_collect(edit_sync_t h, double phase_ms[EDIT_NUM_
 /* Number of kernels the library launched so far on this handle (bench evidence). */
 int64_t edit_sync_kernel_launches(edit_sync_t h);
 
-/* Frees library-owned resources (NCCL comms, ops, events); never the workspace. */
+/* Frees library-owned resources (NCCL comms, ops, events); never the workspace.  With N > 1
+ * it first waits (device mailbox barrier, at most 30 s) until every rank has stopped reading
+ * this rank's exported buffers; if that barrier fails or the handle is poisoned, the
+ * IPC-exported buffers are leaked rather than freed (a peer may still be reading them) and
+ * the communicators are aborted.  Call it explicitly (close()) rather than from a finaliser. */
 edit_status_t edit_sync_destroy(edit_sync_t h);
 
 /* ---------------------------------------------------------------------------------------

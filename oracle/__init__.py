@@ -30,7 +30,11 @@ NO_AE, NO_WA, NO_GC = 1, 2, 4
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle with gcc (plain C99 + OpenMP)."""
+    """Compile the oracle with gcc (plain C99 + OpenMP).  EDIT_ORACLE_LIB=<path> loads a
+    prebuilt copy instead (tests/test_oracle_mutations.py: deliberately broken oracles)."""
+    override = os.environ.get("EDIT_ORACLE_LIB")
+    if override:
+        return override
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", "-fPIC", "-shared",

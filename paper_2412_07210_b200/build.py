@@ -34,20 +34,39 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every source to an object in parallel (one nvcc per file), then link."""
     if not force and not _stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
     inc, lib = nccl_paths()
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v" if verbose else "-O3",
+             "-I", INCLUDE, "-I", CSRC, "-I", inc]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + f".{os.getpid()}.o")
+        r = subprocess.run([NVCC, *flags, "-c", src, "-o", obj], capture_output=True, text=True)
+        return src, obj, r
+
+    with ThreadPoolExecutor(max_workers=len(sources())) as ex:
+        results = list(ex.map(compile_one, sources()))
+    for src, _, r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed on {os.path.basename(src)}")
+        if verbose:
+            sys.stderr.write(r.stderr)
     tmp = f"{LIB}.tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
-           "-Xptxas", "-v" if verbose else "-O3",
-           "-I", INCLUDE, "-I", CSRC, "-I", inc, *sources(),
-           "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}", "-o", tmp]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    objs = [o for _, o, _ in results]
+    r = subprocess.run([NVCC, *ARCH, "-shared", *objs, "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}",
+                        "-o", tmp], capture_output=True, text=True)
+    for o in objs:
+        os.remove(o)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc build of libedit_sync.so failed")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc link of libedit_sync.so failed")
     os.replace(tmp, LIB)
     return LIB
 

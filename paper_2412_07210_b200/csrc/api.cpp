@@ -2,16 +2,16 @@
 // M x N mesh (Alg. 1 l.400), workspace carving and the per-unit
 // enqueue sequence of Sync() (Alg. 2).
 //
-// Per unit, N > 1:
-//   K1 pg_norm(local, anchor -> S, ||Delta_shard||^2)
-//   ncclAllGather(1 fp64, global comm)          module norms + norm sync gamma
-//   K2 decide(-> w, rollback, EMA, record)
-//   ncclAllReduce(S, PreMulSum(w on device), sync comm)   Eq. 3 (l.452)
-//   K3 sumsq(S -> ||Dbar_shard||^2)
-//   ncclAllGather(1 fp64, shard comm)   (M > 1)           module-level G_bar
-//   K4 outer_update(S, anchor, momentum -> anchor, momentum, local)
-// N == 1: K1 (no S) -> [AllGather on the shard comm if M > 1] -> K2 -> K4 (recomputes
-// Delta from local and anchor): two HBM passes.
+// Per unit, N > 1, peer path with the device scalar exchange (the default):
+//   K1 pg_norm(local, anchor -> ||Delta_shard||^2) + [last CTA: K-scalar exchange of the
+//      partials over NVLink mailboxes + K2 decide (z-test, EMA, Eq. 2 weights,
+//      rollback)]
+//   RS  Dbar slice = sum_j w_j (anchor - local_j) pulled from the sync row (Eq. 3, l.452)
+//      + [last CTA: K-scalar exchange of the ||Dbar slice||^2 partials (Eq. 4)]
+//   AG  every Dbar slice pulled from its owner + beta + Nesterov + write-back (l.454-455)
+// = 3 dependent launches per unit.  N == 1: K1 (+K2 in its last CTA) then K4, which
+// recomputes Delta from local and anchor: two HBM passes.  EDIT_XCHG=nccl / EDIT_ALGO_NCCL
+// keep the NCCL baselines (ncclAllGather of the scalars; ncclAllReduce with PreMulSum).
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -28,7 +28,7 @@ typedef int CUresult_t;  // CUresult (driver API) without including cuda.h
 
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3 (ranges for nsys; no-ops without a tool)
 
-#include "internal.h"
+#include "handle.h"
 
 using namespace edit;
 
@@ -47,16 +47,8 @@ struct NvtxRange {
     if (on) nvtxRangePop();
   }
 };
-}  // namespace
-
-namespace {
 
 thread_local std::string g_last_error;
-
-edit_status_t fail(edit_status_t st, const std::string& msg) {
-  g_last_error = msg;
-  return st;
-}
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -67,9 +59,6 @@ struct Layout {
 
 Layout layout_of(const edit_sync_config_t& c) {
   Layout L{};
-  int64_t max_numel = 0;
-  for (int i = 0; i < c.num_layers; ++i) max_numel = std::max<int64_t>(max_numel, c.layer_numel[i]);
-  (void)max_numel;
   size_t off = 0;
   const bool nccl = c.sync_dim > 1 && c.algo == EDIT_ALGO_NCCL;
   L.scratch_off = off;
@@ -126,120 +115,6 @@ edit_status_t validate(const edit_sync_config_t* c) {
   return EDIT_OK;
 }
 
-}  // namespace
-
-// A lane = one in-order pipeline of unit syncs: its stream (internal; the caller's stream for
-// edit_layer_sync), its own NCCL communicators (so two lanes' collectives never interleave on
-// one comm) and its own exchange buffers.  edit_sync_round / the prefetch scheduler deal
-// units round-robin over the lanes, so unit u+1's norm pass and scalar gathers run while unit
-// u's exchange and update run.  Every rank maps unit u to lane u % nlanes: the collective
-// order per communicator is identical on all ranks.
-struct Lane {
-  cudaStream_t stream = nullptr;
-  cudaEvent_t tail = nullptr;  // join event
-  ncclComm_t global = nullptr, sync = nullptr, shard = nullptr;
-  std::vector<ncclRedOp_t> ops;  // NCCL algo: per unit PreMulSum with that unit's device weight
-  float* S = nullptr;            // NCCL algo: fp32 Delta exchange buffer
-  // peer algo: own staging copy of the local (L) and own Dbar slice (D), cudaMalloc'd and
-  // exported by CUDA IPC to the sync row; pp holds every member's mapped pointers
-  void* Lown = nullptr;
-  float* Down = nullptr;
-  PeerPtrs pp{};
-  std::vector<void*> opened;  // IPC mappings to close
-  // device-side scalar exchange (EDIT_XCHG=nccl disables): own mailbox, all ranks' mapped
-  unsigned long long* mailbox = nullptr;
-  MailPtrs mp{};
-  unsigned long long seq[kXchgPhases] = {0, 0};
-  unsigned long long* dseq = nullptr;  // graph mode: device-side sequence counters [kXchgPhases]
-  int* xerr = nullptr;
-};
-
-// EDIT_GRAPH=1: edit_sync_round captures the round once per set of buffer pointers into a
-// CUDA graph and replays it (measured boundary cost of dependent kernels: plain 3.7-4.1 us,
-// graph 0.6-1.4 us, profiles/r1_pdl_graph_launch_gaps.txt).  Requires the mailbox sequence
-// numbers on the device (Lane::dseq); must be equal on every rank.
-struct RoundGraph {
-  std::vector<uintptr_t> key;  // the 3L buffer pointers
-  cudaGraphExec_t exec = nullptr;
-  int64_t launches = 0;        // kernels per replay
-};
-
-struct edit_sync {
-  edit_sync_config_t cfg{};
-  std::vector<int64_t> numel;
-  int M = 1, N = 1, K = 1, sync_idx = 0, shard_idx = 0;
-  int num_sms = 0;
-  std::vector<double*> part1, part2;  // per-unit per-CTA partial slots (workspace)
-  std::vector<Lane> lanes;
-  bool peer = false;             // N > 1 and algo == EDIT_ALGO_PEER
-  int peer_ctas = 148;           // persistent grid of the peer kernels (EDIT_PEER_CTAS env overrides)
-  int peer_tile = kPeerTileVec;  // vectors per TMA tile (EDIT_PEER_TILE env; must match on all ranks)
-  bool dev_xchg = true;          // scalar chain over NVLink mailboxes (EDIT_XCHG=nccl: NCCL gathers)
-  bool ef_direct = false;        // L2 evict_first streaming for edit_layer_sync / edit_sync_round
-  bool ef_sched = false;         // ... for the prefetch scheduler (a forward runs concurrently)
-  // scheduler (co-resident) mode: at most sched_ctas CTAs per streaming kernel, each small
-  // enough (registers, shared memory) to sit next to a GEMM CTA on an SM (EDIT_SCHED_CTAS)
-  // (default 0 = full grids: measured, capping does not buy overlap on B200 -- DESIGN.md 7)
-  int sched_ctas = 0;
-  int sched_smem_kb = 18;
-  // partition mode (edit_sched_set_partition): scheduled units u >= sched_full_units run
-  // as persistent TMA pipelines on sched_part CTAs (one per SM), lanes at high priority
-  int sched_part = 0;
-  int sched_full_units = 2;
-  int lane_prio = 0;             // priority the lanes were created with (env default)
-  // gate (EDIT_SCHED_GATE=1): the sync of unit u+depth starts only when the forward of unit
-  // u may start (an event on the compute stream at acquire(u)), not as soon as its lane frees
-  bool sched_gate = false;
-  std::vector<cudaEvent_t> gate_ev;
-  bool ready = false;            // init completed (destroy may then barrier with the peers)
-  char* ws = nullptr;
-  LayerScratch* scratch = nullptr;
-  edit_ema_t* ema = nullptr;
-  edit_layer_stats_t* rec = nullptr;
-  std::vector<cudaEvent_t> done;  // per unit: recorded after its last kernel
-  cudaEvent_t fork = nullptr;     // round API / scheduler: "the caller's inputs are ready"
-  // profiling: EDIT_NUM_PHASES + 1 timing events per unit, and the units pending collection
-  bool profiling = false;
-  bool graph = false;               // EDIT_GRAPH=1 (round replay from CUDA graphs)
-  bool nvtx = false;                // EDIT_NVTX=1 (NVTX ranges per unit / round)
-  cudaStream_t cap_stream = nullptr;  // the capture origin (the caller's stream may be the legacy one)
-  std::vector<RoundGraph> graphs;   // small cache, most recent last
-  std::vector<cudaEvent_t> prof;
-  std::vector<int32_t> pending;
-  // host-buffer variant: two device staging slots + copy-in / copy-out streams
-  char* staging = nullptr;
-  size_t slot_bytes = 0;
-  int next_slot = 0;
-  cudaStream_t h2d = nullptr, d2h = nullptr;
-  // kHostSlots staging slots: copy-in of unit u+2 need not wait for copy-out of unit u
-  static constexpr int kHostSlots = 3;
-  cudaEvent_t slot_in[kHostSlots] = {}, slot_done[kHostSlots] = {}, slot_free[kHostSlots] = {};
-  double* warm_dev = nullptr;  // warm-up all-reduce: barrier scalars (N + 1)
-  // NEXT-2 registered gather buffers: [L][M] (member q's full-module buffer, mapped)
-  std::vector<std::vector<void*>> reg_gather;
-  std::vector<void*> gather_opened;
-  double* gather_dev = nullptr;  // gather barrier scalars per unit [L][M + 1]
-  // registered caller locals (peer path): my pointers and every member's mapped pointer
-  std::vector<void*> reg_local;                     // [L]
-  std::vector<std::vector<const void*>> reg_peer;   // [L][N]
-  std::vector<void*> reg_opened;                    // distinct IPC mappings to close
-  // prefetch scheduler state
-  std::vector<void*> sched_local;
-  std::vector<float*> sched_anchor, sched_mom;
-  int sched_depth = 0, sched_next_sync = 0, sched_next_acquire = 0;
-  bool sched_active = false;
-  bool poisoned = false;
-  int64_t launches = 0;
-};
-
-extern "C" {
-static edit_status_t exchange_ipc(edit_sync_t h, void* const* ptrs, const size_t* bytes, int L, ncclComm_t comm,
-                                  int P, int me, cudaStream_t st, std::vector<std::vector<void*>>& out,
-                                  std::vector<void*>& opened);
-}
-
-namespace {
-
 #define CUDA_TRY(h, expr)                                                                   \
   do {                                                                                      \
     cudaError_t e_ = (expr);                                                                \
@@ -258,45 +133,87 @@ namespace {
     }                                                                                       \
   } while (0)
 
+#define TRY(expr)                              \
+  do {                                         \
+    edit_status_t s_ = (expr);                 \
+    if (s_ != EDIT_OK) return s_;              \
+  } while (0)
+
+// cudaEventRecord that stays a real (external) event record when `st` is being captured into
+// a CUDA graph (EDIT_GRAPH=1): the round's done / profiling events are read by the host later.
+cudaError_t record_event(cudaEvent_t ev, cudaStream_t st) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  const cudaError_t e = cudaStreamIsCapturing(st, &cap);
+  if (e != cudaSuccess) return e;
+  return cap == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal)
+                                              : cudaEventRecord(ev, st);
+}
+
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusActive;
+}
+
+// The mailbox exchange arguments of lane `ln` for `phase`; takes the lane's next host-side
+// sequence number (graph mode: the device counter is used instead).
+XchgArgs xchg_args(edit_sync_t h, Lane& ln, int phase) {
+  XchgArgs x{};
+  x.mp = ln.mp;
+  x.K = h->K;
+  x.me = h->cfg.rank;
+  x.phase = phase;
+  x.seq = ++ln.seq[phase];
+  x.dseq = ln.dseq;
+  x.err = h->err_dev;
+  x.err_host = h->err_host_dev;
+  x.timeout_ns = h->timeout_ns;
+  return x;
+}
+
+edit_status_t check_unit_args(edit_sync_t h, int32_t layer, const void* local, const void* anchor,
+                              const void* momentum) {
+  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
+  TRY(check_err(h));
+  if (layer < 0 || layer >= h->cfg.num_layers) return fail(EDIT_ERR_INVALID_ARG, "layer out of range");
+  if (h->numel[layer] > 0 && (!local || !anchor || !momentum)) return fail(EDIT_ERR_INVALID_ARG, "null buffer");
+  if ((((uintptr_t)local) | ((uintptr_t)anchor) | ((uintptr_t)momentum)) & 15u)
+    return fail(EDIT_ERR_INVALID_ARG, "buffers must be 16-byte aligned");
+  return EDIT_OK;
+}
+
+void clear_graphs(edit_sync_t h) {
+  for (RoundGraph& g : h->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  h->graphs.clear();
+}
 
 }  // namespace
 
-extern "C" {
+namespace edit {
 
-const char* edit_sync_last_error(void) { return g_last_error.c_str(); }
+edit_status_t fail(edit_status_t st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
 
-const char* edit_sync_version(void) { return "edit_sync 0.1 (sm_100a)"; }
-
-edit_status_t edit_sync_get_unique_id(uint8_t id[EDIT_UNIQUE_ID_BYTES]) {
-  static_assert(sizeof(ncclUniqueId) == EDIT_UNIQUE_ID_BYTES, "ncclUniqueId size");
-  if (!id) return fail(EDIT_ERR_INVALID_ARG, "null id");
-  ncclUniqueId u;
-  ncclResult_t r = ncclGetUniqueId(&u);
-  if (r != ncclSuccess) return fail(EDIT_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
-  memcpy(id, &u, sizeof u);
+edit_status_t check_err(edit_sync_t h) {
+  if (!h->poisoned && h->err_host && *reinterpret_cast<volatile int*>(h->err_host) != 0) h->poisoned = true;
+  if (h->poisoned)
+    return fail(EDIT_ERR_STATE, h->err_host && *reinterpret_cast<volatile int*>(h->err_host)
+                                    ? "device scalar exchange timed out (a peer rank stopped syncing); handle poisoned"
+                                    : "handle poisoned by an earlier CUDA/NCCL error");
   return EDIT_OK;
 }
 
-edit_status_t edit_sync_workspace_bytes(const edit_sync_config_t* cfg, size_t* bytes) {
-  edit_status_t st = validate(cfg);
-  if (st != EDIT_OK) return st;
-  if (!bytes) return fail(EDIT_ERR_INVALID_ARG, "null bytes");
-  *bytes = layout_of(*cfg).total;
-  return EDIT_OK;
-}
-
-edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDIT_UNIQUE_ID_BYTES],
-                             void* workspace, size_t workspace_bytes, edit_sync_t* out) {
-  edit_status_t st = validate(cfg);
-  if (st != EDIT_OK) return st;
+edit_status_t create_local(const edit_sync_config_t* cfg, void* workspace, size_t workspace_bytes,
+                           edit_sync_t* out) {
+  TRY(validate(cfg));
   if (!out) return fail(EDIT_ERR_INVALID_ARG, "null out");
   *out = nullptr;
   const Layout L = layout_of(*cfg);
   if (!workspace) return fail(EDIT_ERR_INVALID_ARG, "null workspace");
   if (((uintptr_t)workspace & 255u) != 0) return fail(EDIT_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
   if (workspace_bytes < L.total) return fail(EDIT_ERR_NO_MEMORY, "workspace too small");
-  const int K = cfg->shard_dim * cfg->sync_dim;
-  if (K > 1 && !id) return fail(EDIT_ERR_INVALID_ARG, "null unique id for a multi-rank mesh");
 
   edit_sync* h = new (std::nothrow) edit_sync();
   if (!h) return fail(EDIT_ERR_NO_MEMORY, "host allocation");
@@ -305,29 +222,19 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
   h->cfg.layer_numel = h->numel.data();
   h->M = cfg->shard_dim;
   h->N = cfg->sync_dim;
-  h->K = K;
+  h->K = h->M * h->N;
   h->sync_idx = cfg->rank / h->M;   // row index n (R20)
   h->shard_idx = cfg->rank % h->M;  // column index m
+  *out = h;  // (on failure the caller destroys it)
 
-  auto bail = [&](edit_status_t s) {
-    edit_sync_destroy(h);
-    return s;
-  };
-#define INIT_CUDA(expr)                                                                     \
+#define LCUDA(expr)                                                                         \
   do {                                                                                      \
     cudaError_t e_ = (expr);                                                                \
-    if (e_ != cudaSuccess)                                                                  \
-      return bail(fail(EDIT_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)));   \
-  } while (0)
-#define INIT_NCCL(expr)                                                                     \
-  do {                                                                                      \
-    ncclResult_t r_ = (expr);                                                               \
-    if (r_ != ncclSuccess)                                                                  \
-      return bail(fail(EDIT_ERR_NCCL, std::string(#expr ": ") + ncclGetErrorString(r_)));   \
+    if (e_ != cudaSuccess) return fail(EDIT_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
   } while (0)
 
-  INIT_CUDA(cudaSetDevice(cfg->device));
-  INIT_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
+  LCUDA(cudaSetDevice(cfg->device));
+  LCUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
   h->peer_ctas = h->num_sms;
   if (const char* e = getenv("EDIT_XCHG")) h->dev_xchg = strcmp(e, "nccl") != 0;
   if (const char* e = getenv("EDIT_GRAPH")) h->graph = atoi(e) != 0;
@@ -336,12 +243,11 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
     const int v = atoi(e);
     if (v >= 32 && v <= 4096 && (v & 31) == 0) h->peer_tile = v;
   }
-  // L2 policy of the streaming passes: EDIT_L2_EVICT_FIRST = 0 | 1 | sched (default 0;
-  // measured neutral standalone and no overlap gain, profiles/r1_overlap_experiments.md)
-  if (const char* e = getenv("EDIT_L2_EVICT_FIRST")) {
-    if (!strcmp(e, "1")) h->ef_direct = h->ef_sched = true;
-    else if (!strcmp(e, "sched")) h->ef_sched = true;
-  }
+  // mailbox wait bound: a peer that stops syncing for longer poisons the handle on every rank
+  // (default 600 s, like torch's NCCL watchdog; 0 = wait forever as NCCL itself does)
+  double tmo = 600.0;
+  if (const char* e = getenv("EDIT_XCHG_TIMEOUT_S")) tmo = atof(e);
+  h->timeout_ns = tmo > 0 ? (unsigned long long)(tmo * 1e9) : 0ull;
   if (const char* e = getenv("EDIT_SCHED_CTAS")) {  // 0 = full grids also in scheduler rounds
     const int v = atoi(e);
     if (v >= 0) h->sched_ctas = std::min(v, kMaxPeerCtas);
@@ -364,15 +270,20 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
     h->part2.push_back(reinterpret_cast<double*>(h->ws + L.parts_off + L.part2[i]));
   }
   // zero scratch (ticket counters), EMA (mu = sigma = 0, count = 0: R8) and records
-  INIT_CUDA(cudaMemset(h->ws + L.scratch_off, 0, L.total - L.scratch_off));
-  INIT_CUDA(cudaDeviceSynchronize());
+  LCUDA(cudaMemset(h->ws + L.scratch_off, 0, L.total - L.scratch_off));
+  // sticky exchange error flag: device word + mapped host mirror
+  LCUDA(cudaMalloc(reinterpret_cast<void**>(&h->err_dev), sizeof(int)));
+  LCUDA(cudaMemset(h->err_dev, 0, sizeof(int)));
+  LCUDA(cudaHostAlloc(reinterpret_cast<void**>(&h->err_host), sizeof(int), cudaHostAllocMapped));
+  *h->err_host = 0;
+  LCUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->err_host_dev), h->err_host, 0));
 
   h->done.assign(cfg->num_layers, nullptr);
-  for (auto& e : h->done) INIT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : h->done) LCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   h->gate_ev.assign(cfg->num_layers, nullptr);
-  for (auto& e : h->gate_ev) INIT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : h->gate_ev) LCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if (const char* e = getenv("EDIT_SCHED_GATE")) h->sched_gate = atoi(e) != 0;
-  INIT_CUDA(cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming));
+  LCUDA(cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming));
 
   // EDIT_LANES (1..8) -- must be equal on every rank.  Lanes hide the latency of the scalar
   // chain of the exchange: N > 1 -> 4 (measured 350M 1x2 3.27 -> 2.78 ms, 1B 7.90 -> 7.21 ms,
@@ -384,7 +295,7 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
     if (v >= 1 && v <= 8) nlanes = v;
   }
   int prio_lo = 0, prio_hi = 0;
-  INIT_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  LCUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   // lane-stream priority (EDIT_SCHED_PRIORITY=high|normal|low, default low): with the
   // LOWEST priority a concurrent forward's GEMM CTAs are placed first and the sync's CTAs
   // fill what they leave free on each SM, instead of displacing them
@@ -401,29 +312,428 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
   const size_t esz = cfg->param_dtype == EDIT_BF16 ? 2 : 4;
   for (int li = 0; li < nlanes; ++li) {
     Lane& ln = h->lanes[li];
-    INIT_CUDA(cudaStreamCreateWithPriority(&ln.stream, cudaStreamNonBlocking, prio));
-    INIT_CUDA(cudaEventCreateWithFlags(&ln.tail, cudaEventDisableTiming));
-    if (K == 1) continue;
+    LCUDA(cudaStreamCreateWithPriority(&ln.stream, cudaStreamNonBlocking, prio));
+    LCUDA(cudaEventCreateWithFlags(&ln.tail, cudaEventDisableTiming));
+    LCUDA(cudaEventCreateWithFlags(&ln.last, cudaEventDisableTiming));
+    if (h->K == 1) continue;
+    LCUDA(cudaMalloc(reinterpret_cast<void**>(&ln.bar), sizeof(double) * (1 + kMaxRanks)));
+    LCUDA(cudaMemset(ln.bar, 0, sizeof(double) * (1 + kMaxRanks)));
+    if (h->dev_xchg) {
+      LCUDA(cudaMalloc(reinterpret_cast<void**>(&ln.mailbox), align_up(mailbox_bytes(h->K), 256)));
+      LCUDA(cudaMemset(ln.mailbox, 0, align_up(mailbox_bytes(h->K), 256)));
+      if (h->graph) {
+        LCUDA(cudaMalloc(reinterpret_cast<void**>(&ln.dseq), sizeof(unsigned long long) * kXchgPhases));
+        LCUDA(cudaMemset(ln.dseq, 0, sizeof(unsigned long long) * kXchgPhases));
+      }
+    }
+    if (h->peer) {
+      const Slicing sl = slicing_of(max_numel, h->N, 0, h->peer_tile);
+      LCUDA(cudaMalloc(&ln.Lown, align_up((size_t)std::max<int64_t>(max_numel, 8) * esz, 256)));
+      LCUDA(cudaMalloc(reinterpret_cast<void**>(&ln.Down), align_up((size_t)sl.slice * 8 * sizeof(float), 256)));
+      ln.pp.L[h->sync_idx] = ln.Lown;
+      ln.pp.D[h->sync_idx] = ln.Down;
+    } else if (h->N > 1) {
+      LCUDA(cudaMalloc(reinterpret_cast<void**>(&ln.S), align_up((size_t)std::max<int64_t>(max_numel, 8) * 4, 256)));
+    }
+  }
+  LCUDA(cudaDeviceSynchronize());
+#undef LCUDA
+  return EDIT_OK;
+}
+
+// ------------------------------------------------------------------------------ one unit
+edit_status_t plan_unit(edit_sync_t h, Lane& ln, int32_t layer, void* local, float* anchor, float* momentum,
+                        cudaStream_t st, const Mode& mode, UnitPlan& p) {
+  p = UnitPlan{};
+  p.ln = &ln;
+  p.layer = layer;
+  p.local = local;
+  p.anchor = anchor;
+  p.momentum = momentum;
+  p.st = st;
+  p.mode = mode;
+  const int N = h->N;
+  LayerScratch* scr = &h->scratch[layer];
+  p.S = (N > 1 && !h->peer) ? ln.S : nullptr;
+  // peer path: read the members' registered locals directly, else stage a copy of ours
+  p.direct = h->peer && !h->reg_local.empty() && h->reg_local[layer] == local;
+  p.pp = ln.pp;
+  if (p.direct)
+    for (int j = 0; j < N; ++j) p.pp.L[j] = h->reg_peer[layer][j];
+  p.ev = h->profiling ? &h->prof[(size_t)layer * (EDIT_NUM_PHASES + 1)] : nullptr;
+  // K2's arguments: module norms of every replica on every rank from one K-scalar gather
+  // (R6)
+  DecideArgs& d = p.d;
+  d.parts = h->K > 1 ? scr->recv1 : &scr->send1;
+  d.M = h->M;
+  d.N = N;
+  d.my_n = h->sync_idx;
+  d.ema = h->ema + (size_t)layer * N;
+  d.rec = h->rec + layer;
+  d.w_out = &scr->w;
+  d.w_all_out = scr->w_all;
+  d.rollback_out = &scr->rollback;
+  d.gsq_out = &scr->gsq;
+  d.alpha = h->cfg.ema_alpha;
+  d.delta = h->cfg.anomaly_threshold;
+  d.warmup = h->cfg.ema_warmup_rounds;
+  d.flags = h->cfg.flags;
+  UpdateArgs& u = p.u;
+  u.local = local;
+  u.anchor = anchor;
+  u.momentum = momentum;
+  u.n = h->numel[layer];
+  u.rollback = &scr->rollback;
+  u.nu = h->cfg.outer_lr;
+  u.mu = h->cfg.outer_momentum;
+  u.phi = h->cfg.clip_threshold;
+  u.eps = h->cfg.clip_eps;
+  u.flags = h->cfg.flags;
+  u.rec = h->rec + layer;
+  p.gathered = !h->reg_gather.empty() && h->numel[layer] > 0;
+  if (p.gathered) {
+    u.gather_M = h->M;
+    u.gather_off = (int64_t)h->shard_idx * h->numel[layer];
+    for (int q = 0; q < h->M; ++q) u.gather[q] = h->reg_gather[layer][q];
+  }
+  if (h->peer) {
+    p.sl = slicing_of(h->numel[layer], N, h->sync_idx, h->peer_tile);
+    u.gparts = scr->recv2;  // every slice of every shard, rank order
+    u.n_gparts = h->K;
+  } else if (N > 1) {
+    u.dbar = p.S;
+    u.gparts = h->M > 1 ? scr->recv2 : &scr->send2;
+    u.n_gparts = h->M > 1 ? h->M : 1;
+  } else {
+    u.dbar = nullptr;  // Dbar = Delta, G_bar = G (module level)
+    u.gparts = &scr->gsq;
+    u.n_gparts = 1;
+  }
+  return EDIT_OK;
+}
+
+edit_status_t enqueue_step(edit_sync_t h, UnitPlan& p, int step) {
+  Lane& ln = *p.ln;
+  const int32_t layer = p.layer;
+  const int64_t n = h->numel[layer];
+  const int dt = h->cfg.param_dtype;
+  LayerScratch* scr = &h->scratch[layer];
+  const int N = h->N, M = h->M;
+  cudaStream_t st = p.st;
+  cudaEvent_t* ev = p.ev;
+  // fold: the scalar exchanges run in the last CTA of the producing kernel (mailboxes), and
+  // K2 in K1's last CTA; off only for the NCCL scalar-gather baseline (EDIT_XCHG=nccl)
+  const bool fold = h->K == 1 || h->dev_xchg;
+  int launched = 0;
+  switch (step) {
+    case kStepBegin:
+      if (!capturing(st)) {
+        // this lane's buffers and this unit's scratch may have been used last on another
+        // stream (edit_layer_sync on any caller stream, rounds, the scheduler): order after it
+        CUDA_TRY(h, cudaStreamWaitEvent(st, ln.last, 0));
+        CUDA_TRY(h, cudaStreamWaitEvent(st, h->done[layer], 0));
+      }
+      if (ev) CUDA_TRY(h, record_event(ev[0], st));
+      break;
+    case kStepNorm: {  // K1: Delta and its shard norm (Alg. 2 l.442-443) [+ exchange + K2]
+      FoldArgs f{};
+      f.on = fold ? 1 : 0;
+      if (fold) {
+        if (h->K > 1) f.x = xchg_args(h, ln, 0);
+        else f.x.K = 1;
+        f.dec = p.d;
+      }
+      if (p.mode.part > 0 && !p.S && (!h->peer || p.direct))
+        launched += launch_pg_norm_tma(dt, p.local, p.anchor, n, scr, h->part1[layer], p.mode.part, f, st);
+      else if (h->peer && !p.direct)
+        launched += launch_pg_norm_copy(dt, p.local, p.anchor, ln.Lown, n, scr, h->part1[layer], p.mode.cap, f, st);
+      else
+        launched += launch_pg_norm(dt, p.local, p.anchor, p.S, n, scr, h->part1[layer], p.mode.cap, f, st);
+      CUDA_TRY(h, cudaGetLastError());
+      if (ev) CUDA_TRY(h, record_event(ev[1], st));
+      break;
+    }
+    case kStepDecide:
+      if (!fold) {  // NCCL baseline: gather the K partials, then K2
+        NCCL_TRY(h, ncclAllGather(&scr->send1, scr->recv1, 1, ncclFloat64, ln.global, st));
+        launched += launch_decide(p.d, st);
+        CUDA_TRY(h, cudaGetLastError());
+      }
+      if (ev) CUDA_TRY(h, record_event(ev[2], st));
+      break;
+    case kStepExchange:
+      if (h->peer) {
+        // Eq. 3 as a reduce-scatter over NVLink peer memory: this rank's slice of Dbar; its
+        // last CTA exchanges the slice norms (also the barrier after which every member's D
+        // slice is complete)
+        FoldArgs f{};
+        f.on = h->dev_xchg ? 1 : 0;
+        if (h->dev_xchg) f.x = xchg_args(h, ln, 1);
+        launched += launch_rs(dt, p.pp, p.sl, p.anchor, ln.Down, scr, h->part2[layer], p.mode.peer_ctas,
+                              p.mode.smem_kb, f, st);
+        CUDA_TRY(h, cudaGetLastError());
+        if (ev) CUDA_TRY(h, record_event(ev[3], st));
+      } else if (N > 1) {
+        // Eq. 3: Dbar = sum_n w_n Delta_n, the weight applied inside NCCL (PreMulSum)
+        NCCL_TRY(h, ncclAllReduce(p.S, p.S, (size_t)n, ncclFloat32, ln.ops[layer], ln.sync, st));
+        if (ev) CUDA_TRY(h, record_event(ev[3], st));
+        launched += launch_sumsq(p.S, n, scr, h->part2[layer], p.mode.cap, st);
+        CUDA_TRY(h, cudaGetLastError());
+      }
+      break;
+    case kStepDbarNorm:
+      if (h->peer) {
+        if (!h->dev_xchg) NCCL_TRY(h, ncclAllGather(&scr->send2, scr->recv2, 1, ncclFloat64, ln.global, st));
+        if (ev) CUDA_TRY(h, record_event(ev[4], st));
+      } else if (N > 1) {
+        if (M > 1) NCCL_TRY(h, ncclAllGather(&scr->send2, scr->recv2, 1, ncclFloat64, ln.shard, st));
+        if (ev) CUDA_TRY(h, record_event(ev[4], st));
+      }
+      break;
+    case kStepUpdate:
+      if (h->peer) {
+        launched += launch_ag_update(dt, p.u, p.pp, p.sl, p.mode.peer_ctas, p.mode.smem_kb, st);
+      } else if (p.mode.part > 0 && !p.u.dbar && !p.gathered) {
+        launched += launch_update_tma(dt, p.u, p.mode.part, st);
+      } else {
+        launched += launch_update(dt, p.u, p.mode.cap, st);
+      }
+      CUDA_TRY(h, cudaGetLastError());
+      break;
+    case kStepGather:
+      if (p.gathered) {
+        // every member of the shard group has stored its shard into every gathered module
+        // once this barrier completes (their update kernels precede their contributions)
+        if (h->dev_xchg) {
+          launched += launch_xchg(xchg_args(h, ln, 2), ln.bar, ln.bar + 1, nullptr, st);
+          CUDA_TRY(h, cudaGetLastError());
+        } else {
+          double* gd = h->gather_dev + (size_t)layer * (h->M + 1);
+          NCCL_TRY(h, ncclAllGather(gd, gd + 1, 1, ncclFloat64, ln.shard, st));
+        }
+      }
+      break;
+    case kStepEnd:
+      if (ev) {
+        CUDA_TRY(h, record_event(ev[5], st));
+        h->pending.push_back(layer);
+      }
+      CUDA_TRY(h, record_event(h->done[layer], st));  // read by edit_sync_stats / acquire
+      CUDA_TRY(h, record_event(ln.last, st));
+      break;
+    default:
+      return fail(EDIT_ERR_INVALID_ARG, "bad step");
+  }
+  h->launches += launched;
+  return EDIT_OK;
+}
+
+edit_status_t enqueue_units(edit_sync_t const* hs, int nh, int nunits, const int32_t* layers,
+                            void* const* locals, float* const* anchors, float* const* momenta,
+                            const cudaStream_t* streams, bool use_lanes) {
+  if (use_lanes)
+    for (int k = 0; k < nh; ++k) {
+      edit_sync_t h = hs[k];
+      CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+      CUDA_TRY(h, cudaEventRecord(h->fork, streams[k]));
+      for (Lane& ln : h->lanes) CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->fork, 0));
+    }
+  std::vector<UnitPlan> plans(nh);
+  for (int i = 0; i < nunits; ++i) {
+    const int32_t layer = layers[i];
+    for (int k = 0; k < nh; ++k) {
+      edit_sync_t h = hs[k];
+      Lane& ln = use_lanes ? h->lanes[layer % (int)h->lanes.size()] : h->lanes[0];
+      Mode mode{};
+      mode.peer_ctas = h->peer_ctas;
+      const size_t at = (size_t)k * nunits + i;
+      TRY(plan_unit(h, ln, layer, locals[at], anchors[at], momenta[at], use_lanes ? ln.stream : streams[k], mode,
+                    plans[k]));
+    }
+    for (int step = 0; step < kNumSteps; ++step)
+      for (int k = 0; k < nh; ++k) {
+        if (nh > 1) CUDA_TRY(hs[k], cudaSetDevice(hs[k]->cfg.device));
+        const NvtxRange range(hs[k]->nvtx && step == kStepBegin, "edit_sync unit %d", layer);
+        TRY(enqueue_step(hs[k], plans[k], step));
+      }
+  }
+  if (use_lanes)
+    for (int k = 0; k < nh; ++k) {
+      edit_sync_t h = hs[k];
+      for (Lane& ln : h->lanes) {
+        CUDA_TRY(h, cudaEventRecord(ln.tail, ln.stream));
+        CUDA_TRY(h, cudaStreamWaitEvent(streams[k], ln.tail, 0));
+      }
+    }
+  return EDIT_OK;
+}
+
+// Warm-up all-reduce (Alg. 1 l.422-424), peer variant, step-major over nh handles: stage the
+// gradient where the row can read it; barrier; each member averages its 1/N slice from every
+// member; barrier; every member pulls each averaged slice from its owner.
+edit_status_t enqueue_warmup(edit_sync_t const* hs, int nh, int32_t layer, void* const* grads,
+                             const cudaStream_t* streams, bool force_peer) {
+  const char* wa = getenv("EDIT_WARMUP_ALGO");
+  for (int k = 0; k < nh; ++k) {
+    edit_sync_t h = hs[k];
+    TRY(check_unit_args(h, layer, grads[k], grads[k], grads[k]));
+    if (h->N == 1) return EDIT_OK;
+    const bool warm_peer = h->peer && (force_peer || (wa && !strcmp(wa, "peer")));
+    if (!warm_peer) {
+      if (nh > 1) return fail(EDIT_ERR_INVALID_ARG, "the simulated mesh runs the peer warm-up only");
+      // a pure mean (no compute to fuse): NCCL's all-reduce measured faster than the peer
+      // kernels (1x4 bf16 7B: 34.6 vs 54.1 ms; 2x2: 14.2 vs 16.3 ms), so it is the default
+      const int dt = h->cfg.param_dtype;
+      CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+      cudaStream_t st = streams[0];
+      Lane& ln = h->lanes[0];
+      CUDA_TRY(h, cudaStreamWaitEvent(st, ln.last, 0));
+      NCCL_TRY(h, ncclAllReduce(grads[0], grads[0], (size_t)h->numel[layer],
+                                dt == EDIT_BF16 ? ncclBfloat16 : ncclFloat32, ncclAvg, ln.sync, st));
+      CUDA_TRY(h, cudaEventRecord(ln.last, st));
+      return EDIT_OK;
+    }
+    CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+    if (!h->dev_xchg && !h->warm_dev)
+      CUDA_TRY(h, cudaMalloc(reinterpret_cast<void**>(&h->warm_dev), sizeof(double) * (h->N + 1)));
+  }
+  auto barrier = [&](edit_sync_t h, cudaStream_t st) -> edit_status_t {
+    Lane& ln = h->lanes[0];
+    if (h->dev_xchg) {
+      h->launches += launch_xchg(xchg_args(h, ln, 2), ln.bar, ln.bar + 1, nullptr, st);
+      CUDA_TRY(h, cudaGetLastError());
+    } else {
+      NCCL_TRY(h, ncclAllGather(h->warm_dev, h->warm_dev + 1, 1, ncclFloat64, ln.sync, st));
+    }
+    return EDIT_OK;
+  };
+  for (int step = 0; step < 6; ++step)
+    for (int k = 0; k < nh; ++k) {
+      edit_sync_t h = hs[k];
+      Lane& ln = h->lanes[0];
+      cudaStream_t st = streams[k];
+      const int dt = h->cfg.param_dtype;
+      const size_t esz = dt == EDIT_BF16 ? 2 : 4;
+      const Slicing sl = slicing_of(h->numel[layer], h->N, h->sync_idx, h->peer_tile);
+      if (nh > 1) CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+      switch (step) {
+        case 0:
+          CUDA_TRY(h, cudaStreamWaitEvent(st, ln.last, 0));
+          CUDA_TRY(h, cudaMemcpyAsync(ln.Lown, grads[k], (size_t)h->numel[layer] * esz, cudaMemcpyDeviceToDevice, st));
+          break;
+        case 1:  // staging complete on every member before any RS reads it
+        case 3:  // every averaged slice complete before any AG pulls it
+          TRY(barrier(h, st));
+          break;
+        case 2:
+          h->launches += launch_warm_rs(dt, ln.pp, sl, ln.Down, h->err_dev, st);
+          CUDA_TRY(h, cudaGetLastError());
+          break;
+        case 4:
+          h->launches += launch_warm_ag(dt, ln.pp, sl, grads[k], h->err_dev, st);
+          CUDA_TRY(h, cudaGetLastError());
+          break;
+        case 5:
+          CUDA_TRY(h, cudaEventRecord(ln.last, st));
+          break;
+      }
+    }
+  return EDIT_OK;
+}
+
+}  // namespace edit
+
+extern "C" {
+static edit_status_t exchange_ipc(edit_sync_t h, void* const* ptrs, const size_t* bytes, int L, ncclComm_t comm,
+                                  int P, int me, cudaStream_t st, std::vector<std::vector<void*>>& out,
+                                  std::vector<void*>& opened);
+
+const char* edit_sync_last_error(void) { return g_last_error.c_str(); }
+
+const char* edit_sync_version(void) { return "edit_sync 0.2 (sm_100a)"; }
+
+edit_status_t edit_sync_get_unique_id(uint8_t id[EDIT_UNIQUE_ID_BYTES]) {
+  static_assert(sizeof(ncclUniqueId) == EDIT_UNIQUE_ID_BYTES, "ncclUniqueId size");
+  if (!id) return fail(EDIT_ERR_INVALID_ARG, "null id");
+  ncclUniqueId u;
+  ncclResult_t r = ncclGetUniqueId(&u);
+  if (r != ncclSuccess) return fail(EDIT_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  memcpy(id, &u, sizeof u);
+  return EDIT_OK;
+}
+
+edit_status_t edit_sync_workspace_bytes(const edit_sync_config_t* cfg, size_t* bytes) {
+  TRY(validate(cfg));
+  if (!bytes) return fail(EDIT_ERR_INVALID_ARG, "null bytes");
+  *bytes = layout_of(*cfg).total;
+  return EDIT_OK;
+}
+
+// Settings every rank must agree on (slice layout, lane mapping, exchange protocol, units):
+// a digest of them is all-gathered at init and compared.
+struct ConfigDigest {
+  int32_t nlanes, peer_tile, dev_xchg, graph, algo, L, M, N, dtype, flags;
+  uint64_t numel_hash;
+};
+
+edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDIT_UNIQUE_ID_BYTES],
+                             void* workspace, size_t workspace_bytes, edit_sync_t* out) {
+  TRY(validate(cfg));
+  if (!out) return fail(EDIT_ERR_INVALID_ARG, "null out");
+  *out = nullptr;
+  const int K = cfg->shard_dim * cfg->sync_dim;
+  if (K > 1 && !id) return fail(EDIT_ERR_INVALID_ARG, "null unique id for a multi-rank mesh");
+  edit_sync_t h = nullptr;
+  edit_status_t st = create_local(cfg, workspace, workspace_bytes, &h);
+  auto bail = [&](edit_status_t s) {
+    if (h) edit_sync_destroy(h);
+    return s;
+  };
+  if (st != EDIT_OK) return bail(st);
+#define INIT_CUDA(expr)                                                                     \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return bail(fail(EDIT_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)));   \
+  } while (0)
+#define INIT_NCCL(expr)                                                                     \
+  do {                                                                                      \
+    ncclResult_t r_ = (expr);                                                               \
+    if (r_ != ncclSuccess)                                                                  \
+      return bail(fail(EDIT_ERR_NCCL, std::string(#expr ": ") + ncclGetErrorString(r_)));   \
+  } while (0)
+  const int nlanes = (int)h->lanes.size();
+  for (int li = 0; li < nlanes && K > 1; ++li) {
+    Lane& ln = h->lanes[li];
     if (li == 0) {
       ncclUniqueId u;
       memcpy(&u, id, sizeof u);
       INIT_NCCL(ncclCommInitRank(&ln.global, K, u, cfg->rank));
+      // every rank must agree on the settings that fix slice layout, lane mapping and the
+      // exchange protocol (read per rank from the environment): compare digests
+      ConfigDigest mine{nlanes, h->peer_tile, h->dev_xchg ? 1 : 0, h->graph ? 1 : 0, cfg->algo, cfg->num_layers,
+                        h->M, h->N, cfg->param_dtype, (int32_t)cfg->flags, 1469598103934665603ull};
+      for (int64_t x : h->numel) mine.numel_hash = (mine.numel_hash ^ (uint64_t)x) * 1099511628211ull;
+      char* dev = nullptr;
+      INIT_CUDA(cudaMalloc(&dev, sizeof(ConfigDigest) * (K + 1)));
+      INIT_CUDA(cudaMemcpy(dev, &mine, sizeof mine, cudaMemcpyHostToDevice));
+      INIT_NCCL(ncclAllGather(dev, dev + sizeof mine, sizeof mine, ncclChar, ln.global, ln.stream));
+      INIT_CUDA(cudaStreamSynchronize(ln.stream));
+      std::vector<ConfigDigest> all(K);
+      INIT_CUDA(cudaMemcpy(all.data(), dev + sizeof mine, sizeof mine * K, cudaMemcpyDeviceToHost));
+      INIT_CUDA(cudaFree(dev));
+      for (int r = 0; r < K; ++r)
+        if (memcmp(&all[r], &all[0], sizeof mine) != 0)
+          return bail(fail(EDIT_ERR_INVALID_ARG,
+                           "ranks disagree on EDIT_LANES / EDIT_PEER_TILE / EDIT_XCHG / EDIT_GRAPH / algo / "
+                           "units / dtype / flags (rank " + std::to_string(r) + " differs from rank 0)"));
     } else {
       INIT_NCCL(ncclCommSplit(h->lanes[0].global, 0, cfg->rank, &ln.global, nullptr));  // a dup
     }
     // sync group (row): same shard index m, ordered by n; shard group (column): same n.
     INIT_NCCL(ncclCommSplit(ln.global, h->shard_idx, h->sync_idx, &ln.sync, nullptr));
     INIT_NCCL(ncclCommSplit(ln.global, h->sync_idx, h->shard_idx, &ln.shard, nullptr));
-    if (h->dev_xchg) {
-      INIT_CUDA(cudaMalloc(reinterpret_cast<void**>(&ln.mailbox), align_up(mailbox_bytes(K), 256)));
-      INIT_CUDA(cudaMemset(ln.mailbox, 0, align_up(mailbox_bytes(K), 256)));
-      INIT_CUDA(cudaMalloc(reinterpret_cast<void**>(&ln.xerr), sizeof(int)));
-      INIT_CUDA(cudaMemset(ln.xerr, 0, sizeof(int)));
-      if (h->graph) {
-        INIT_CUDA(cudaMalloc(reinterpret_cast<void**>(&ln.dseq), sizeof(unsigned long long) * kXchgPhases));
-        INIT_CUDA(cudaMemset(ln.dseq, 0, sizeof(unsigned long long) * kXchgPhases));
-      }
-      INIT_CUDA(cudaDeviceSynchronize());
+    if (ln.mailbox) {
       void* mine = ln.mailbox;
       size_t mb = mailbox_bytes(K);
       std::vector<std::vector<void*>> boxes;
@@ -432,9 +742,6 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
       for (int r = 0; r < K; ++r) ln.mp.box[r] = static_cast<unsigned long long*>(boxes[0][r]);
     }
     if (h->peer) {
-      const Slicing sl = slicing_of(max_numel, h->N, 0, h->peer_tile);
-      INIT_CUDA(cudaMalloc(&ln.Lown, align_up((size_t)std::max<int64_t>(max_numel, 8) * esz, 256)));
-      INIT_CUDA(cudaMalloc(reinterpret_cast<void**>(&ln.Down), align_up((size_t)sl.slice * 8 * sizeof(float), 256)));
       // exchange the IPC handles over the lane's sync comm (row): [N][2] cudaIpcMemHandle_t
       cudaIpcMemHandle_t mine[2];
       INIT_CUDA(cudaIpcGetMemHandle(&mine[0], ln.Lown));
@@ -449,11 +756,7 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
       INIT_CUDA(cudaMemcpy(all.data(), dev + hb, hb * h->N, cudaMemcpyDeviceToHost));
       INIT_CUDA(cudaFree(dev));
       for (int j = 0; j < h->N; ++j) {
-        if (j == h->sync_idx) {
-          ln.pp.L[j] = ln.Lown;
-          ln.pp.D[j] = ln.Down;
-          continue;
-        }
+        if (j == h->sync_idx) continue;
         void *pl = nullptr, *pd = nullptr;
         INIT_CUDA(cudaIpcOpenMemHandle(&pl, all[2 * j], cudaIpcMemLazyEnablePeerAccess));
         ln.opened.push_back(pl);
@@ -463,12 +766,12 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
         ln.pp.D[j] = static_cast<float*>(pd);
       }
     } else if (h->N > 1) {
-      INIT_CUDA(cudaMalloc(reinterpret_cast<void**>(&ln.S), align_up((size_t)std::max<int64_t>(max_numel, 8) * 4, 256)));
       ln.ops.assign(cfg->num_layers, ncclRedOp_t{});
       for (int l = 0; l < cfg->num_layers; ++l)
         INIT_NCCL(ncclRedOpCreatePreMulSum(&ln.ops[l], &h->scratch[l].w, ncclFloat32, ncclScalarDevice, ln.sync));
     }
   }
+  INIT_CUDA(cudaDeviceSynchronize());
 #undef INIT_CUDA
 #undef INIT_NCCL
   h->ready = true;
@@ -476,176 +779,12 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
   return EDIT_OK;
 }
 
-static edit_status_t check_unit_args(edit_sync_t h, int32_t layer, const void* local, const void* anchor,
-                                     const void* momentum) {
-  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
-  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
-  if (layer < 0 || layer >= h->cfg.num_layers) return fail(EDIT_ERR_INVALID_ARG, "layer out of range");
-  if (h->numel[layer] > 0 && (!local || !anchor || !momentum)) return fail(EDIT_ERR_INVALID_ARG, "null buffer");
-  if ((((uintptr_t)local) | ((uintptr_t)anchor) | ((uintptr_t)momentum)) & 15u)
-    return fail(EDIT_ERR_INVALID_ARG, "buffers must be 16-byte aligned");
-  return EDIT_OK;
-}
-
-// Enqueue Sync() of one unit on stream `st` using lane `ln`'s communicators and buffers.
-struct Mode {
-  bool ef;        // L2 evict_first streaming
-  int cap;        // max CTAs of the LDG streaming kernels (0 = full grid)
-  int peer_ctas;  // persistent grid of the TMA peer kernels
-  int smem_kb;    // shared-memory ring of the TMA peer kernels (0 = default)
-  int part = 0;   // > 0: partition mode, K1 / K4 / peer kernels on <= part persistent CTAs
-};
-
-// cudaEventRecord that stays a real (external) event record when `st` is being captured into
-// a CUDA graph (EDIT_GRAPH=1): the round's done / profiling events are read by the host later.
-static cudaError_t record_event(cudaEvent_t ev, cudaStream_t st) {
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  const cudaError_t e = cudaStreamIsCapturing(st, &cap);
-  if (e != cudaSuccess) return e;
-  return cap == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal)
-                                              : cudaEventRecord(ev, st);
-}
-
-static edit_status_t sync_unit(edit_sync_t h, Lane& ln, int32_t layer, void* local, float* anchor, float* momentum,
-                               cudaStream_t st, const Mode& mode) {
-  const bool ef = mode.ef;
-  const int64_t n = h->numel[layer];
-  const int dt = h->cfg.param_dtype;
-  LayerScratch* scr = &h->scratch[layer];
-  const int M = h->M, N = h->N;
-  int launched = 0;
-  const NvtxRange range(h->nvtx, "edit_sync unit %d", layer);
-
-  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
-  cudaEvent_t* ev = h->profiling ? &h->prof[(size_t)layer * (EDIT_NUM_PHASES + 1)] : nullptr;
-  if (ev) CUDA_TRY(h, record_event(ev[0], st));
-  // K1: Delta and its shard norm (Alg. 2 l.442-443)
-  float* S = (N > 1 && !h->peer) ? ln.S : nullptr;
-  // peer path: read the members' registered locals directly, else stage a copy of ours
-  const bool direct = h->peer && !h->reg_local.empty() && h->reg_local[layer] == local;
-  PeerPtrs pp = ln.pp;
-  if (direct)
-    for (int j = 0; j < N; ++j) pp.L[j] = h->reg_peer[layer][j];
-  if (mode.part > 0 && !S && (!h->peer || direct))
-    launched += launch_pg_norm_tma(dt, local, anchor, n, scr, h->part1[layer], mode.part, st);
-  else if (h->peer && !direct)
-    launched += launch_pg_norm_copy(dt, local, anchor, ln.Lown, n, scr, h->part1[layer], ef, mode.cap, st);
-  else
-    launched += launch_pg_norm(dt, local, anchor, S, n, scr, h->part1[layer], ef, mode.cap, st);
-  CUDA_TRY(h, cudaGetLastError());
-  if (ev) CUDA_TRY(h, record_event(ev[1], st));
-  // module norms of every replica on every rank: one K-scalar gather (R6),
-  // then K2 on the gathered norms (fused into the mailbox exchange kernel when K > 1)
-  DecideArgs d{};
-  d.parts = h->K > 1 ? scr->recv1 : &scr->send1;
-  d.M = M;
-  d.N = N;
-  d.my_n = h->sync_idx;
-  d.ema = h->ema + (size_t)layer * N;
-  d.rec = h->rec + layer;
-  d.w_out = &scr->w;
-  d.w_all_out = scr->w_all;
-  d.rollback_out = &scr->rollback;
-  d.gsq_out = &scr->gsq;
-  d.alpha = h->cfg.ema_alpha;
-  d.delta = h->cfg.anomaly_threshold;
-  d.warmup = h->cfg.ema_warmup_rounds;
-  d.flags = h->cfg.flags;
-  if (h->K > 1 && ln.mailbox) {
-    launched += launch_xchg(ln.mp, h->K, h->cfg.rank, 0, ++ln.seq[0], &scr->send1, scr->recv1, ln.xerr, st, &d,
-                            ln.dseq);
-    CUDA_TRY(h, cudaGetLastError());
-  } else {
-    if (h->K > 1) NCCL_TRY(h, ncclAllGather(&scr->send1, scr->recv1, 1, ncclFloat64, ln.global, st));
-    launched += launch_decide(d, st);
-    CUDA_TRY(h, cudaGetLastError());
-  }
-  if (ev) CUDA_TRY(h, record_event(ev[2], st));
-
-  UpdateArgs u{};
-  u.local = local;
-  u.anchor = anchor;
-  u.momentum = momentum;
-  u.n = n;
-  u.rollback = &scr->rollback;
-  u.nu = h->cfg.outer_lr;
-  u.mu = h->cfg.outer_momentum;
-  u.phi = h->cfg.clip_threshold;
-  u.eps = h->cfg.clip_eps;
-  u.flags = h->cfg.flags;
-  u.rec = h->rec + layer;
-  const bool gathered = !h->reg_gather.empty() && h->numel[layer] > 0;
-  if (gathered) {
-    u.gather_M = h->M;
-    u.gather_off = (int64_t)h->shard_idx * n;
-    for (int q = 0; q < h->M; ++q) u.gather[q] = h->reg_gather[layer][q];
-  }
-  if (h->peer) {
-    // Eq. 3 as a reduce-scatter over NVLink peer memory: this rank's slice of Dbar
-    const Slicing sl = slicing_of(n, N, h->sync_idx, h->peer_tile);
-    launched += launch_rs(dt, pp, sl, anchor, ln.Down, scr, h->part2[layer], mode.peer_ctas, ef, mode.smem_kb, st);
-    CUDA_TRY(h, cudaGetLastError());
-    if (ev) CUDA_TRY(h, record_event(ev[3], st));
-    // ||Dbar||^2 of the module = sum over every slice of every shard: one K-scalar gather
-    // (also the barrier after which every member's D slice is complete)
-    if (ln.mailbox) {
-      launched += launch_xchg(ln.mp, h->K, h->cfg.rank, 1, ++ln.seq[1], &scr->send2, scr->recv2, ln.xerr, st,
-                              nullptr, ln.dseq);
-      CUDA_TRY(h, cudaGetLastError());
-    } else {
-      NCCL_TRY(h, ncclAllGather(&scr->send2, scr->recv2, 1, ncclFloat64, ln.global, st));
-    }
-    if (ev) CUDA_TRY(h, record_event(ev[4], st));
-    u.gparts = scr->recv2;
-    u.n_gparts = h->K;
-    launched += launch_ag_update(dt, u, pp, sl, mode.peer_ctas, ef, mode.smem_kb, st);
-  } else if (N > 1) {
-    // Eq. 3: Dbar = sum_n w_n Delta_n, the weight applied inside NCCL (PreMulSum)
-    NCCL_TRY(h, ncclAllReduce(S, S, (size_t)n, ncclFloat32, ln.ops[layer], ln.sync, st));
-    if (ev) CUDA_TRY(h, record_event(ev[3], st));
-    launched += launch_sumsq(S, n, scr, h->part2[layer], ef, mode.cap, st);
-    CUDA_TRY(h, cudaGetLastError());
-    if (M > 1) {
-      NCCL_TRY(h, ncclAllGather(&scr->send2, scr->recv2, 1, ncclFloat64, ln.shard, st));
-      u.gparts = scr->recv2;
-      u.n_gparts = M;
-    } else {
-      u.gparts = &scr->send2;
-      u.n_gparts = 1;
-    }
-    u.dbar = S;
-    if (ev) CUDA_TRY(h, record_event(ev[4], st));
-  } else {
-    u.dbar = nullptr;  // Dbar = Delta, G_bar = G (module level)
-    u.gparts = &scr->gsq;
-    u.n_gparts = 1;
-  }
-  if (!h->peer) {
-    if (mode.part > 0 && !u.dbar && !gathered) launched += launch_update_tma(dt, u, mode.part, st);
-    else launched += launch_update(dt, u, ef, mode.cap, st);
-  }
-  CUDA_TRY(h, cudaGetLastError());
-  if (gathered) {
-    // every member of the shard group has stored its shard into every gathered module once
-    // this scalar gather completes (their update kernels precede their contributions)
-    double* gd = h->gather_dev + (size_t)layer * (h->M + 1);
-    NCCL_TRY(h, ncclAllGather(gd, gd + 1, 1, ncclFloat64, ln.shard, st));
-  }
-  if (ev) {
-    CUDA_TRY(h, record_event(ev[5], st));
-    h->pending.push_back(layer);
-  }
-  CUDA_TRY(h, record_event(h->done[layer], st));  // read by edit_sync_stats / acquire
-  h->launches += launched;
-  return EDIT_OK;
-}
-
 edit_status_t edit_layer_sync(edit_sync_t h, int32_t layer, void* local, float* anchor, float* momentum,
                               void* stream) {
-  edit_status_t rc = check_unit_args(h, layer, local, anchor, momentum);
-  if (rc != EDIT_OK) return rc;
-  return sync_unit(h, h->lanes[0], layer, local, anchor, momentum, static_cast<cudaStream_t>(stream),
-                   Mode{h->ef_direct, 0, h->peer_ctas, 0});
+  TRY(check_unit_args(h, layer, local, anchor, momentum));
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return enqueue_units(&h, 1, 1, &layer, &local, &anchor, &momentum, &st, false);
 }
 
 typedef CUresult_t (*AddrRangeFn)(unsigned long long*, size_t*, unsigned long long);
@@ -725,7 +864,7 @@ static edit_status_t exchange_ipc(edit_sync_t h, void* const* ptrs, const size_t
 
 edit_status_t edit_sync_register_gather(edit_sync_t h, void* const* full_bufs) {
   if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
-  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  TRY(check_err(h));
   if (!full_bufs) return fail(EDIT_ERR_INVALID_ARG, "null buffer array");
   if (h->M == 1) return EDIT_OK;
   if (!h->reg_gather.empty()) return fail(EDIT_ERR_INVALID_ARG, "gather buffers already registered");
@@ -742,16 +881,16 @@ edit_status_t edit_sync_register_gather(edit_sync_t h, void* const* full_bufs) {
     bytes[u] = (size_t)h->M * h->numel[u] * esz;
   }
   Lane& ln = h->lanes[0];
-  edit_status_t rc = exchange_ipc(h, ptrs.data(), bytes.data(), L, ln.shard, h->M, h->shard_idx, ln.stream,
-                                  h->reg_gather, h->gather_opened);
-  if (rc != EDIT_OK) return rc;
+  TRY(exchange_ipc(h, ptrs.data(), bytes.data(), L, ln.shard, h->M, h->shard_idx, ln.stream, h->reg_gather,
+                   h->gather_opened));
   CUDA_TRY(h, cudaMalloc(reinterpret_cast<void**>(&h->gather_dev), sizeof(double) * (size_t)L * (h->M + 1)));
+  clear_graphs(h);  // a captured round holds the non-gathering update kernels
   return EDIT_OK;
 }
 
 edit_status_t edit_sync_register_locals(edit_sync_t h, void* const* locals) {
   if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
-  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  TRY(check_err(h));
   if (!locals) return fail(EDIT_ERR_INVALID_ARG, "null buffer array");
   if (!h->peer) return EDIT_OK;
   if (!h->reg_local.empty()) return fail(EDIT_ERR_INVALID_ARG, "locals already registered");
@@ -769,70 +908,60 @@ edit_status_t edit_sync_register_locals(edit_sync_t h, void* const* locals) {
   }
   std::vector<std::vector<void*>> peers;
   Lane& ln = h->lanes[0];
-  edit_status_t rc = exchange_ipc(h, ptrs.data(), bytes.data(), L, ln.sync, h->N, h->sync_idx, ln.stream, peers,
-                                  h->reg_opened);
-  if (rc != EDIT_OK) return rc;
+  TRY(exchange_ipc(h, ptrs.data(), bytes.data(), L, ln.sync, h->N, h->sync_idx, ln.stream, peers, h->reg_opened));
   h->reg_peer.assign(L, std::vector<const void*>(h->N, nullptr));
   for (int u = 0; u < L; ++u)
     for (int j = 0; j < h->N; ++j) h->reg_peer[u][j] = peers[u][j];
   h->reg_local.assign(locals, locals + L);
+  clear_graphs(h);  // a captured round reads the staging copies
   return EDIT_OK;
 }
 
 edit_status_t edit_sync_round(edit_sync_t h, void* const* locals, float* const* anchors, float* const* momenta,
                               void* stream) {
   if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
-  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  TRY(check_err(h));
   if (!locals || !anchors || !momenta) return fail(EDIT_ERR_INVALID_ARG, "null buffer arrays");
   if (h->sched_active) return fail(EDIT_ERR_INVALID_ARG, "a scheduled round is active");
   const int L = h->cfg.num_layers;
-  for (int u = 0; u < L; ++u) {
-    edit_status_t rc = check_unit_args(h, u, locals[u], anchors[u], momenta[u]);
-    if (rc != EDIT_OK) return rc;
-  }
+  for (int u = 0; u < L; ++u) TRY(check_unit_args(h, u, locals[u], anchors[u], momenta[u]));
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   const NvtxRange range(h->nvtx, "edit_sync_round (%d units)", L);
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  std::vector<int32_t> layers(L);
+  for (int u = 0; u < L; ++u) layers[u] = u;
   const bool use_graph = h->graph && (h->K == 1 || h->lanes[0].dseq != nullptr);
+  if (!use_graph) return enqueue_units(&h, 1, L, layers.data(), locals, (float* const*)anchors, (float* const*)momenta,
+                                       &cs, true);
   std::vector<uintptr_t> key;
-  if (use_graph) {
-    key.reserve(3 * (size_t)L);
-    for (int u = 0; u < L; ++u) {
-      key.push_back(reinterpret_cast<uintptr_t>(locals[u]));
-      key.push_back(reinterpret_cast<uintptr_t>(anchors[u]));
-      key.push_back(reinterpret_cast<uintptr_t>(momenta[u]));
-    }
-    key.push_back(h->profiling ? 1u : 0u);  // a profiled capture holds the phase events
-    for (const RoundGraph& g : h->graphs)
-      if (g.key == key) {
-        CUDA_TRY(h, cudaGraphLaunch(g.exec, cs));
-        h->launches += g.launches;
-        if (h->profiling)
-          for (int u = 0; u < L; ++u) h->pending.push_back(u);
-        return EDIT_OK;
-      }
-    // capture on a library stream (the caller's may be the legacy default stream, which
-    // cannot be captured); the graph is then launched on the caller's stream
-    if (!h->cap_stream) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
-    CUDA_TRY(h, cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeRelaxed));
+  key.reserve(3 * (size_t)L + 1);
+  for (int u = 0; u < L; ++u) {
+    key.push_back(reinterpret_cast<uintptr_t>(locals[u]));
+    key.push_back(reinterpret_cast<uintptr_t>(anchors[u]));
+    key.push_back(reinterpret_cast<uintptr_t>(momenta[u]));
   }
-  cudaStream_t origin = use_graph ? h->cap_stream : cs;
+  key.push_back(h->profiling ? 1u : 0u);  // a profiled capture holds the phase events
+  // a replay (or the first launch) is ordered after every earlier use of the lanes' buffers
+  // and of the units' scratch, on whatever stream it ran
+  auto launch = [&](RoundGraph& g) -> edit_status_t {
+    for (Lane& ln : h->lanes) CUDA_TRY(h, cudaStreamWaitEvent(cs, ln.last, 0));
+    for (int u = 0; u < L; ++u) CUDA_TRY(h, cudaStreamWaitEvent(cs, h->done[u], 0));
+    CUDA_TRY(h, cudaGraphLaunch(g.exec, cs));
+    h->launches += g.launches;
+    if (h->profiling)
+      for (int u = 0; u < L; ++u) h->pending.push_back(u);
+    return EDIT_OK;
+  };
+  for (RoundGraph& g : h->graphs)
+    if (g.key == key) return launch(g);
+  // capture on a library stream (the caller's may be the legacy default stream, which
+  // cannot be captured); the graph is then launched on the caller's stream
+  if (!h->cap_stream) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+  CUDA_TRY(h, cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeRelaxed));
   const int64_t launches0 = h->launches;
-  edit_status_t rc = EDIT_OK;
-  const int nl = (int)h->lanes.size();
-  if (cudaEventRecord(h->fork, origin) != cudaSuccess) rc = fail(EDIT_ERR_CUDA, "fork record");
-  for (Lane& ln : h->lanes)
-    if (rc == EDIT_OK && cudaStreamWaitEvent(ln.stream, h->fork, 0) != cudaSuccess) rc = fail(EDIT_ERR_CUDA, "fork wait");
-  for (int u = 0; u < L && rc == EDIT_OK; ++u) {
-    Lane& ln = h->lanes[u % nl];
-    rc = sync_unit(h, ln, u, locals[u], anchors[u], momenta[u], ln.stream, Mode{h->ef_direct, 0, h->peer_ctas, 0});
-  }
-  for (Lane& ln : h->lanes) {
-    if (rc != EDIT_OK) break;
-    if (cudaEventRecord(ln.tail, ln.stream) != cudaSuccess || cudaStreamWaitEvent(origin, ln.tail, 0) != cudaSuccess)
-      rc = fail(EDIT_ERR_CUDA, "join");
-  }
-  if (!use_graph) return rc;
+  const std::vector<int32_t> pending0 = h->pending;
+  edit_status_t rc = enqueue_units(&h, 1, L, layers.data(), locals, (float* const*)anchors, (float* const*)momenta,
+                                   &h->cap_stream, true);
   cudaGraph_t graph = nullptr;
   const cudaError_t ec = cudaStreamEndCapture(h->cap_stream, &graph);
   if (rc != EDIT_OK) {
@@ -843,60 +972,30 @@ edit_status_t edit_sync_round(edit_sync_t h, void* const* locals, float* const* 
   RoundGraph g;
   g.key = std::move(key);
   g.launches = h->launches - launches0;
+  h->launches = launches0;  // capture launched nothing; the replay below does
+  h->pending = pending0;
   const cudaError_t ei = cudaGraphInstantiate(&g.exec, graph, 0);
   cudaGraphDestroy(graph);
   CUDA_TRY(h, ei);
-  h->launches = launches0;  // capture launched nothing; the replay below does
   if (h->graphs.size() >= 4) {
     cudaGraphExecDestroy(h->graphs.front().exec);
     h->graphs.erase(h->graphs.begin());
   }
   h->graphs.push_back(std::move(g));
-  CUDA_TRY(h, cudaGraphLaunch(h->graphs.back().exec, cs));
-  h->launches += h->graphs.back().launches;
-  return EDIT_OK;
+  return launch(h->graphs.back());
 }
 
 edit_status_t edit_warmup_allreduce(edit_sync_t h, int32_t layer, void* grad, void* stream) {
-  edit_status_t rc = check_unit_args(h, layer, grad, grad, grad);
-  if (rc != EDIT_OK) return rc;
-  if (h->N == 1) return EDIT_OK;
-  const int64_t n = h->numel[layer];
-  const int dt = h->cfg.param_dtype;
-  const size_t esz = dt == EDIT_BF16 ? 2 : 4;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  Lane& ln = h->lanes[0];
+  TRY(check_unit_args(h, layer, grad, grad, grad));
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
-  // a pure mean (no compute to fuse): NCCL's all-reduce measured faster than the peer
-  // kernels (1x4 bf16 7B: 34.6 vs 54.1 ms; 2x2: 14.2 vs 16.3 ms, profiles/r1_bench_4gpu_final_*),
-  // so it is the default; EDIT_WARMUP_ALGO=peer selects the peer-memory variant
-  const char* wa = getenv("EDIT_WARMUP_ALGO");
-  const bool warm_peer = h->peer && wa && !strcmp(wa, "peer");
-  if (!warm_peer) {
-    NCCL_TRY(h, ncclAllReduce(grad, grad, (size_t)n, dt == EDIT_BF16 ? ncclBfloat16 : ncclFloat32, ncclAvg,
-                              ln.sync, st));
-    return EDIT_OK;
-  }
-  if (!h->warm_dev) CUDA_TRY(h, cudaMalloc(reinterpret_cast<void**>(&h->warm_dev), sizeof(double) * (h->N + 1)));
-  const Slicing sl = slicing_of(n, h->N, h->sync_idx, h->peer_tile);
-  int launched = 0;
-  // stage this member's gradient where the row can read it; the scalar gathers are the
-  // cross-rank barriers (staging complete before any RS; every RS complete before any AG)
-  CUDA_TRY(h, cudaMemcpyAsync(ln.Lown, grad, (size_t)n * esz, cudaMemcpyDeviceToDevice, st));
-  NCCL_TRY(h, ncclAllGather(h->warm_dev, h->warm_dev + 1, 1, ncclFloat64, ln.sync, st));
-  launched += launch_warm_rs(dt, ln.pp, sl, ln.Down, st);
-  CUDA_TRY(h, cudaGetLastError());
-  NCCL_TRY(h, ncclAllGather(h->warm_dev, h->warm_dev + 1, 1, ncclFloat64, ln.sync, st));
-  launched += launch_warm_ag(dt, ln.pp, sl, grad, st);
-  CUDA_TRY(h, cudaGetLastError());
-  h->launches += launched;
-  return EDIT_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return enqueue_warmup(&h, 1, layer, &grad, &st, false);
 }
 
 edit_status_t edit_layer_sync_host(edit_sync_t h, int32_t layer, void* local_host, float* anchor_host,
                                    float* momentum_host, void* stream) {
   if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
-  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  TRY(check_err(h));
   if (layer < 0 || layer >= h->cfg.num_layers) return fail(EDIT_ERR_INVALID_ARG, "layer out of range");
   const int64_t n = h->numel[layer];
   if (n > 0 && (!local_host || !anchor_host || !momentum_host)) return fail(EDIT_ERR_INVALID_ARG, "null buffer");
@@ -932,8 +1031,7 @@ edit_status_t edit_layer_sync_host(edit_sync_t h, int32_t layer, void* local_hos
   CUDA_TRY(h, cudaMemcpyAsync(loc, local_host, (size_t)n * esz, cudaMemcpyHostToDevice, h->h2d));
   CUDA_TRY(h, cudaEventRecord(h->slot_in[slot], h->h2d));
   CUDA_TRY(h, cudaStreamWaitEvent(st, h->slot_in[slot], 0));
-  edit_status_t rc = edit_layer_sync(h, layer, loc, anc, mom, stream);
-  if (rc != EDIT_OK) return rc;
+  TRY(edit_layer_sync(h, layer, loc, anc, mom, stream));
   CUDA_TRY(h, cudaEventRecord(h->slot_done[slot], st));
   CUDA_TRY(h, cudaStreamWaitEvent(h->d2h, h->slot_done[slot], 0));
   CUDA_TRY(h, cudaMemcpyAsync(anchor_host, anc, (size_t)n * 4, cudaMemcpyDeviceToHost, h->d2h));
@@ -945,7 +1043,7 @@ edit_status_t edit_layer_sync_host(edit_sync_t h, int32_t layer, void* local_hos
 
 edit_status_t edit_sync_host_wait(edit_sync_t h, void* stream) {
   if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
-  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  TRY(check_err(h));
   if (!h->staging) return EDIT_OK;
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -960,8 +1058,8 @@ static edit_status_t sched_enqueue_next(edit_sync_t h, cudaStream_t gate = nullp
     CUDA_TRY(h, cudaEventRecord(h->gate_ev[u], gate));
     CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->gate_ev[u], 0));
   }
-  Mode mode{h->ef_sched, h->sched_ctas, h->sched_ctas > 0 ? h->sched_ctas : h->peer_ctas,
-            h->sched_ctas > 0 ? h->sched_smem_kb : 0};
+  Mode mode{h->sched_ctas, h->sched_ctas > 0 ? h->sched_ctas : h->peer_ctas, h->sched_ctas > 0 ? h->sched_smem_kb : 0,
+            0};
   if (h->sched_part > 0 && u >= h->sched_full_units) {
     // partition mode: persistent TMA pipelines with full rings; the lanes run concurrently,
     // so each lane's kernels get an equal share of the sched_part SMs
@@ -972,21 +1070,22 @@ static edit_status_t sched_enqueue_next(edit_sync_t h, cudaStream_t gate = nullp
     mode.smem_kb = 0;
     mode.part = per;
   }
-  return sync_unit(h, ln, u, h->sched_local[u], h->sched_anchor[u], h->sched_mom[u], ln.stream, mode);
+  UnitPlan p;
+  TRY(plan_unit(h, ln, u, h->sched_local[u], h->sched_anchor[u], h->sched_mom[u], ln.stream, mode, p));
+  const NvtxRange range(h->nvtx, "edit_sync unit %d (scheduled)", u);
+  for (int step = 0; step < kNumSteps; ++step) TRY(enqueue_step(h, p, step));
+  return EDIT_OK;
 }
 
 edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* const* anchors,
                                      float* const* momenta, int32_t depth, void* compute_stream) {
   if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
-  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  TRY(check_err(h));
   if (!locals || !anchors || !momenta) return fail(EDIT_ERR_INVALID_ARG, "null buffer arrays");
   if (depth < 1) return fail(EDIT_ERR_INVALID_ARG, "depth must be >= 1");
   if (h->sched_active) return fail(EDIT_ERR_INVALID_ARG, "a round is already active");
   const int L = h->cfg.num_layers;
-  for (int u = 0; u < L; ++u) {
-    edit_status_t rc = check_unit_args(h, u, locals[u], anchors[u], momenta[u]);
-    if (rc != EDIT_OK) return rc;
-  }
+  for (int u = 0; u < L; ++u) TRY(check_unit_args(h, u, locals[u], anchors[u], momenta[u]));
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   h->sched_local.assign(locals, locals + L);
   h->sched_anchor.assign(anchors, anchors + L);
@@ -999,43 +1098,32 @@ edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* 
   // inner steps that produced the locals)
   CUDA_TRY(h, cudaEventRecord(h->fork, static_cast<cudaStream_t>(compute_stream)));
   for (Lane& ln : h->lanes) CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->fork, 0));
-  while (h->sched_next_sync < std::min(depth, L)) {
-    edit_status_t rc = sched_enqueue_next(h);
-    if (rc != EDIT_OK) return rc;
-  }
+  while (h->sched_next_sync < std::min(depth, L)) TRY(sched_enqueue_next(h));
   return EDIT_OK;
 }
 
 edit_status_t edit_sched_acquire(edit_sync_t h, int32_t layer, void* compute_stream) {
   if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
-  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  TRY(check_err(h));
   if (!h->sched_active) return fail(EDIT_ERR_INVALID_ARG, "no active round");
   if (layer != h->sched_next_acquire) return fail(EDIT_ERR_INVALID_ARG, "acquire units in order 0..L-1");
   const int L = h->cfg.num_layers;
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
-  while (h->sched_next_sync <= layer) {  // (depth can only lag if acquire skipped ahead)
-    edit_status_t rc = sched_enqueue_next(h);
-    if (rc != EDIT_OK) return rc;
-  }
+  while (h->sched_next_sync <= layer) TRY(sched_enqueue_next(h));  // (depth can only lag if acquire skipped ahead)
   CUDA_TRY(h, cudaStreamWaitEvent(static_cast<cudaStream_t>(compute_stream), h->done[layer], 0));
   h->sched_next_acquire = layer + 1;
-  if (h->sched_next_sync < L && h->sched_next_sync <= layer + h->sched_depth) {
-    edit_status_t rc = sched_enqueue_next(h, static_cast<cudaStream_t>(compute_stream));
-    if (rc != EDIT_OK) return rc;
-  }
+  if (h->sched_next_sync < L && h->sched_next_sync <= layer + h->sched_depth)
+    TRY(sched_enqueue_next(h, static_cast<cudaStream_t>(compute_stream)));
   return EDIT_OK;
 }
 
 edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream) {
   if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
-  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  TRY(check_err(h));
   if (!h->sched_active) return fail(EDIT_ERR_INVALID_ARG, "no active round");
   const int L = h->cfg.num_layers;
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
-  while (h->sched_next_sync < L) {
-    edit_status_t rc = sched_enqueue_next(h);
-    if (rc != EDIT_OK) return rc;
-  }
+  while (h->sched_next_sync < L) TRY(sched_enqueue_next(h));
   cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
   for (Lane& ln : h->lanes) {
     CUDA_TRY(h, cudaEventRecord(ln.tail, ln.stream));
@@ -1047,7 +1135,7 @@ edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream) {
 
 edit_status_t edit_sched_set_partition(edit_sync_t h, int32_t sms, int32_t full_units) {
   if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
-  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  TRY(check_err(h));
   if (h->sched_active) return fail(EDIT_ERR_INVALID_ARG, "a scheduled round is active");
   if (sms < 0 || sms > h->num_sms || full_units < 0)
     return fail(EDIT_ERR_INVALID_ARG, "sms must be in [0, #SMs], full_units >= 0");
@@ -1067,6 +1155,7 @@ edit_status_t edit_sched_set_partition(edit_sync_t h, int32_t sms, int32_t full_
     ln.stream = nullptr;
     CUDA_TRY(h, cudaStreamCreateWithPriority(&ln.stream, cudaStreamNonBlocking, prio));
   }
+  clear_graphs(h);  // captured rounds reference the old lane streams' work order
   h->sched_part = sms;
   h->sched_full_units = full_units;
   return EDIT_OK;
@@ -1074,19 +1163,12 @@ edit_status_t edit_sched_set_partition(edit_sync_t h, int32_t sms, int32_t full_
 
 edit_status_t edit_sync_stats(edit_sync_t h, int32_t layer, edit_layer_stats_t* out) {
   if (!h || !out) return fail(EDIT_ERR_INVALID_ARG, "null argument");
-  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  TRY(check_err(h));
   if (layer < 0 || layer >= h->cfg.num_layers) return fail(EDIT_ERR_INVALID_ARG, "layer out of range");
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   CUDA_TRY(h, cudaEventSynchronize(h->done[layer]));
+  TRY(check_err(h));  // an exchange of this (or an earlier) unit timed out
   for (Lane& ln : h->lanes) {
-    if (ln.xerr) {
-      int e = 0;
-      CUDA_TRY(h, cudaMemcpy(&e, ln.xerr, sizeof e, cudaMemcpyDeviceToHost));
-      if (e) {
-        h->poisoned = true;
-        return fail(EDIT_ERR_STATE, "device scalar exchange timed out (a peer rank stopped syncing)");
-      }
-    }
     if (!ln.global) continue;
     ncclResult_t async_err = ncclSuccess;
     NCCL_TRY(h, ncclCommGetAsyncError(ln.global, &async_err));
@@ -1101,7 +1183,7 @@ edit_status_t edit_sync_stats(edit_sync_t h, int32_t layer, edit_layer_stats_t* 
 
 edit_status_t edit_sync_get_state(edit_sync_t h, void* host_buf, size_t* bytes) {
   if (!h || !bytes) return fail(EDIT_ERR_INVALID_ARG, "null argument");
-  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  TRY(check_err(h));
   const size_t need = sizeof(edit_ema_t) * (size_t)h->cfg.num_layers * h->N;
   if (!host_buf || *bytes < need) {
     *bytes = need;
@@ -1116,7 +1198,7 @@ edit_status_t edit_sync_get_state(edit_sync_t h, void* host_buf, size_t* bytes) 
 
 edit_status_t edit_sync_set_state(edit_sync_t h, const void* host_buf, size_t bytes) {
   if (!h || !host_buf) return fail(EDIT_ERR_INVALID_ARG, "null argument");
-  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  TRY(check_err(h));
   const size_t need = sizeof(edit_ema_t) * (size_t)h->cfg.num_layers * h->N;
   if (bytes != need) return fail(EDIT_ERR_INVALID_ARG, "state size must be L*N*sizeof(edit_ema_t)");
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
@@ -1127,7 +1209,7 @@ edit_status_t edit_sync_set_state(edit_sync_t h, const void* host_buf, size_t by
 
 edit_status_t edit_sync_set_profiling(edit_sync_t h, int32_t enable) {
   if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
-  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  TRY(check_err(h));
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   if (enable && h->prof.empty()) {
     h->prof.assign((size_t)h->cfg.num_layers * (EDIT_NUM_PHASES + 1), nullptr);
@@ -1141,7 +1223,7 @@ edit_status_t edit_sync_set_profiling(edit_sync_t h, int32_t enable) {
 edit_status_t edit_sync_profile_collect(edit_sync_t h, double phase_ms[EDIT_NUM_PHASES], double busy_ms[EDIT_NUM_PHASES],
                                         int64_t* syncs, int64_t* elements) {
   if (!h || !phase_ms) return fail(EDIT_ERR_INVALID_ARG, "null argument");
-  if (h->poisoned) return fail(EDIT_ERR_STATE, "handle poisoned by an earlier CUDA/NCCL error");
+  TRY(check_err(h));
   for (int p = 0; p < EDIT_NUM_PHASES; ++p) phase_ms[p] = 0.0;
   int64_t elems = 0;
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
@@ -1202,22 +1284,40 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
   if (!h) return EDIT_OK;
   edit_status_t st = EDIT_OK;
   cudaSetDevice(h->cfg.device);
+  if (h->err_host && *reinterpret_cast<volatile int*>(h->err_host)) h->poisoned = true;
+  // (a poisoned handle may have exchange kernels spinning until their timeout: do not block)
   if (!h->poisoned) cudaDeviceSynchronize();
   // captured rounds first: a graph holding NCCL collectives references the communicators,
   // which must outlive it (the NCCL-exchange graph case once stalled in teardown with the
   // graphs destroyed after the comms)
-  for (RoundGraph& g : h->graphs)
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-  h->graphs.clear();
-  if ((h->peer || !h->reg_gather.empty() || h->dev_xchg) && h->ready && !h->poisoned && !h->lanes.empty() &&
-      h->lanes[0].global) {
-    // barrier: no member may free its IPC-exported buffers while a peer still reads them
-    double* tmpd = nullptr;
-    if (cudaMalloc(&tmpd, sizeof(double) * (h->K + 1)) == cudaSuccess) {
-      if (ncclAllGather(tmpd, tmpd + 1, 1, ncclFloat64, h->lanes[0].global, h->lanes[0].stream) != ncclSuccess)
-        st = EDIT_ERR_NCCL;
-      cudaStreamSynchronize(h->lanes[0].stream);
-      cudaFree(tmpd);
+  clear_graphs(h);
+  // (the simulated mesh's members are destroyed together after a device synchronize)
+  bool ipc_safe = true;
+  const bool exported = h->peer || !h->reg_gather.empty() || h->dev_xchg;
+  if (exported && h->K > 1 && !h->simulated) {
+    ipc_safe = false;
+    if (h->ready && !h->poisoned && !h->lanes.empty() && h->lanes[0].global) {
+      // barrier: no member may free its IPC-exported buffers while a peer still reads them.
+      // Device mailbox exchange, bounded (30 s or the exchange timeout if shorter): a rank
+      // unwinding after a peer died must not hang here
+      Lane& ln = h->lanes[0];
+      if (h->dev_xchg && ln.mailbox) {
+        XchgArgs x = xchg_args(h, ln, 2);
+        const unsigned long long cap = 30ull * 1000000000ull;
+        x.timeout_ns = (h->timeout_ns && h->timeout_ns < cap) ? h->timeout_ns : cap;
+        launch_xchg(x, ln.bar, ln.bar + 1, nullptr, ln.stream);
+        cudaStreamSynchronize(ln.stream);
+        int e = 0;
+        cudaMemcpy(&e, h->err_dev, sizeof e, cudaMemcpyDeviceToHost);
+        ipc_safe = e == 0;
+      } else {
+        double* tmpd = nullptr;
+        if (cudaMalloc(&tmpd, sizeof(double) * (h->K + 1)) == cudaSuccess) {
+          if (ncclAllGather(tmpd, tmpd + 1, 1, ncclFloat64, ln.global, ln.stream) != ncclSuccess) st = EDIT_ERR_NCCL;
+          ipc_safe = cudaStreamSynchronize(ln.stream) == cudaSuccess && st == EDIT_OK;
+          cudaFree(tmpd);
+        }
+      }
     }
   }
   for (void* p : h->reg_opened) cudaIpcCloseMemHandle(p);
@@ -1227,17 +1327,28 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
     for (size_t l = 0; l < ln.ops.size(); ++l)
       if (ln.sync) ncclRedOpDestroy(ln.ops[l], ln.sync);
     for (void* p : ln.opened) cudaIpcCloseMemHandle(p);
-    if (ln.Lown) cudaFree(ln.Lown);
-    if (ln.Down) cudaFree(ln.Down);
+    // IPC-exported buffers a peer may still be reading (no completed barrier): leaked, not
+    // freed -- freeing them could fault the peers' GPUs
+    if (ipc_safe) {
+      if (ln.Lown) cudaFree(ln.Lown);
+      if (ln.Down) cudaFree(ln.Down);
+      if (ln.mailbox) cudaFree(ln.mailbox);
+    }
     if (ln.S) cudaFree(ln.S);
-    if (ln.mailbox) cudaFree(ln.mailbox);
     if (ln.dseq) cudaFree(ln.dseq);
-    if (ln.xerr) cudaFree(ln.xerr);
-    if (ln.shard) ncclCommDestroy(ln.shard);
-    if (ln.sync) ncclCommDestroy(ln.sync);
-    if (ln.global) ncclCommDestroy(ln.global);
+    if (ln.bar) cudaFree(ln.bar);
+    // a poisoned handle's communicators may have collectives that never complete: abort them
+    auto drop = [&](ncclComm_t c) {
+      if (!c) return;
+      if (h->poisoned) ncclCommAbort(c);
+      else ncclCommDestroy(c);
+    };
+    drop(ln.shard);
+    drop(ln.sync);
+    drop(ln.global);
     if (ln.tail) cudaEventDestroy(ln.tail);
-    if (ln.stream) cudaStreamDestroy(ln.stream);
+    if (ln.last) cudaEventDestroy(ln.last);
+    if (ln.stream && !h->poisoned) cudaStreamDestroy(ln.stream);
   }
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   if (h->fork) cudaEventDestroy(h->fork);
@@ -1256,6 +1367,10 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
   if (h->h2d) cudaStreamDestroy(h->h2d);
   if (h->d2h) cudaStreamDestroy(h->d2h);
   if (h->staging) cudaFree(h->staging);
+  if (!h->poisoned) {
+    if (h->err_dev) cudaFree(h->err_dev);
+    if (h->err_host) cudaFreeHost(h->err_host);
+  }
   delete h;
   return st;
 }

@@ -232,9 +232,10 @@ __device__ double block_sum_n(double v) {
 __device__ __forceinline__ double block_sum(double v) { return block_sum_n<kThreads>(v); }
 
 // Writes this CTA's partial; the last CTA to finish adds all partials in index order
-// (fp64) and stores the total in *out, then re-arms the ticket counter.
+// (fp64) and stores the total in *out, then re-arms the ticket counter.  Returns (in every
+// thread of the CTA) whether this CTA was the last one; *out is then visible to the whole CTA.
 template <int NT>
-__device__ void finish_partials_n(double cta_total, double* cta_parts, uint32_t* counter, double* out) {
+__device__ bool finish_partials_n(double cta_total, double* cta_parts, uint32_t* counter, double* out) {
   __shared__ bool is_last;
   if (threadIdx.x == 0) {
     cta_parts[blockIdx.x] = cta_total;
@@ -242,7 +243,7 @@ __device__ void finish_partials_n(double cta_total, double* cta_parts, uint32_t*
     is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (!is_last) return;
+  if (!is_last) return false;
   __threadfence();
   // thread t adds partials t, t+NT, t+2NT, ... in that order; 8 loads in flight per step
   const int G = (int)gridDim.x;
@@ -261,10 +262,93 @@ __device__ void finish_partials_n(double cta_total, double* cta_parts, uint32_t*
     *out = v;
     *counter = 0u;
   }
+  __syncthreads();
+  return true;
 }
-__device__ __forceinline__ void finish_partials(double cta_total, double* cta_parts, uint32_t* counter,
+__device__ __forceinline__ bool finish_partials(double cta_total, double* cta_parts, uint32_t* counter,
                                                 double* out) {
-  finish_partials_n<kThreads>(cta_total, cta_parts, counter, out);
+  return finish_partials_n<kThreads>(cta_total, cta_parts, counter, out);
+}
+
+// ---------------------------------------------------------------- scalar exchange (mailboxes)
+// Called by every thread of ONE CTA (>= K threads): threads t < K store *src's value into rank
+// t's mailbox (value, then the sequence number with st.release.sys), then wait for sender t
+// in this rank's own mailbox (ld.acquire.sys) and write out[t].  Slots alternate by sequence
+// parity: a rank can only write seq+2 into a slot after the reader published seq+1, i.e.
+// after it finished reading seq -- no slot is overwritten early.  Returns false (in every
+// thread) if the handle already had an error or this wait timed out (the error is then set).
+static __device__ __noinline__ bool xchg_body(const XchgArgs& x, const double* src, double* out) {
+  __shared__ unsigned long long s_seq;
+  __shared__ int s_ok;
+  const int t = threadIdx.x;
+  if (t == 0) {
+    s_ok = *reinterpret_cast<volatile int*>(x.err) == 0;
+    unsigned long long seq = x.seq;
+    if (x.dseq) {
+      seq = x.dseq[x.phase] + 1;
+      x.dseq[x.phase] = seq;
+    }
+    s_seq = seq;
+  }
+  __syncthreads();
+  if (!s_ok) return false;  // silent after an earlier error of this handle
+  const unsigned long long seq = s_seq;
+  const int K = x.K, me = x.me;
+  const int base = (x.phase * 2 + (int)(seq & 1)) * K;
+  if (t < K) {
+    const double v = *src;
+    unsigned long long* slot = x.mp.box[t] + 2 * (base + me);
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(slot), "l"((unsigned long long)__double_as_longlong(v))
+                 : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot + 1), "l"(seq) : "memory");
+  }
+  __syncthreads();  // (all publishes issued before anyone may leave on a timeout)
+  if (t < K) {
+    unsigned long long* slot = x.mp.box[me] + 2 * (base + t);
+    unsigned long long s = 0, t0, now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    bool ok = true;
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(s) : "l"(slot + 1) : "memory");
+      if (s == seq) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (x.timeout_ns && now - t0 > x.timeout_ns) {  // a peer stopped syncing: fatal
+        ok = false;
+        break;
+      }
+    }
+    if (ok) {
+      unsigned long long vb;
+      asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(vb) : "l"(slot) : "memory");
+      out[t] = __longlong_as_double((long long)vb);
+    } else {
+      atomicExch(x.err, 1);
+      if (x.err_host) {
+        *reinterpret_cast<volatile int*>(x.err_host) = 1;
+        __threadfence_system();
+      }
+      s_ok = 0;
+    }
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+// K1's last CTA (after finish_partials): the phase-0 exchange of the module-norm partials
+// (K > 1), then K2 on the gathered values -- what xchg_kernel + decide_kernel do as two
+// launches.  An exchange failure leaves the EMA untouched and aborts the unit (kAbort).
+static __device__ __forceinline__ void fold_norm_decide(const FoldArgs& f, LayerScratch* scr) {
+  bool ok = true;
+  if (f.x.K > 1) ok = xchg_body(f.x, &scr->send1, scr->recv1);
+  if (threadIdx.x == 0) {
+    if (ok) decide_body(f.dec);
+    else scr->rollback = kAbort;
+  }
+}
+// RS's last CTA: the phase-1 exchange of the ||Dbar slice||^2 partials (every rank's).
+static __device__ __forceinline__ void fold_dbar_norm(const FoldArgs& f, LayerScratch* scr) {
+  const bool ok = xchg_body(f.x, &scr->send2, scr->recv2);
+  if (!ok && threadIdx.x == 0) scr->rollback = kAbort;
 }
 
 // ---------------------------------------------------------------- mbarrier + TMA (sm_90+/sm_100a)

@@ -108,52 +108,78 @@ inline Slicing slicing_of(int64_t n, int N, int me, int tile = kPeerTileVec) {
 }
 
 // Device-side scalar exchange over NVLink (replaces the tiny NCCL all-gathers of the scalar
-// chain): every rank's mailbox, mapped in every rank through CUDA IPC.
+// chain): every rank's mailbox, mapped in every rank through CUDA IPC (or, in the single-GPU
+// simulated mesh of tests/sim, plain device pointers of the other members' mailboxes).
 // Slot layout: box[((phase * 2 + (seq & 1)) * K + src) * 2 + {0: value bits, 1: seq}].
-constexpr int kXchgPhases = 2;
+// Phases: 0 = module norms (fused into K1), 1 = ||Dbar|| partials (fused into RS),
+// 2 = barriers (fused shard all-gather, warm-up all-reduce).
+constexpr int kXchgPhases = 3;
 struct MailPtrs {
   unsigned long long* box[kMaxRanks];
 };
 inline size_t mailbox_bytes(int K) { return sizeof(unsigned long long) * 2 * 2 * kXchgPhases * (size_t)K; }
-// out[r] = rank r's *src for r < K.  One CTA; spins (bounded: ~10 s, then *err = 1) only in
-// this kernel, never in the big streaming kernels -> no cross-lane starvation.
-// dec != nullptr: K2 (decide) runs in the same kernel right after the gather.
-// dseq != nullptr: seq comes from (and advances) the lane's device counter dseq[phase]
-// (graph-replayable); else the host-passed seq.
-int launch_xchg(const MailPtrs& mp, int K, int me, int phase, unsigned long long seq, const double* src,
-                double* out, int* err, cudaStream_t st, const DecideArgs* dec = nullptr,
-                unsigned long long* dseq = nullptr);
+
+// One exchange of one fp64 per rank: publish to every rank's mailbox, wait for all K.
+//  seq:  host-passed sequence number (dseq == nullptr), else the lane's device counter
+//        dseq[phase] is advanced by the exchanging CTA (graph-replayable).
+//  err:  the handle's sticky device error flag.  A wait longer than timeout_ns (0 = forever)
+//        sets it (and *err_host, mapped host memory the library polls at every call); once
+//        set, every later exchange of the handle returns at once without publishing, and the
+//        unit's data kernels skip all writes (LayerScratch::rollback = kAbort).  So a peer that
+//        stops syncing poisons every rank instead of letting them apply stale data.
+struct XchgArgs {
+  MailPtrs mp;
+  int32_t K, me, phase;
+  unsigned long long seq;
+  unsigned long long* dseq;
+  int* err;
+  int* err_host;
+  unsigned long long timeout_ns;
+};
+constexpr int32_t kAbort = 2;  // LayerScratch::rollback value: skip the unit entirely
+
+// K1 / RS fold: the kernel's last CTA (the one adding the per-CTA partials) runs the exchange
+// of its result (and, for K1, K2 right after) -- one dependent launch fewer per exchange.
+//  K1: K == 1 -> K2 on the own partial; K > 1 -> exchange phase 0 into recv1, then K2.
+//  RS: exchange phase 1 of send2 into recv2.
+struct FoldArgs {
+  XchgArgs x;
+  DecideArgs dec;
+  int32_t on;       // 0: no fold (NCCL scalar gathers), 1: fold
+};
+
+int launch_xchg(const XchgArgs& x, const double* src, double* out, int32_t* rollback, cudaStream_t st,
+                const DecideArgs* dec = nullptr);
 
 // Launchers (kernels.cu).  Each returns the number of kernels launched.
 // cta_parts: grid_of(n, kVecReduce) fp64 slots for the per-CTA partials.
-// ef: stream with an L2 evict_first policy (device_common.cuh).  cap > 0: at most `cap` CTAs
-// (grid-stride over chunks) -- the co-resident mode next to a forward's GEMMs.
+// cap > 0: at most `cap` CTAs (grid-stride over chunks) -- the co-resident mode next to a
+// forward's GEMMs.
 int launch_pg_norm(int dtype, const void* local, const float* anchor, float* S, int64_t n,
-                   LayerScratch* scr, double* cta_parts, bool ef, int cap, cudaStream_t st);
-int launch_sumsq(const float* x, int64_t n, LayerScratch* scr, double* cta_parts, bool ef, int cap,
-                 cudaStream_t st);
+                   LayerScratch* scr, double* cta_parts, int cap, const FoldArgs& f, cudaStream_t st);
+int launch_sumsq(const float* x, int64_t n, LayerScratch* scr, double* cta_parts, int cap, cudaStream_t st);
 int launch_decide(const DecideArgs& a, cudaStream_t st);
 // K1 variant for the peer-memory path: also copies the local into this rank's staging L.
 int launch_pg_norm_copy(int dtype, const void* local, const float* anchor, void* Lcopy, int64_t n,
-                        LayerScratch* scr, double* cta_parts, bool ef, int cap, cudaStream_t st);
+                        LayerScratch* scr, double* cta_parts, int cap, const FoldArgs& f, cudaStream_t st);
 // RS (peer_kernels.cu): Dbar = sum_j w_j (anchor - L_j) over this rank's slice, written to its D;
 // ||Dbar_slice||^2 -> scr->send2 (persistent grid <= max_ctas; cta_parts needs that many slots).
 // smem_kb > 0: shared-memory ring budget per CTA (tiles shrink to fit; co-resident mode).
 int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anchor, float* Dmine,
-              LayerScratch* scr, double* cta_parts, int max_ctas, bool ef, int smem_kb, cudaStream_t st);
+              LayerScratch* scr, double* cta_parts, int max_ctas, int smem_kb, const FoldArgs& f, cudaStream_t st);
 // AG + update: Dbar pulled from each slice's owner, then the K4 math on the whole shard.
 int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl, int max_ctas,
-                     bool ef, int smem_kb, cudaStream_t st);
+                     int smem_kb, cudaStream_t st);
 // Partition mode of the prefetch scheduler (peer_kernels.cu): K1 (no S, no copy) and the
 // N == 1 K4 as persistent TMA pipelines on <= max_ctas CTAs, each with the full ~200 KB
 // ring (one CTA per SM, no GEMM CTA beside it).
 int launch_pg_norm_tma(int dtype, const void* local, const float* anchor, int64_t n, LayerScratch* scr,
-                       double* cta_parts, int max_ctas, cudaStream_t st);
+                       double* cta_parts, int max_ctas, const FoldArgs& f, cudaStream_t st);
 int launch_update_tma(int dtype, const UpdateArgs& a, int max_ctas, cudaStream_t st);
 inline int64_t rs_partial_slots(int64_t, int) { return kMaxPeerCtas; }
 // Warm-up gradient all-reduce (mean) over the sync row, peer path (peer_kernels.cu).
-int launch_warm_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, void* Dmine, cudaStream_t st);
-int launch_warm_ag(int dtype, const PeerPtrs& pp, const Slicing& sl, void* out, cudaStream_t st);
-int launch_update(int dtype, const UpdateArgs& a, bool ef, int cap, cudaStream_t st);
+int launch_warm_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, void* Dmine, const int* err, cudaStream_t st);
+int launch_warm_ag(int dtype, const PeerPtrs& pp, const Slicing& sl, void* out, const int* err, cudaStream_t st);
+int launch_update(int dtype, const UpdateArgs& a, int cap, cudaStream_t st);
 
 }  // namespace edit

@@ -28,16 +28,17 @@ using namespace dev;
 // Shape: CTA b owns vectors [b*T*U*I, (b+1)*T*U*I); a thread walks I steps of U vectors
 // (stride T), issuing the U vectors' loads before any arithmetic.
 // kCopy: also store the local unchanged into Lcopy (the peer-memory path's staging buffer).
-template <typename T, bool kWriteS, int U, int I, bool kCopy = false, bool kEF = false>
+// f.on: the last CTA also runs the norm exchange (K > 1) and K2 (fold_norm_decide).
+template <typename T, bool kWriteS, int U, int I, bool kCopy = false>
 __global__ void __launch_bounds__(kThreads) pg_norm_kernel(const T* __restrict__ local,
                                                            const float* __restrict__ anchor,
                                                            float* __restrict__ S, int64_t n,
                                                            LayerScratch* __restrict__ scr,
                                                            double* __restrict__ cta_parts,
-                                                           T* __restrict__ Lcopy = nullptr) {
+                                                           T* __restrict__ Lcopy,
+                                                           const __grid_constant__ FoldArgs f) {
   const int64_t n8 = n >> 3;
   const int64_t nchunks = (n8 + kThreads * U * I - 1) / (kThreads * U * I);
-  const uint64_t pol = kEF ? l2_evict_first_policy() : 0;
   float acc = 0.f;
   // one chunk per CTA with the full grid; grid-stride over chunks when the grid is capped
   // (the scheduler's co-resident mode, 1 CTA per SM)
@@ -51,15 +52,15 @@ __global__ void __launch_bounds__(kThreads) pg_norm_kernel(const T* __restrict__
     for (int u = 0; u < U; ++u) {
       const int64_t i = base + (int64_t)u * kThreads;
       if (i < n8) {
-        load8<kEF>(local + 8 * i, l[u], pol);
-        load8<kEF>(anchor + 8 * i, a[u], pol);
+        load8(local + 8 * i, l[u]);
+        load8(anchor + 8 * i, a[u]);
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = base + (int64_t)u * kThreads;
       if (i < n8) {
-        if (kCopy) store8<kEF>(Lcopy + 8 * i, l[u], pol);  // exact: bf16 -> f32 -> bf16 round-trips
+        if (kCopy) store8(Lcopy + 8 * i, l[u]);  // exact: bf16 -> f32 -> bf16 round-trips
         float d[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -69,7 +70,7 @@ __global__ void __launch_bounds__(kThreads) pg_norm_kernel(const T* __restrict__
         if (kWriteS) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) d[j] = isfinite(d[j]) ? d[j] : 0.f;  // R9: w = 0 must give 0
-          store8<kEF>(S + 8 * i, d, pol);
+          store8(S + 8 * i, d);
         }
       }
     }
@@ -85,18 +86,17 @@ __global__ void __launch_bounds__(kThreads) pg_norm_kernel(const T* __restrict__
     if (kCopy) store1(Lcopy + k, lk);
   }
   accd = block_sum(accd);
-  finish_partials(accd, cta_parts, &scr->counter1, &scr->send1);
+  if (finish_partials(accd, cta_parts, &scr->counter1, &scr->send1) && f.on) fold_norm_decide(f, scr);
 }
 
 // ---------------------------------------------------------------- K3
 // Eq. 4: partial ||Dbar||^2 of this shard of the all-reduced pseudo-gradient.
-template <int U, int I, bool kEF = false>
+template <int U, int I>
 __global__ void __launch_bounds__(kThreads) sumsq_kernel(const float* __restrict__ x, int64_t n,
                                                          LayerScratch* __restrict__ scr,
                                                          double* __restrict__ cta_parts) {
   const int64_t n8 = n >> 3;
   const int64_t nchunks = (n8 + kThreads * U * I - 1) / (kThreads * U * I);
-  const uint64_t pol = kEF ? l2_evict_first_policy() : 0;
   float acc = 0.f;
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
   const int64_t cta0 = c * kThreads * U * I + threadIdx.x;
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kThreads) sumsq_kernel(const float* __restrict
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = base + (int64_t)u * kThreads;
-      if (i < n8) load8<kEF>(x + 8 * i, v[u], pol);
+      if (i < n8) load8(x + 8 * i, v[u]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -140,7 +140,7 @@ __global__ void decide_kernel(DecideArgs p) {
 // ---------------------------------------------------------------- K4
 // beta (Eq. 4), then OuterOpt = Nesterov (R2) on (anchor, momentum) and the
 // write-back local = rne(anchor) (Alg. 2 l.454-455).  Rollback: local = rne(anchor).
-template <typename T, bool kFromS, int U, int I, bool kEF = false, bool kG = false>
+template <typename T, bool kFromS, int U, int I, bool kG = false>
 __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
   T* __restrict__ local = static_cast<T*>(p.local);
   float* __restrict__ anchor = p.anchor;
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
     beta_d = beta_d < 1.0 ? beta_d : 1.0;
     if (p.flags & EDIT_NO_GC) beta_d = 1.0;
     const int rb = *p.rollback;
-    if (blockIdx.x == 0) {
+    if (blockIdx.x == 0 && rb != kAbort) {
       p.rec->G_bar = rb ? 0.0 : gbar;
       p.rec->beta = rb ? 1.0 : beta_d;
       p.rec->rollback = rb;
@@ -166,8 +166,8 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
     s_rollback = rb;
   }
   __syncthreads();
+  if (s_rollback == kAbort) return;  // the unit's exchange failed: no write at all
   const float beta = s_beta, mu = p.mu, nu = p.nu;
-  const uint64_t pol = kEF ? l2_evict_first_policy() : 0;
   const int64_t n8 = p.n >> 3;
   const int64_t nchunks = (n8 + kThreads * U * I - 1) / (kThreads * U * I);
   const bool tail = blockIdx.x == 0 && threadIdx.x < (p.n & 7);
@@ -181,9 +181,9 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
         const int64_t i = cta0 + (int64_t)(it * U + u) * kThreads;
         if (i < n8) {
           float a[8];
-          load8<kEF>(anchor + 8 * i, a, pol);
-          store8<kEF>(local + 8 * i, a, pol);
-          if (kG) gather_store8_t<kEF, T>(p, 8 * i, a, pol);
+          load8(anchor + 8 * i, a);
+          store8(local + 8 * i, a);
+          if (kG) gather_store8_t<false, T>(p, 8 * i, a, 0);
         }
       }
     }
@@ -207,12 +207,12 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
       const int64_t i = base + (int64_t)u * kThreads;
       if (i < n8) {
         if (kFromS) {
-          load8<kEF>(dbar + 8 * i, d[u], pol);
+          load8(dbar + 8 * i, d[u]);
         } else {
-          load8<kEF>(local + 8 * i, d[u], pol);  // the local; Delta formed below
+          load8(local + 8 * i, d[u]);  // the local; Delta formed below
         }
-        load8<kEF>(anchor + 8 * i, a[u], pol);
-        load8<kEF>(mom + 8 * i, m[u], pol);
+        load8(anchor + 8 * i, a[u]);
+        load8(mom + 8 * i, m[u]);
       }
     }
 #pragma unroll
@@ -226,10 +226,10 @@ __global__ void __launch_bounds__(kThreads) outer_update_kernel(UpdateArgs p) {
           m[u][j] = fmaf(mu, m[u][j], g);               // m' = mu m + g
           a[u][j] = a[u][j] - nu * fmaf(mu, m[u][j], g);  // a' = a - nu (g + mu m')
         }
-        store8<kEF>(mom + 8 * i, m[u], pol);
-        store8<kEF>(anchor + 8 * i, a[u], pol);
-        store8<kEF>(local + 8 * i, a[u], pol);
-        if (kG) gather_store8_t<kEF, T>(p, 8 * i, a[u], pol);
+        store8(mom + 8 * i, m[u]);
+        store8(anchor + 8 * i, a[u]);
+        store8(local + 8 * i, a[u]);
+        if (kG) gather_store8_t<false, T>(p, 8 * i, a[u], 0);
       }
     }
   }
@@ -255,44 +255,38 @@ constexpr int kRedU = kReduceShape[0], kRedI = kReduceShape[1];
 constexpr int kUpdU = kUpdateShape[0], kUpdI = kUpdateShape[1];
 
 template <typename T, bool kWriteS, bool kCopy>
-void pg_norm_ef(bool ef, unsigned grid, cudaStream_t st, const void* local, const float* anchor, float* S, int64_t n,
-                LayerScratch* scr, double* cta_parts, void* Lcopy) {
-  if (ef)
-    pg_norm_kernel<T, kWriteS, kRedU, kRedI, kCopy, true><<<grid, kThreads, 0, st>>>(
-        static_cast<const T*>(local), anchor, S, n, scr, cta_parts, static_cast<T*>(Lcopy));
-  else
-    pg_norm_kernel<T, kWriteS, kRedU, kRedI, kCopy, false><<<grid, kThreads, 0, st>>>(
-        static_cast<const T*>(local), anchor, S, n, scr, cta_parts, static_cast<T*>(Lcopy));
+void pg_norm_go(unsigned grid, cudaStream_t st, const void* local, const float* anchor, float* S, int64_t n,
+                LayerScratch* scr, double* cta_parts, void* Lcopy, const FoldArgs& f) {
+  pg_norm_kernel<T, kWriteS, kRedU, kRedI, kCopy><<<grid, kThreads, 0, st>>>(
+      static_cast<const T*>(local), anchor, S, n, scr, cta_parts, static_cast<T*>(Lcopy), f);
 }
 
 static unsigned capped(int64_t g, int cap) { return (unsigned)(cap > 0 && g > cap ? cap : g); }
 
 int launch_pg_norm(int dtype, const void* local, const float* anchor, float* S, int64_t n,
-                   LayerScratch* scr, double* cta_parts, bool ef, int cap, cudaStream_t st) {
+                   LayerScratch* scr, double* cta_parts, int cap, const FoldArgs& f, cudaStream_t st) {
   const unsigned grid = capped(grid_of(n, kRedU * kRedI), cap);
   if (dtype == EDIT_BF16) {
-    if (S) pg_norm_ef<__nv_bfloat16, true, false>(ef, grid, st, local, anchor, S, n, scr, cta_parts, nullptr);
-    else pg_norm_ef<__nv_bfloat16, false, false>(ef, grid, st, local, anchor, S, n, scr, cta_parts, nullptr);
+    if (S) pg_norm_go<__nv_bfloat16, true, false>(grid, st, local, anchor, S, n, scr, cta_parts, nullptr, f);
+    else pg_norm_go<__nv_bfloat16, false, false>(grid, st, local, anchor, S, n, scr, cta_parts, nullptr, f);
   } else {
-    if (S) pg_norm_ef<float, true, false>(ef, grid, st, local, anchor, S, n, scr, cta_parts, nullptr);
-    else pg_norm_ef<float, false, false>(ef, grid, st, local, anchor, S, n, scr, cta_parts, nullptr);
+    if (S) pg_norm_go<float, true, false>(grid, st, local, anchor, S, n, scr, cta_parts, nullptr, f);
+    else pg_norm_go<float, false, false>(grid, st, local, anchor, S, n, scr, cta_parts, nullptr, f);
   }
   return 1;
 }
 
 int launch_pg_norm_copy(int dtype, const void* local, const float* anchor, void* Lcopy, int64_t n,
-                        LayerScratch* scr, double* cta_parts, bool ef, int cap, cudaStream_t st) {
+                        LayerScratch* scr, double* cta_parts, int cap, const FoldArgs& f, cudaStream_t st) {
   const unsigned grid = capped(grid_of(n, kRedU * kRedI), cap);
-  if (dtype == EDIT_BF16) pg_norm_ef<__nv_bfloat16, false, true>(ef, grid, st, local, anchor, nullptr, n, scr, cta_parts, Lcopy);
-  else pg_norm_ef<float, false, true>(ef, grid, st, local, anchor, nullptr, n, scr, cta_parts, Lcopy);
+  if (dtype == EDIT_BF16) pg_norm_go<__nv_bfloat16, false, true>(grid, st, local, anchor, nullptr, n, scr, cta_parts, Lcopy, f);
+  else pg_norm_go<float, false, true>(grid, st, local, anchor, nullptr, n, scr, cta_parts, Lcopy, f);
   return 1;
 }
 
-int launch_sumsq(const float* x, int64_t n, LayerScratch* scr, double* cta_parts, bool ef, int cap,
-                 cudaStream_t st) {
+int launch_sumsq(const float* x, int64_t n, LayerScratch* scr, double* cta_parts, int cap, cudaStream_t st) {
   const unsigned grid = capped(grid_of(n, kRedU * kRedI), cap);
-  if (ef) sumsq_kernel<kRedU, kRedI, true><<<grid, kThreads, 0, st>>>(x, n, scr, cta_parts);
-  else sumsq_kernel<kRedU, kRedI, false><<<grid, kThreads, 0, st>>>(x, n, scr, cta_parts);
+  sumsq_kernel<kRedU, kRedI><<<grid, kThreads, 0, st>>>(x, n, scr, cta_parts);
   return 1;
 }
 
@@ -302,22 +296,21 @@ int launch_decide(const DecideArgs& a, cudaStream_t st) {
 }
 
 template <typename T, bool kFromS>
-void update_ef(bool ef, unsigned grid, cudaStream_t st, const UpdateArgs& a) {
-  const bool g = a.gather_M > 0;  // NEXT-2 stores compiled only into the gathering variants
-  if (ef && g) outer_update_kernel<T, kFromS, kUpdU, kUpdI, true, true><<<grid, kThreads, 0, st>>>(a);
-  else if (ef) outer_update_kernel<T, kFromS, kUpdU, kUpdI, true, false><<<grid, kThreads, 0, st>>>(a);
-  else if (g) outer_update_kernel<T, kFromS, kUpdU, kUpdI, false, true><<<grid, kThreads, 0, st>>>(a);
-  else outer_update_kernel<T, kFromS, kUpdU, kUpdI, false, false><<<grid, kThreads, 0, st>>>(a);
+void update_go(unsigned grid, cudaStream_t st, const UpdateArgs& a) {
+  if (a.gather_M > 0)  // NEXT-2 stores compiled only into the gathering variant
+    outer_update_kernel<T, kFromS, kUpdU, kUpdI, true><<<grid, kThreads, 0, st>>>(a);
+  else
+    outer_update_kernel<T, kFromS, kUpdU, kUpdI, false><<<grid, kThreads, 0, st>>>(a);
 }
 
-int launch_update(int dtype, const UpdateArgs& a, bool ef, int cap, cudaStream_t st) {
+int launch_update(int dtype, const UpdateArgs& a, int cap, cudaStream_t st) {
   const unsigned grid = capped(grid_of(a.n, kUpdU * kUpdI), cap);
   if (dtype == EDIT_BF16) {
-    if (a.dbar) update_ef<__nv_bfloat16, true>(ef, grid, st, a);
-    else update_ef<__nv_bfloat16, false>(ef, grid, st, a);
+    if (a.dbar) update_go<__nv_bfloat16, true>(grid, st, a);
+    else update_go<__nv_bfloat16, false>(grid, st, a);
   } else {
-    if (a.dbar) update_ef<float, true>(ef, grid, st, a);
-    else update_ef<float, false>(ef, grid, st, a);
+    if (a.dbar) update_go<float, true>(grid, st, a);
+    else update_go<float, false>(grid, st, a);
   }
   return 1;
 }

@@ -54,12 +54,13 @@ __device__ __forceinline__ void ring_init(RingBars* b, int K) {
 }
 
 // ------------------------------------------------------------------------------ RS
-template <typename T, bool kEF>
+template <typename T>
 __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_constant__ PeerPtrs pp, Slicing sl,
                                                               const float* __restrict__ anchor,
                                                               float* __restrict__ Dmine,
                                                               LayerScratch* __restrict__ scr,
-                                                              double* __restrict__ cta_parts, int K, int V) {
+                                                              double* __restrict__ cta_parts, int K, int V,
+                                                              const __grid_constant__ FoldArgs f) {
   extern __shared__ __align__(128) char smem[];
   __shared__ RingBars bars;
   const int N = sl.N;
@@ -71,8 +72,7 @@ __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_const
     nact += (j < N && w[j] != 0.f) ? 1 : 0;
   }
   const int lbytes = (int)sizeof(T);
-  const bool skip = scr->rollback != 0;
-  const uint64_t pol = kEF ? l2_evict_first_policy() : 0;
+  const bool skip = scr->rollback != 0;  // rollback (l.449) or an aborted unit
   const int64_t n8 = sl.n >> 3;
   const int64_t s0 = (int64_t)sl.me * sl.slice;                       // first vector of my slice
   const int64_t s1 = min(s0 + sl.slice, n8);                           // end (full vectors only)
@@ -93,11 +93,11 @@ __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_const
           const int nv = (int)min((int64_t)V, s1 - v0);
           char* st = smem + (size_t)s * stage_bytes;
           mbar_arrive_expect_tx(&bars.full[s], (uint32_t)(nv * 8 * (4 + nact * lbytes)));
-          tma_load_1d<kEF>(st, anchor + 8 * v0, nv * 32, &bars.full[s], pol);
+          tma_load_1d(st, anchor + 8 * v0, nv * 32, &bars.full[s]);
           for (int j = 0; j < N; ++j) {
             if (w[j] == 0.f) continue;
-            tma_load_1d<kEF>(st + V * 32 + j * V * 8 * lbytes, static_cast<const T*>(pp.L[j]) + 8 * v0,
-                             (uint32_t)(nv * 8 * lbytes), &bars.full[s], pol);
+            tma_load_1d(st + V * 32 + j * V * 8 * lbytes, static_cast<const T*>(pp.L[j]) + 8 * v0,
+                        (uint32_t)(nv * 8 * lbytes), &bars.full[s]);
           }
         }
       }
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_const
           }
 #pragma unroll
           for (int k = 0; k < 4; ++k) acc = fmaf(d[k], d[k], acc);
-          store4<kEF>(Dmine + 8 * (v0 - s0) + 4 * v, d, pol);
+          store4(Dmine + 8 * (v0 - s0) + 4 * v, d);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.empty[s]);
@@ -146,11 +146,13 @@ __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_const
     Dmine[k - 8 * s0] = d;
   }
   accd = block_sum_n<kPeerThreads>(accd);
-  finish_partials_n<kPeerThreads>(accd, cta_parts, &scr->counter2, &scr->send2);
+  // the last CTA: ||Dbar||^2 partials of every rank (module level, Eq. 4), also the barrier
+  // after which every member's D slice is complete
+  if (finish_partials_n<kPeerThreads>(accd, cta_parts, &scr->counter2, &scr->send2) && f.on) fold_dbar_norm(f, scr);
 }
 
 // ------------------------------------------------------------------------------ AG + update
-template <typename T, bool kEF, bool kG>
+template <typename T, bool kG>
 __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs p,
                                                                      const __grid_constant__ PeerPtrs pp,
                                                                      Slicing sl, int K, int V) {
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
     beta_d = beta_d < 1.0 ? beta_d : 1.0;
     if (p.flags & EDIT_NO_GC) beta_d = 1.0;
     const int rb = *p.rollback;
-    if (blockIdx.x == 0) {
+    if (blockIdx.x == 0 && rb != kAbort) {
       p.rec->G_bar = rb ? 0.0 : gbar;
       p.rec->beta = rb ? 1.0 : beta_d;
       p.rec->rollback = rb;
@@ -179,8 +181,8 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
     s_rollback = rb;
   }
   ring_init(&bars, K);  // (contains __syncthreads)
+  if (s_rollback == kAbort) return;  // the unit's exchange failed: no write at all
   const float beta = s_beta, mu = p.mu, nu = p.nu;
-  const uint64_t pol = kEF ? l2_evict_first_policy() : 0;
   const int64_t n8 = p.n >> 3;
   const int N = sl.N;
   const int64_t tps = sl.slice / V;                      // tiles per slice (slices are tile-aligned)
@@ -198,9 +200,9 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += stride) {
       float a[8];
-      load8<kEF>(anchor + 8 * i, a, pol);
-      store8<kEF>(local + 8 * i, a, pol);
-      if (kG) gather_store8_t<kEF, T>(p, 8 * i, a, pol);
+      load8(anchor + 8 * i, a);
+      store8(local + 8 * i, a);
+      if (kG) gather_store8_t<false, T>(p, 8 * i, a, 0);
     }
     if (blockIdx.x == 0 && threadIdx.x < (p.n & 7)) {
       const int64_t k = 8 * n8 + threadIdx.x;
@@ -221,9 +223,9 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
         if (use > 0) mbar_wait(&bars.empty[s], (use - 1) & 1);
         char* st = smem + (size_t)s * stage_bytes;
         mbar_arrive_expect_tx(&bars.full[s], (uint32_t)(nv * 96));
-        tma_load_1d<kEF>(st, pp.D[owner] + 8 * (v0 - owner * sl.slice), nv * 32, &bars.full[s], pol);
-        tma_load_1d<kEF>(st + V * 32, anchor + 8 * v0, nv * 32, &bars.full[s], pol);
-        tma_load_1d<kEF>(st + V * 64, mom + 8 * v0, nv * 32, &bars.full[s], pol);
+        tma_load_1d(st, pp.D[owner] + 8 * (v0 - owner * sl.slice), nv * 32, &bars.full[s]);
+        tma_load_1d(st + V * 32, anchor + 8 * v0, nv * 32, &bars.full[s]);
+        tma_load_1d(st + V * 64, mom + 8 * v0, nv * 32, &bars.full[s]);
         ++it;
       }
     }
@@ -253,10 +255,10 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
           a[k] = a[k] - nu * fmaf(mu, m[k], g);       // a' = a - nu (g + mu m')
         }
         const int64_t i = 8 * v0 + 4 * v;             // first element of the unit
-        store4<kEF>(mom + i, m, pol);
-        store4<kEF>(anchor + i, a, pol);
-        store4<kEF>(local + i, a, pol);
-        if (kG) gather_store4_t<kEF, T>(p, i, a, pol);
+        store4(mom + i, m);
+        store4(anchor + i, a);
+        store4(local + i, a);
+        if (kG) gather_store4_t<false, T>(p, i, a, 0);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.empty[s]);
@@ -291,7 +293,8 @@ template <typename T>
 __global__ void __launch_bounds__(kPeerThreads) pg_norm_tma_kernel(const T* __restrict__ local,
                                                                    const float* __restrict__ anchor, int64_t n,
                                                                    LayerScratch* __restrict__ scr,
-                                                                   double* __restrict__ cta_parts, int K, int V) {
+                                                                   double* __restrict__ cta_parts, int K, int V,
+                                                                   const __grid_constant__ FoldArgs f) {
   extern __shared__ __align__(128) char smem[];
   __shared__ RingBars bars;
   const int lbytes = (int)sizeof(T);
@@ -344,7 +347,7 @@ __global__ void __launch_bounds__(kPeerThreads) pg_norm_tma_kernel(const T* __re
     accd += (double)(d * d);
   }
   accd = block_sum_n<kPeerThreads>(accd);
-  finish_partials_n<kPeerThreads>(accd, cta_parts, &scr->counter1, &scr->send1);
+  if (finish_partials_n<kPeerThreads>(accd, cta_parts, &scr->counter1, &scr->send1) && f.on) fold_norm_decide(f, scr);
 }
 
 // K4 at N == 1 (Eq. 4-5, Alg. 2 l.449, l.454-455): Dbar = Delta = anchor - local, beta from
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(kPeerThreads) update_tma_kernel(UpdateArgs p, 
     beta_d = beta_d < 1.0 ? beta_d : 1.0;
     if (p.flags & EDIT_NO_GC) beta_d = 1.0;
     const int rb = *p.rollback;
-    if (blockIdx.x == 0) {
+    if (blockIdx.x == 0 && rb != kAbort) {
       p.rec->G_bar = rb ? 0.0 : gbar;
       p.rec->beta = rb ? 1.0 : beta_d;
       p.rec->rollback = rb;
@@ -377,6 +380,7 @@ __global__ void __launch_bounds__(kPeerThreads) update_tma_kernel(UpdateArgs p, 
     s_rollback = rb;
   }
   ring_init(&bars, K);  // (contains __syncthreads)
+  if (s_rollback == kAbort) return;
   const float beta = s_beta, mu = p.mu, nu = p.nu;
   const int lbytes = (int)sizeof(T);
   const int64_t n8 = p.n >> 3;
@@ -457,7 +461,8 @@ __global__ void __launch_bounds__(kPeerThreads) update_tma_kernel(UpdateArgs p, 
 // peer with the whole GPU, profiles/r1_peer_bench_2gpu.txt).
 template <typename T>
 __global__ void __launch_bounds__(kThreads) warm_rs_kernel(const __grid_constant__ PeerPtrs pp, Slicing sl,
-                                                           T* __restrict__ Dmine) {
+                                                           T* __restrict__ Dmine, const int* __restrict__ err) {
+  if (*err) return;  // the barrier before this kernel failed: peers' staging may be stale
   // the owner averages its slice in fp32 (fixed member order) and rounds ONCE to the
   // gradient type, so the pull below moves b_l bytes per element and every member ends
   // with the owner's bits
@@ -493,7 +498,8 @@ __global__ void __launch_bounds__(kThreads) warm_rs_kernel(const __grid_constant
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) warm_ag_kernel(const __grid_constant__ PeerPtrs pp, Slicing sl,
-                                                           T* __restrict__ out) {
+                                                           T* __restrict__ out, const int* __restrict__ err) {
+  if (*err) return;
   const int64_t n8 = sl.n >> 3;
   const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   if (i < n8) {  // a pure copy of the owner's rounded mean (16 B per bf16 vector)
@@ -514,56 +520,16 @@ __global__ void __launch_bounds__(kThreads) warm_ag_kernel(const __grid_constant
 }
 
 // ------------------------------------------------------------------------------ scalar exchange
-// Publish this rank's scalar into every rank's mailbox (value, then seq with release
-// semantics at system scope), then wait for all K senders in its own mailbox (acquire).
-// Slots alternate by seq parity: a rank can only write seq+2 into a slot after the reader
-// published seq+1, i.e. after it finished reading seq -- no slot is overwritten early.
-// with_decide: K2 (decide_body) runs right after the gather in the same 1-CTA kernel (the
-// phase-0 exchange feeds it), saving one dependent launch per unit.
-// dseq != nullptr: the sequence number is this lane's device counter for the phase, incremented
-// here (so a captured CUDA graph can be replayed: every replay takes the next number; only this
-// 1-CTA kernel on the lane's stream touches the counter); else the host-passed seq.
-__global__ void xchg_kernel(const __grid_constant__ MailPtrs mp, int K, int me, int phase,
-                            unsigned long long seq_arg, unsigned long long* dseq, const double* src, double* out,
-                            int* err, const __grid_constant__ DecideArgs dec, int with_decide) {
-  const int t = threadIdx.x;
-  __shared__ unsigned long long s_seq;
-  if (dseq) {
-    if (t == 0) {
-      s_seq = dseq[phase] + 1;
-      dseq[phase] = s_seq;
-    }
-    __syncthreads();
-  }
-  const unsigned long long seq = dseq ? s_seq : seq_arg;
-  const int base = (phase * 2 + (int)(seq & 1)) * K;
-  if (t < K) {
-    const double v = *src;
-    unsigned long long* slot = mp.box[t] + 2 * (base + me);
-    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(slot), "l"((unsigned long long)__double_as_longlong(v))
-                 : "memory");
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot + 1), "l"(seq) : "memory");
-  }
-  if (t < K) {
-    unsigned long long* slot = mp.box[me] + 2 * (base + t);
-    unsigned long long s = 0, t0, now;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    while (true) {
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(s) : "l"(slot + 1) : "memory");
-      if (s == seq) break;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-      if (now - t0 > 10000000000ull) {  // 10 s: a peer is gone; fail loudly instead of hanging
-        atomicExch(err, 1);
-        break;
-      }
-    }
-    unsigned long long vb;
-    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(vb) : "l"(slot) : "memory");
-    out[t] = __longlong_as_double((long long)vb);
-  }
-  if (with_decide) {
-    __syncthreads();  // out[0..K) written by threads 0..K-1 of this CTA
-    if (t == 0) decide_body(dec);
+// One CTA: the mailbox exchange (xchg_body, device_common.cuh) as its own launch -- used for
+// the barrier phase (fused shard all-gather, warm-up) and by the NCCL-exchange-free paths that
+// have no producing kernel to fold it into.  dec_on: K2 right after the gather.  On failure
+// *rollback (if given) := kAbort so the unit's data kernels write nothing.
+__global__ void xchg_kernel(const __grid_constant__ XchgArgs x, const double* src, double* out,
+                            int32_t* rollback, const __grid_constant__ DecideArgs dec, int dec_on) {
+  const bool ok = xchg_body(x, src, out);
+  if (threadIdx.x == 0) {
+    if (!ok && rollback) *rollback = kAbort;
+    if (ok && dec_on) decide_body(dec);
   }
 }
 
@@ -599,16 +565,15 @@ void set_smem(KernelT kernel, int bytes) {
 
 }  // namespace
 
-template <typename T, bool kEF>
+template <typename T>
 void rs_go(unsigned grid, const Ring& r, cudaStream_t st, const PeerPtrs& pp, const Slicing& sl, const float* anchor,
-           float* Dmine, LayerScratch* scr, double* cta_parts) {
-  set_smem(rs_tma_kernel<T, kEF>, r.K * r.stage_bytes);
-  rs_tma_kernel<T, kEF><<<grid, kPeerThreads, r.K * r.stage_bytes, st>>>(pp, sl, anchor, Dmine, scr, cta_parts,
-                                                                          r.K, r.V);
+           float* Dmine, LayerScratch* scr, double* cta_parts, const FoldArgs& f) {
+  set_smem(rs_tma_kernel<T>, r.K * r.stage_bytes);
+  rs_tma_kernel<T><<<grid, kPeerThreads, r.K * r.stage_bytes, st>>>(pp, sl, anchor, Dmine, scr, cta_parts, r.K, r.V, f);
 }
 
 int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anchor, float* Dmine,
-              LayerScratch* scr, double* cta_parts, int max_ctas, bool ef, int smem_kb, cudaStream_t st) {
+              LayerScratch* scr, double* cta_parts, int max_ctas, int smem_kb, const FoldArgs& f, cudaStream_t st) {
   const int esz = dtype == EDIT_BF16 ? 2 : 4;
   const Ring r = ring_for(sl.tile, 8 * (4 + sl.N * esz), smem_kb);
   const int64_t n8 = sl.n >> 3;
@@ -616,60 +581,50 @@ int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anc
   const int64_t s1 = n8 < s0 + sl.slice ? n8 : s0 + sl.slice;
   const int64_t ntiles = s1 > s0 ? (s1 - s0 + r.V - 1) / r.V : 0;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, max_ctas));
-  if (dtype == EDIT_BF16) {
-    if (ef) rs_go<__nv_bfloat16, true>(grid, r, st, pp, sl, anchor, Dmine, scr, cta_parts);
-    else rs_go<__nv_bfloat16, false>(grid, r, st, pp, sl, anchor, Dmine, scr, cta_parts);
-  } else {
-    if (ef) rs_go<float, true>(grid, r, st, pp, sl, anchor, Dmine, scr, cta_parts);
-    else rs_go<float, false>(grid, r, st, pp, sl, anchor, Dmine, scr, cta_parts);
-  }
+  if (dtype == EDIT_BF16) rs_go<__nv_bfloat16>(grid, r, st, pp, sl, anchor, Dmine, scr, cta_parts, f);
+  else rs_go<float>(grid, r, st, pp, sl, anchor, Dmine, scr, cta_parts, f);
   return 1;
 }
 
-template <typename T, bool kEF>
+template <typename T>
 void ag_go(unsigned grid, const Ring& r, cudaStream_t st, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl) {
   if (a.gather_M > 0) {
-    set_smem(ag_update_tma_kernel<T, kEF, true>, r.K * r.stage_bytes);
-    ag_update_tma_kernel<T, kEF, true><<<grid, kPeerThreads, r.K * r.stage_bytes, st>>>(a, pp, sl, r.K, r.V);
+    set_smem(ag_update_tma_kernel<T, true>, r.K * r.stage_bytes);
+    ag_update_tma_kernel<T, true><<<grid, kPeerThreads, r.K * r.stage_bytes, st>>>(a, pp, sl, r.K, r.V);
   } else {
-    set_smem(ag_update_tma_kernel<T, kEF, false>, r.K * r.stage_bytes);
-    ag_update_tma_kernel<T, kEF, false><<<grid, kPeerThreads, r.K * r.stage_bytes, st>>>(a, pp, sl, r.K, r.V);
+    set_smem(ag_update_tma_kernel<T, false>, r.K * r.stage_bytes);
+    ag_update_tma_kernel<T, false><<<grid, kPeerThreads, r.K * r.stage_bytes, st>>>(a, pp, sl, r.K, r.V);
   }
 }
 
 int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl, int max_ctas,
-                     bool ef, int smem_kb, cudaStream_t st) {
+                     int smem_kb, cudaStream_t st) {
   const Ring r = ring_for(sl.tile, 8 * 12, smem_kb);
   const int64_t nq = (int64_t)sl.N * (sl.slice / r.V);
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nq, max_ctas));
-  if (dtype == EDIT_BF16) {
-    if (ef) ag_go<__nv_bfloat16, true>(grid, r, st, a, pp, sl);
-    else ag_go<__nv_bfloat16, false>(grid, r, st, a, pp, sl);
-  } else {
-    if (ef) ag_go<float, true>(grid, r, st, a, pp, sl);
-    else ag_go<float, false>(grid, r, st, a, pp, sl);
-  }
+  if (dtype == EDIT_BF16) ag_go<__nv_bfloat16>(grid, r, st, a, pp, sl);
+  else ag_go<float>(grid, r, st, a, pp, sl);
   return 1;
 }
 
 template <typename T>
 void pg_norm_tma_go(unsigned grid, const Ring& r, cudaStream_t st, const void* local, const float* anchor, int64_t n,
-                    LayerScratch* scr, double* cta_parts) {
+                    LayerScratch* scr, double* cta_parts, const FoldArgs& f) {
   set_smem(pg_norm_tma_kernel<T>, r.K * r.stage_bytes);
   pg_norm_tma_kernel<T><<<grid, kPeerThreads, r.K * r.stage_bytes, st>>>(static_cast<const T*>(local), anchor, n,
-                                                                         scr, cta_parts, r.K, r.V);
+                                                                         scr, cta_parts, r.K, r.V, f);
 }
 
 int launch_pg_norm_tma(int dtype, const void* local, const float* anchor, int64_t n, LayerScratch* scr,
-                       double* cta_parts, int max_ctas, cudaStream_t st) {
+                       double* cta_parts, int max_ctas, const FoldArgs& f, cudaStream_t st) {
   const int esz = dtype == EDIT_BF16 ? 2 : 4;
   const Ring r = ring_for(2 * kPeerTileVec, 8 * (4 + esz), 0);  // bf16: 1024-vector tiles x 4 stages
   const int64_t ntiles = ((n >> 3) + r.V - 1) / r.V;
   // never more CTAs than the unit's partial slots (grid_of(n, kVecReduce), the full-grid K1's)
   const int64_t g = std::min<int64_t>({ntiles, (int64_t)max_ctas, grid_of(n, kVecReduce)});
   const unsigned grid = (unsigned)std::max<int64_t>(1, g);
-  if (dtype == EDIT_BF16) pg_norm_tma_go<__nv_bfloat16>(grid, r, st, local, anchor, n, scr, cta_parts);
-  else pg_norm_tma_go<float>(grid, r, st, local, anchor, n, scr, cta_parts);
+  if (dtype == EDIT_BF16) pg_norm_tma_go<__nv_bfloat16>(grid, r, st, local, anchor, n, scr, cta_parts, f);
+  else pg_norm_tma_go<float>(grid, r, st, local, anchor, n, scr, cta_parts, f);
   return 1;
 }
 
@@ -688,30 +643,31 @@ int launch_update_tma(int dtype, const UpdateArgs& a, int max_ctas, cudaStream_t
   return 1;
 }
 
-int launch_xchg(const MailPtrs& mp, int K, int me, int phase, unsigned long long seq, const double* src,
-                double* out, int* err, cudaStream_t st, const DecideArgs* dec, unsigned long long* dseq) {
+int launch_xchg(const XchgArgs& x, const double* src, double* out, int32_t* rollback, cudaStream_t st,
+                const DecideArgs* dec) {
   DecideArgs d{};
   if (dec) d = *dec;
-  xchg_kernel<<<1, 64, 0, st>>>(mp, K, me, phase, seq, dseq, src, out, err, d, dec ? 1 : 0);
+  xchg_kernel<<<1, 64, 0, st>>>(x, src, out, rollback, d, dec ? 1 : 0);
   return 1;
 }
 
-int launch_warm_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, void* Dmine, cudaStream_t st) {
+int launch_warm_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, void* Dmine, const int* err, cudaStream_t st) {
   const int64_t n8 = sl.n >> 3;
   const int64_t s0 = (int64_t)sl.me * sl.slice;
   const int64_t cnt = std::max<int64_t>(0, std::min(s0 + sl.slice, n8) - s0);
   const unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + kThreads - 1) / kThreads);
   if (dtype == EDIT_BF16)
-    warm_rs_kernel<__nv_bfloat16><<<grid, kThreads, 0, st>>>(pp, sl, static_cast<__nv_bfloat16*>(Dmine));
+    warm_rs_kernel<__nv_bfloat16><<<grid, kThreads, 0, st>>>(pp, sl, static_cast<__nv_bfloat16*>(Dmine), err);
   else
-    warm_rs_kernel<float><<<grid, kThreads, 0, st>>>(pp, sl, static_cast<float*>(Dmine));
+    warm_rs_kernel<float><<<grid, kThreads, 0, st>>>(pp, sl, static_cast<float*>(Dmine), err);
   return 1;
 }
 
-int launch_warm_ag(int dtype, const PeerPtrs& pp, const Slicing& sl, void* out, cudaStream_t st) {
+int launch_warm_ag(int dtype, const PeerPtrs& pp, const Slicing& sl, void* out, const int* err, cudaStream_t st) {
   const unsigned grid = (unsigned)std::max<int64_t>(1, ((sl.n >> 3) + kThreads - 1) / kThreads);
-  if (dtype == EDIT_BF16) warm_ag_kernel<__nv_bfloat16><<<grid, kThreads, 0, st>>>(pp, sl, static_cast<__nv_bfloat16*>(out));
-  else warm_ag_kernel<float><<<grid, kThreads, 0, st>>>(pp, sl, static_cast<float*>(out));
+  if (dtype == EDIT_BF16)
+    warm_ag_kernel<__nv_bfloat16><<<grid, kThreads, 0, st>>>(pp, sl, static_cast<__nv_bfloat16*>(out), err);
+  else warm_ag_kernel<float><<<grid, kThreads, 0, st>>>(pp, sl, static_cast<float*>(out), err);
   return 1;
 }
 
