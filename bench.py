@@ -244,8 +244,9 @@ def main() -> None:
     ap.add_argument("--overlap-tokens", default="8192,65536",
                     help="tokens/GPU of the synthetic forward(s) for the prefetch-overlap measurement, comma "
                          "list (0 = skip); 8,192 = SURVEY 8d default, 65,536 = the paper's 1024 seqs x 4096 / 64")
-    ap.add_argument("--partition", default="0,32",
-                    help="scheduler partition modes to measure (comma list of SM counts; 0 = full grids)")
+    ap.add_argument("--partition", default="-1,0,32",
+                    help="scheduler partition modes to measure (comma list: -1 = auto, the library default; "
+                         "0 = full grids; > 0 = that many SMs)")
     ap.add_argument("--full-units", type=int, default=2,
                     help="partition mode: units before this index keep full grids (embedding + first layer)")
     ap.add_argument("--overlap-steps", type=int, default=3)
@@ -530,7 +531,7 @@ def main() -> None:
             sync.set_partition(sms, args.full_units)
             t, k = timed_clk(sched_only, args.overlap_steps)
             t_sync_sched[str(sms)] = {"ms": t, "clocks": k}
-        sync.set_partition(0, args.full_units)
+        sync.set_partition(-1, args.full_units)
         runs = []
         for tokens in tokens_list:
             fwd = SyntheticForward(args.model, units, tokens, dev)
@@ -558,7 +559,7 @@ def main() -> None:
                                  "clocks_fwd": clk_fwd, "clocks_fwd_plus_sync": clk_both,
                                  "fwd_tflops": fwd.flops_per_round() / (t_fwd * 1e-3) / 1e12,
                                  "hidden_fraction": 1.0 - (t_both - t_fwd) / t_sync_alone})
-            sync.set_partition(0, args.full_units)
+            sync.set_partition(-1, args.full_units)
             del fwd
             torch.cuda.empty_cache()
         best = {}
@@ -566,15 +567,19 @@ def main() -> None:
             k = r["tokens_per_gpu"]
             if k not in best or r["hidden_fraction"] > best[k]["hidden_fraction"]:
                 best[k] = r
+        default = {str(r["tokens_per_gpu"]): r for r in runs if r["partition_sms"] == -1 and r["depth"] == 1}
         head = best[tokens_list[0]]
         overlap = {"tokens_per_gpu": head["tokens_per_gpu"], "t_sync_ms": t_sync_alone, "clocks_sync": clk_sync,
                    "t_sync_sched_alone_ms_by_partition": t_sync_sched,
-                   "t_fwd_ms": head["t_fwd_ms"], "best": {str(k): v for k, v in best.items()}, "runs": runs,
+                   "t_fwd_ms": head["t_fwd_ms"], "best": {str(k): v for k, v in best.items()},
+                   "default_settings": default, "runs": runs,
                    "full_units": args.full_units,
                    "note": ("synthetic forward (bf16 GEMMs of each unit, weights = the synced local) on the "
                             "compute stream; syncs on the library's side streams; acquire(u) before forward(u); "
                             "partition_sms > 0: edit_sched_set_partition (units >= full_units on that many "
-                            "persistent TMA CTAs, one per SM); h = 1 - (t_fwd+sync - t_fwd) / t_sync_alone")}
+                            "persistent TMA CTAs, one per SM; -1 = auto, the library default: per unit the fewest SMs that "
+                            "finish its sync within the forward it overlaps, measured in the previous round); "
+                            "h = 1 - (t_fwd+sync - t_fwd) / t_sync_alone")}
 
     # NEXT-3: warm-up gradient all-reduce (mean over the sync group) of a full set of bf16
     # gradient shards, library path vs torch.distributed/NCCL all_reduce on the same group

@@ -238,17 +238,24 @@ edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* 
 edit_status_t edit_sched_acquire(edit_sync_t h, int32_t layer, void* compute_stream);
 edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream);
 /* Partition mode of the scheduler (how the overlap of P:70 is obtained on one GPU whose
- * forward is tensor-bound on every SM).  sms > 0: the syncs of units u >= full_units run as
- * persistent TMA pipelines on about `sms` SMs in total (each lane's kernels get
- * ceil(sms / lanes) CTAs; the lanes run concurrently), each CTA holding a ~200 KB
- * shared-memory ring so that it owns its SM; the concurrent forward keeps the other SMs.  The side streams are
- * switched to the highest stream priority (so a freed SM goes to a sync CTA first).  Units
- * u < full_units (the ones a forward reaches before its first GEMM, e.g. the embedding: 2)
- * keep full grids.  sms == 0 restores the default (full grids, init priority).
- * Covers K1 and the N == 1 update (peer path: also RS and AG); the NCCL path's K1/K3/K4 and
- * the NEXT-2 gathering update keep their full-grid kernels.  Results are those of the
- * default mode within R17 (only the reduction grouping of K1 differs).  Not during a round.
- * EDIT_ERR_INVALID_ARG: sms < 0 or > #SMs, full_units < 0, a round is active. */
+ * forward is tensor-bound on every SM).  The syncs of units u >= full_units run as persistent
+ * TMA pipelines on a few SMs, each CTA holding a ~200 KB shared-memory ring so that it owns
+ * its SM; the concurrent forward keeps the other SMs.  Units u < full_units (the ones a
+ * forward reaches before its first GEMM, e.g. the embedding: 2) keep full grids.
+ *   sms == -1 (the DEFAULT, "auto"): per unit, the fewest SMs that stream the unit's bytes
+ *     within the forward time its sync overlaps (units u-depth .. u-1, measured on the
+ *     compute stream between acquire calls of the previous round; EDIT_SM_GBPS, default 100
+ *     GB/s per SM, the measured per-SM streaming rate), x1.25 margin, in [4, #SMs]; the first
+ *     round (nothing measured yet) uses #SMs / 4.  A forward too short to hide anything
+ *     gets all SMs: the sync then runs back to back with it.
+ *   sms > 0: fixed, ceil(sms / lanes) CTAs per lane's kernels (the lanes run concurrently).
+ *   sms == 0: full grids at the lowest stream priority (the sync fills what the forward
+ *     leaves free; measured worse than serial on a tensor-bound forward, DESIGN 7).
+ * The side streams run at the highest priority for sms != 0 (a freed SM goes to a sync CTA
+ * first).  Covers K1 and the N == 1 update (peer path: also RS and AG); the NCCL path's
+ * K1/K3/K4 and the NEXT-2 gathering update keep their full-grid kernels.  Results are those
+ * of the default mode within R17 (only the reduction grouping of K1 differs).  Not during a
+ * round.  EDIT_ERR_INVALID_ARG: sms < -1 or > #SMs, full_units < 0, a round is active. */
 edit_status_t edit_sched_set_partition(edit_sync_t h, int32_t sms, int32_t full_units);
 
 /* Warm-up phase (Alg. 1 l.422-424): while (t*tau + p) <= t_warm the gradients

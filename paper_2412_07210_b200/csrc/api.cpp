@@ -22,6 +22,7 @@ typedef int CUresult_t;  // CUresult (driver API) without including cuda.h
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <new>
 #include <string>
 #include <vector>
@@ -282,6 +283,14 @@ edit_status_t create_local(const edit_sync_config_t* cfg, void* workspace, size_
   for (auto& e : h->done) LCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   h->gate_ev.assign(cfg->num_layers, nullptr);
   for (auto& e : h->gate_ev) LCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  h->acq_ev.assign(cfg->num_layers + 1, nullptr);
+  for (auto& e : h->acq_ev) LCUDA(cudaEventCreate(&e));
+  h->fwd_ms.assign(cfg->num_layers, 0.0);
+  h->sched_sms.assign(cfg->num_layers, 0);
+  if (const char* e = getenv("EDIT_SM_GBPS")) {
+    const double v = atof(e);
+    if (v > 0) h->sm_gbps = v;
+  }
   if (const char* e = getenv("EDIT_SCHED_GATE")) h->sched_gate = atoi(e) != 0;
   LCUDA(cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming));
 
@@ -296,12 +305,13 @@ edit_status_t create_local(const edit_sync_config_t* cfg, void* workspace, size_
   }
   int prio_lo = 0, prio_hi = 0;
   LCUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-  // lane-stream priority (EDIT_SCHED_PRIORITY=high|normal|low, default low): with the
-  // LOWEST priority a concurrent forward's GEMM CTAs are placed first and the sync's CTAs
-  // fill what they leave free on each SM, instead of displacing them
-  int prio = prio_lo;
+  // lane-stream priority (EDIT_SCHED_PRIORITY=high|normal|low).  Default high: the
+  // scheduler's default auto-partition mode wants each SM a forward CTA releases to go to a
+  // sync CTA first (edit_sched_set_partition(h, 0, .) -- full grids -- switches to low: then a
+  // concurrent forward's GEMM CTAs are placed first and the sync fills the gaps)
+  int prio = prio_hi;
   if (const char* e = getenv("EDIT_SCHED_PRIORITY")) {
-    if (!strcmp(e, "high")) prio = prio_hi;
+    if (!strcmp(e, "low")) prio = prio_lo;
     else if (!strcmp(e, "normal")) prio = 0;
   }
   h->lane_prio = prio;
@@ -1051,6 +1061,31 @@ edit_status_t edit_sync_host_wait(edit_sync_t h, void* stream) {
   return EDIT_OK;
 }
 
+// HBM bytes per param one unit sync streams through the SMs (the dataflow's, not the
+// algorithmic minimum): N == 1: K1 (b_l + 4) + K4 (16 + 2 b_l); peer path: K1 (+ staging copy
+// unless registered) + RS (b_l + 8/N) + AG (20 + b_l).
+static double unit_bytes_per_param(edit_sync_t h, int u) {
+  const double bl = h->cfg.param_dtype == EDIT_BF16 ? 2.0 : 4.0;
+  if (h->N == 1) return (bl + 4) + (16 + 2 * bl);
+  const bool direct = h->peer && !h->reg_local.empty() && h->reg_local[u] == h->sched_local[u];
+  return (bl + 4) + (direct ? 0 : bl) + (bl + 8.0 / h->N) + (20 + bl);
+}
+
+// Auto partition (the scheduler's default): the sync of unit u is enqueued when the forward
+// acquires unit u - depth and must be complete when it acquires u, so it overlaps the forward
+// of units u-depth .. u-1.  Give it the fewest SMs that stream its bytes in that time at the
+// measured per-SM rate (x1.25 margin): the forward keeps every other SM.  Without a measured
+// forward (first round) or with a forward too short to hide anything, all SMs.
+static int sched_auto_sms(edit_sync_t h, int u) {
+  if (!h->fwd_valid) return std::max(8, h->num_sms / 4);
+  double budget_ms = 0.0;
+  for (int k = std::max(0, u - h->sched_depth); k < u; ++k) budget_ms += h->fwd_ms[k];
+  const double bytes = unit_bytes_per_param(h, u) * (double)h->numel[u];
+  if (budget_ms <= 0.0) return h->num_sms;
+  const double sms = 1.25 * bytes / (h->sm_gbps * 1e9 * budget_ms * 1e-3);
+  return std::max(4, std::min(h->num_sms, (int)std::ceil(sms)));
+}
+
 static edit_status_t sched_enqueue_next(edit_sync_t h, cudaStream_t gate = nullptr) {
   const int u = h->sched_next_sync++;
   Lane& ln = h->lanes[u % h->lanes.size()];
@@ -1060,16 +1095,22 @@ static edit_status_t sched_enqueue_next(edit_sync_t h, cudaStream_t gate = nullp
   }
   Mode mode{h->sched_ctas, h->sched_ctas > 0 ? h->sched_ctas : h->peer_ctas, h->sched_ctas > 0 ? h->sched_smem_kb : 0,
             0};
+  int per = 0;
   if (h->sched_part > 0 && u >= h->sched_full_units) {
     // partition mode: persistent TMA pipelines with full rings; the lanes run concurrently,
     // so each lane's kernels get an equal share of the sched_part SMs
     const int nl = (int)h->lanes.size();
-    const int per = std::max(1, (h->sched_part + nl - 1) / nl);
+    per = std::max(1, (h->sched_part + nl - 1) / nl);
+  } else if (h->sched_part == kSchedAuto && u >= h->sched_full_units) {
+    per = sched_auto_sms(h, u);
+  }
+  if (per > 0) {
     mode.cap = 0;
     mode.peer_ctas = per;
     mode.smem_kb = 0;
     mode.part = per;
   }
+  h->sched_sms[u] = per;
   UnitPlan p;
   TRY(plan_unit(h, ln, u, h->sched_local[u], h->sched_anchor[u], h->sched_mom[u], ln.stream, mode, p));
   const NvtxRange range(h->nvtx, "edit_sync unit %d (scheduled)", u);
@@ -1094,6 +1135,19 @@ edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* 
   h->sched_next_sync = 0;
   h->sched_next_acquire = 0;
   h->sched_active = true;
+  // auto partition: the previous round's per-unit forward times (acquire(u) -> acquire(u+1),
+  // the last unit -> end_round), if those events have completed (no host blocking)
+  if (h->sched_part == kSchedAuto && h->acq_ev.size() == (size_t)L + 1 &&
+      cudaEventQuery(h->acq_ev[L]) == cudaSuccess && h->sched_rounds > 0) {
+    bool ok = true;
+    for (int u = 0; u < L && ok; ++u) {
+      float ms = 0.f;
+      ok = cudaEventElapsedTime(&ms, h->acq_ev[u], h->acq_ev[u + 1]) == cudaSuccess;
+      h->fwd_ms[u] = ms;
+    }
+    h->fwd_valid = ok;
+    cudaGetLastError();  // (clear a failed elapsed-time query)
+  }
   // the side streams (lanes) start after everything already on the compute stream (the
   // inner steps that produced the locals)
   CUDA_TRY(h, cudaEventRecord(h->fork, static_cast<cudaStream_t>(compute_stream)));
@@ -1111,6 +1165,8 @@ edit_status_t edit_sched_acquire(edit_sync_t h, int32_t layer, void* compute_str
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   while (h->sched_next_sync <= layer) TRY(sched_enqueue_next(h));  // (depth can only lag if acquire skipped ahead)
   CUDA_TRY(h, cudaStreamWaitEvent(static_cast<cudaStream_t>(compute_stream), h->done[layer], 0));
+  // (auto partition) the forward of unit `layer` starts here on the compute stream
+  CUDA_TRY(h, cudaEventRecord(h->acq_ev[layer], static_cast<cudaStream_t>(compute_stream)));
   h->sched_next_acquire = layer + 1;
   if (h->sched_next_sync < L && h->sched_next_sync <= layer + h->sched_depth)
     TRY(sched_enqueue_next(h, static_cast<cudaStream_t>(compute_stream)));
@@ -1125,6 +1181,12 @@ edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream) {
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   while (h->sched_next_sync < L) TRY(sched_enqueue_next(h));
   cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
+  // (auto partition) the forward of the last unit ends here -- valid only if every unit was
+  // acquired in this round
+  if (h->sched_next_acquire == L) {
+    CUDA_TRY(h, cudaEventRecord(h->acq_ev[L], cs));
+    h->sched_rounds += 1;
+  }
   for (Lane& ln : h->lanes) {
     CUDA_TRY(h, cudaEventRecord(ln.tail, ln.stream));
     CUDA_TRY(h, cudaStreamWaitEvent(cs, ln.tail, 0));
@@ -1137,14 +1199,14 @@ edit_status_t edit_sched_set_partition(edit_sync_t h, int32_t sms, int32_t full_
   if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
   TRY(check_err(h));
   if (h->sched_active) return fail(EDIT_ERR_INVALID_ARG, "a scheduled round is active");
-  if (sms < 0 || sms > h->num_sms || full_units < 0)
-    return fail(EDIT_ERR_INVALID_ARG, "sms must be in [0, #SMs], full_units >= 0");
+  if (sms < kSchedAuto || sms > h->num_sms || full_units < 0)
+    return fail(EDIT_ERR_INVALID_ARG, "sms must be -1 (auto) or in [0, #SMs], full_units >= 0");
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   int prio_lo = 0, prio_hi = 0;
   CUDA_TRY(h, cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   // partition mode: the lanes' persistent CTAs should take each SM a forward CTA releases,
   // so the lanes run at the highest priority; otherwise back to the priority of init
-  const int prio = sms > 0 ? prio_hi : h->lane_prio;
+  const int prio = sms != 0 ? h->lane_prio : prio_lo;
   for (Lane& ln : h->lanes) {
     int cur = 0;
     CUDA_TRY(h, cudaStreamGetPriority(ln.stream, &cur));
@@ -1356,6 +1418,8 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
   for (auto e : h->done)
     if (e) cudaEventDestroy(e);
   for (auto e : h->gate_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto e : h->acq_ev)
     if (e) cudaEventDestroy(e);
   for (auto e : h->prof)
     if (e) cudaEventDestroy(e);

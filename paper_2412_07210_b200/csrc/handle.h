@@ -54,6 +54,8 @@ struct RoundGraph {
 };
 
 // How a unit's kernels are shaped (default full grids; the scheduler's modes).
+constexpr int kSchedAuto = -1;  // edit_sched_set_partition(sms = -1): sized per unit from the forward
+
 struct Mode {
   int cap = 0;        // max CTAs of the LDG streaming kernels (0 = full grid)
   int peer_ctas = 0;  // persistent grid of the TMA peer kernels
@@ -86,9 +88,18 @@ struct edit_sync {
   int sched_ctas = 0;
   int sched_smem_kb = 18;
   // partition mode (edit_sched_set_partition): scheduled units u >= sched_full_units run
-  // as persistent TMA pipelines on sched_part CTAs (one per SM), lanes at high priority
-  int sched_part = 0;
+  // as persistent TMA pipelines on sched_part CTAs (one per SM), lanes at high priority.
+  // sched_part == kSchedAuto (the default): per unit, the fewest SMs that finish the unit's
+  // sync within the forward time it overlaps (measured in the previous round from events at
+  // acquire), at sm_gbps per SM (EDIT_SM_GBPS, measured ~100 GB/s per SM, DESIGN 6)
+  int sched_part = -1;
   int sched_full_units = 2;
+  double sm_gbps = 100.0;
+  std::vector<cudaEvent_t> acq_ev;   // [L + 1] timing events on the compute stream at acquire / end
+  std::vector<double> fwd_ms;        // [L] forward time of each unit in the last measured round
+  bool fwd_valid = false;
+  int64_t sched_rounds = 0;          // completed scheduled rounds (all units acquired)
+  std::vector<int> sched_sms;        // [L] SMs given to each unit's sync in the current round
   int lane_prio = 0;             // priority the lanes were created with (env default)
   // gate (EDIT_SCHED_GATE=1): the sync of unit u+depth starts only when the forward of unit
   // u may start (an event on the compute stream at acquire(u)), not as soon as its lane frees

@@ -249,8 +249,9 @@ class EditSync:
         self._round_refs = None
 
     def set_partition(self, sms: int, full_units: int = 2) -> None:
-        """Scheduler partition mode (edit_sched_set_partition): units >= full_units sync on at
-        most `sms` persistent TMA CTAs (one per SM) while the forward keeps the other SMs."""
+        """Scheduler partition mode (edit_sched_set_partition): units >= full_units sync on
+        persistent TMA CTAs (one per SM) while the forward keeps the other SMs.  sms = -1
+        (default): sized per unit from the measured forward; > 0: fixed; 0: full grids."""
         _check(self._lib.edit_sched_set_partition(self._h, int(sms), int(full_units)))
 
     def _check_round(self, locals_, anchors, momenta):
