@@ -541,6 +541,7 @@ edit_status_t enqueue_step(edit_sync_t h, UnitPlan& p, int step) {
 edit_status_t enqueue_units(edit_sync_t const* hs, int nh, int nunits, const int32_t* layers,
                             void* const* locals, float* const* anchors, float* const* momenta,
                             const cudaStream_t* streams, bool use_lanes) {
+  for (int k = 0; k < nh; ++k) TRY(check_err(hs[k]));
   if (use_lanes)
     for (int k = 0; k < nh; ++k) {
       edit_sync_t h = hs[k];

@@ -259,9 +259,10 @@ def test_prefetch_scheduler_partition_mode_matches_oracle(dtype, sms, full_units
         assert torch.equal(c.local[i], c.anchor[i].to(DTYPES[dtype])), tag
         if i == 3:
             assert out.rollback and np.array_equal(c.anchor[i].cpu().numpy(), c.o_anchor[i])
-    c.sync.set_partition(0, 2)                               # back to full grids
+    c.sync.set_partition(0, 2)                               # full grids
+    c.sync.set_partition(-1, 2)                              # back to the default (auto)
     with pytest.raises(Exception):
-        c.sync.set_partition(-1, 0)
+        c.sync.set_partition(-2, 0)
 
 
 def test_prefetch_scheduler_argument_errors():

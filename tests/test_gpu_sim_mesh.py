@@ -76,6 +76,7 @@ class MeshCase:
         self.plant = {k: v for k, v in plant.items() if k[1] < N}
         self.recipe = synth.Recipe()
         self.numel = [synth.shard_numel(u.numel, M) for u in self.units]
+        self.full = None
         if lanes is not None:
             os.environ["EDIT_LANES"] = str(lanes)
         try:
