@@ -249,7 +249,7 @@ def main() -> None:
                          "0 = full grids; > 0 = that many SMs)")
     ap.add_argument("--full-units", type=int, default=2,
                     help="partition mode: units before this index keep full grids (embedding + first layer)")
-    ap.add_argument("--overlap-steps", type=int, default=3)
+    ap.add_argument("--overlap-steps", type=int, default=4)
     ap.add_argument("--warmup-allreduce", action="store_true", help="NEXT-3 measurement (N > 1)")
     ap.add_argument("--gather", action="store_true", help="NEXT-2 fused shard all-gather measurement (M > 1)")
     ap.add_argument("--no-register", action="store_true",
@@ -549,16 +549,48 @@ def main() -> None:
                     sync.end_round(stream)
                 return run
 
+            def once(fn, redraw_first, k=[0]):
+                k[0] += 1
+                if redraw_first:
+                    redraw(3000 + k[0])
+                barrier()
+                torch.cuda.synchronize()
+                ev0.record(stream)
+                fn()
+                ev1.record(stream)
+                torch.cuda.synchronize()
+                return max_over_ranks(ev0.elapsed_time(ev1), world, dev)
+
             t_fwd, clk_fwd = timed_clk(forward_only, args.overlap_steps, redraw_first=False)
             for sms in parts:
                 sync.set_partition(sms, args.full_units)
                 for depth in (1, 2):
-                    t_both, clk_both = timed_clk(fwd_and_sync(depth), args.overlap_steps)
+                    # warm-up rounds: the auto mode (-1) tunes itself over its first 8 rounds
+                    for _ in range(9 if sms == -1 else 1):
+                        once(fwd_and_sync(depth), True)
+                    # paired measurement: the forward alone and forward + sync back to back, the
+                    # exposed sync time = the median of the pair differences (the forward runs
+                    # at the power cap and drifts by more than t_sync between separate runs)
+                    c = Clocks(local_rank)
+                    diffs, tb, tf = [], [], []
+                    with c:
+                        for _ in range(args.overlap_steps):
+                            a_ = once(forward_only, False)
+                            b_ = once(fwd_and_sync(depth), True)
+                            diffs.append(b_ - a_)
+                            tf.append(a_)
+                            tb.append(b_)
+                    k = c.summary()
+                    exposed = statistics.median(diffs)
                     runs.append({"tokens_per_gpu": tokens, "partition_sms": sms, "depth": depth,
-                                 "t_fwd_ms": t_fwd, "t_fwd_plus_sync_ms": t_both,
-                                 "clocks_fwd": clk_fwd, "clocks_fwd_plus_sync": clk_both,
+                                 "t_fwd_ms": statistics.mean(tf), "t_fwd_plus_sync_ms": statistics.mean(tb),
+                                 "exposed_ms_median_pair": exposed, "exposed_ms_pairs": diffs,
+                                 "clocks_fwd": clk_fwd,
+                                 "clocks_pairs": {"sm_mhz": k["sm_mhz"], "power_w": k.get("power_w"),
+                                                  "power_cap_frac": k.get("power_cap_frac"), "samples": k["samples"]},
                                  "fwd_tflops": fwd.flops_per_round() / (t_fwd * 1e-3) / 1e12,
-                                 "hidden_fraction": 1.0 - (t_both - t_fwd) / t_sync_alone})
+                                 "plan": sync.sched_plan() if sms == -1 else None,
+                                 "hidden_fraction": 1.0 - exposed / t_sync_alone})
             sync.set_partition(-1, args.full_units)
             del fwd
             torch.cuda.empty_cache()
@@ -579,7 +611,8 @@ def main() -> None:
                             "partition_sms > 0: edit_sched_set_partition (units >= full_units on that many "
                             "persistent TMA CTAs, one per SM; -1 = auto, the library default: per unit the fewest SMs that "
                             "finish its sync within the forward it overlaps, measured in the previous round); "
-                            "h = 1 - (t_fwd+sync - t_fwd) / t_sync_alone")}
+                            "h = 1 - exposed / t_sync_alone, exposed = median over pairs of (fwd+sync) - (fwd alone) run back to "
+                            "back; the auto mode is measured after its 8 tuning rounds")}
 
     # NEXT-3: warm-up gradient all-reduce (mean over the sync group) of a full set of bf16
     # gradient shards, library path vs torch.distributed/NCCL all_reduce on the same group

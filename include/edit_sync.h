@@ -242,12 +242,16 @@ edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream);
  * TMA pipelines on a few SMs, each CTA holding a ~200 KB shared-memory ring so that it owns
  * its SM; the concurrent forward keeps the other SMs.  Units u < full_units (the ones a
  * forward reaches before its first GEMM, e.g. the embedding: 2) keep full grids.
- *   sms == -1 (the DEFAULT, "auto"): per unit, the fewest SMs that stream the unit's bytes
- *     within the forward time its sync overlaps (units u-depth .. u-1, measured on the
- *     compute stream between acquire calls of the previous round; EDIT_SM_GBPS, default 100
- *     GB/s per SM, the measured per-SM streaming rate), x1.25 margin, in [4, #SMs]; the first
- *     round (nothing measured yet) uses #SMs / 4.  A forward too short to hide anything
- *     gets all SMs: the sync then runs back to back with it.
+ *   sms == -1 (the DEFAULT, "auto"): self-tuning.  Each round runs one of four plans and
+ *     is timed on the compute stream (begin_round -> end_round): SERIAL (unit u's sync starts
+ *     when the forward reaches acquire(u), on full grids: no overlap, i.e. never slower than
+ *     the two back to back) or PARTITION with f = 1.0 / 1.6 / 2.5 x the fewest SMs that
+ *     stream unit u's bytes within the forward time its sync overlaps (units u-depth .. u-1,
+ *     measured per unit between acquire calls; EDIT_SM_GBPS, default 100 GB/s per SM, the
+ *     measured per-SM streaming rate), in [4, #SMs].  Every plan is measured twice (serial
+ *     first), then the fastest median is kept; a > 15 % drift of its newest round time
+ *     re-measures all.  So after 8 rounds the default is the best of serial and the
+ *     partitions for this forward (edit_sched_get_plan reports the choice).
  *   sms > 0: fixed, ceil(sms / lanes) CTAs per lane's kernels (the lanes run concurrently).
  *   sms == 0: full grids at the lowest stream priority (the sync fills what the forward
  *     leaves free; measured worse than serial on a tensor-bound forward, DESIGN 7).
@@ -257,6 +261,12 @@ edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream);
  * of the default mode within R17 (only the reduction grouping of K1 differs).  Not during a
  * round.  EDIT_ERR_INVALID_ARG: sms < -1 or > #SMs, full_units < 0, a round is active. */
 edit_status_t edit_sched_set_partition(edit_sync_t h, int32_t sms, int32_t full_units);
+/* The scheduler's plan of its last round (host values, no device sync): *candidate = -1 for a
+ * fixed setting (sms >= 0), else the auto mode's choice: 0 = serial, 1..3 = partition with
+ * 1.0 / 1.6 / 2.5 x the minimum SMs; sms[u] (nullable, [L]) = SMs given to unit u's sync
+ * (0 = full grid, -1 = serial); median_ms (nullable, [4]) = the measured median round time of
+ * each candidate so far (0 = not measured). */
+edit_status_t edit_sched_get_plan(edit_sync_t h, int32_t* candidate, int32_t* sms, double* median_ms);
 
 /* Warm-up phase (Alg. 1 l.422-424): while (t*tau + p) <= t_warm the gradients
  * of the synchronous mini-batch phase are all-reduced within the model sync group, after the

@@ -150,6 +150,10 @@ cudaError_t record_event(cudaEvent_t ev, cudaStream_t st) {
                                               : cudaEventRecord(ev, st);
 }
 
+// the peer kernels' variant: LDG full grids for full-speed rounds (EDIT_PEER_KERNELS), the
+// persistent TMA pipelines whenever the grid is capped (partition / co-resident modes)
+int full_speed(edit_sync_t h, const Mode& m) { return (m.part == 0 && m.cap == 0 && m.smem_kb == 0) ? h->peer_ldg : 0; }
+
 bool capturing(cudaStream_t st) {
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   return cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusActive;
@@ -239,6 +243,7 @@ edit_status_t create_local(const edit_sync_config_t* cfg, void* workspace, size_
   h->peer_ctas = h->num_sms;
   if (const char* e = getenv("EDIT_XCHG")) h->dev_xchg = strcmp(e, "nccl") != 0;
   if (const char* e = getenv("EDIT_GRAPH")) h->graph = atoi(e) != 0;
+  if (const char* e = getenv("EDIT_PEER_KERNELS")) h->peer_ldg = !strcmp(e, "tma") ? 0 : !strcmp(e, "ldg2") ? 2 : 1;
   if (const char* e = getenv("EDIT_NVTX")) h->nvtx = atoi(e) != 0;
   if (const char* e = getenv("EDIT_PEER_TILE")) {
     const int v = atoi(e);
@@ -283,8 +288,14 @@ edit_status_t create_local(const edit_sync_config_t* cfg, void* workspace, size_
   for (auto& e : h->done) LCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   h->gate_ev.assign(cfg->num_layers, nullptr);
   for (auto& e : h->gate_ev) LCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  h->acq_ev.assign(cfg->num_layers + 1, nullptr);
-  for (auto& e : h->acq_ev) LCUDA(cudaEventCreate(&e));
+  h->pre_ev.assign(cfg->num_layers, nullptr);
+  for (auto& e : h->pre_ev) LCUDA(cudaEventCreate(&e));
+  h->post_ev.assign(cfg->num_layers, nullptr);
+  for (auto& e : h->post_ev) LCUDA(cudaEventCreate(&e));
+  LCUDA(cudaEventCreate(&h->end_ev));
+  LCUDA(cudaEventCreate(&h->rnd_ev0));
+  LCUDA(cudaEventCreate(&h->rnd_ev1));
+  h->tune_ms.assign(kTuneCands, {});
   h->fwd_ms.assign(cfg->num_layers, 0.0);
   h->sched_sms.assign(cfg->num_layers, 0);
   if (const char* e = getenv("EDIT_SM_GBPS")) {
@@ -480,7 +491,7 @@ edit_status_t enqueue_step(edit_sync_t h, UnitPlan& p, int step) {
         f.on = h->dev_xchg ? 1 : 0;
         if (h->dev_xchg) f.x = xchg_args(h, ln, 1);
         launched += launch_rs(dt, p.pp, p.sl, p.anchor, ln.Down, scr, h->part2[layer], p.mode.peer_ctas,
-                              p.mode.smem_kb, f, st);
+                              p.mode.smem_kb, full_speed(h, p.mode), f, st);
         CUDA_TRY(h, cudaGetLastError());
         if (ev) CUDA_TRY(h, record_event(ev[3], st));
       } else if (N > 1) {
@@ -502,7 +513,7 @@ edit_status_t enqueue_step(edit_sync_t h, UnitPlan& p, int step) {
       break;
     case kStepUpdate:
       if (h->peer) {
-        launched += launch_ag_update(dt, p.u, p.pp, p.sl, p.mode.peer_ctas, p.mode.smem_kb, st);
+        launched += launch_ag_update(dt, p.u, p.pp, p.sl, p.mode.peer_ctas, p.mode.smem_kb, full_speed(h, p.mode), st);
       } else if (p.mode.part > 0 && !p.u.dbar && !p.gathered) {
         launched += launch_update_tma(dt, p.u, p.mode.part, st);
       } else {
@@ -683,7 +694,7 @@ edit_status_t edit_sync_workspace_bytes(const edit_sync_config_t* cfg, size_t* b
 // Settings every rank must agree on (slice layout, lane mapping, exchange protocol, units):
 // a digest of them is all-gathered at init and compared.
 struct ConfigDigest {
-  int32_t nlanes, peer_tile, dev_xchg, graph, algo, L, M, N, dtype, flags;
+  int32_t nlanes, peer_tile, dev_xchg, graph, algo, L, M, N, dtype, flags, peer_ldg, pad;
   uint64_t numel_hash;
 };
 
@@ -722,8 +733,12 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
       INIT_NCCL(ncclCommInitRank(&ln.global, K, u, cfg->rank));
       // every rank must agree on the settings that fix slice layout, lane mapping and the
       // exchange protocol (read per rank from the environment): compare digests
-      ConfigDigest mine{nlanes, h->peer_tile, h->dev_xchg ? 1 : 0, h->graph ? 1 : 0, cfg->algo, cfg->num_layers,
-                        h->M, h->N, cfg->param_dtype, (int32_t)cfg->flags, 1469598103934665603ull};
+      ConfigDigest mine;
+      memset(&mine, 0, sizeof mine);  // (padding too: the digests are compared bytewise)
+      const int32_t vals[11] = {nlanes, h->peer_tile, h->dev_xchg ? 1 : 0, h->graph ? 1 : 0, cfg->algo,
+                                cfg->num_layers, h->M, h->N, cfg->param_dtype, (int32_t)cfg->flags, h->peer_ldg};
+      memcpy(&mine, vals, sizeof vals);
+      mine.numel_hash = 1469598103934665603ull;
       for (int64_t x : h->numel) mine.numel_hash = (mine.numel_hash ^ (uint64_t)x) * 1099511628211ull;
       char* dev = nullptr;
       INIT_CUDA(cudaMalloc(&dev, sizeof(ConfigDigest) * (K + 1)));
@@ -1072,25 +1087,91 @@ static double unit_bytes_per_param(edit_sync_t h, int u) {
   return (bl + 4) + (direct ? 0 : bl) + (bl + 8.0 / h->N) + (20 + bl);
 }
 
-// Auto partition (the scheduler's default): the sync of unit u is enqueued when the forward
-// acquires unit u - depth and must be complete when it acquires u, so it overlaps the forward
-// of units u-depth .. u-1.  Give it the fewest SMs that stream its bytes in that time at the
-// measured per-SM rate (x1.25 margin): the forward keeps every other SM.  Without a measured
-// forward (first round) or with a forward too short to hide anything, all SMs.
-static int sched_auto_sms(edit_sync_t h, int u) {
-  if (!h->fwd_valid) return std::max(8, h->num_sms / 4);
+// ---------------------------------------------------------------- the scheduler's auto mode
+// A self-tuning controller over a few candidate plans, chosen per round by the measured
+// round time (compute stream, begin_round -> end_round; the caller's forward is the same work
+// every round, so the round time IS the objective):
+//   candidate 0 = serial: unit u's sync starts when the forward reaches acquire(u) (after the
+//                 forward of u-1) on full grids, and the forward of u waits for it -- no
+//                 overlap, never slower than running the two back to back;
+//   candidate c > 0 = partition: unit u's sync (enqueued depth units ahead) gets
+//                 f_c x the fewest SMs that stream its bytes within the forward time it
+//                 overlaps (units u-depth .. u-1, measured per unit between acquire calls)
+//                 at EDIT_SM_GBPS per SM; units < full_units keep full grids.
+// Each candidate is measured kTuneSamples times (serial first: it also measures the forward
+// cleanly), then the one with the lowest median round time is kept; if its newest sample
+// drifts > 15 % from its median (the workload changed) every candidate is re-measured.
+static const double kTuneFactors[kTuneCands] = {0.0, 1.0, 1.6, 2.5};
+
+static int partition_sms(edit_sync_t h, int u, double factor) {
   double budget_ms = 0.0;
   for (int k = std::max(0, u - h->sched_depth); k < u; ++k) budget_ms += h->fwd_ms[k];
   const double bytes = unit_bytes_per_param(h, u) * (double)h->numel[u];
   if (budget_ms <= 0.0) return h->num_sms;
-  const double sms = 1.25 * bytes / (h->sm_gbps * 1e9 * budget_ms * 1e-3);
+  const double sms = factor * bytes / (h->sm_gbps * 1e9 * budget_ms * 1e-3);
   return std::max(4, std::min(h->num_sms, (int)std::ceil(sms)));
 }
+
+static double median_of(std::vector<float> v) {
+  if (v.empty()) return 0.0;
+  std::sort(v.begin(), v.end());
+  const size_t n = v.size();
+  return n % 2 ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
+}
+
+// begin_round: fold the previous round's measurements in (without blocking: only if its
+// events have completed), then pick this round's candidate.
+static void tune_begin(edit_sync_t h) {
+  const int L = h->cfg.num_layers;
+  if (h->rnd_pending && cudaEventQuery(h->rnd_ev1) == cudaSuccess) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, h->rnd_ev0, h->rnd_ev1) == cudaSuccess && h->round_cand >= 0)
+      h->tune_ms[h->round_cand].push_back(ms);
+    bool ok = true;
+    for (int u = 0; u < L && ok; ++u) {
+      float f = 0.f;
+      ok = cudaEventElapsedTime(&f, h->post_ev[u], u + 1 < L ? h->pre_ev[u + 1] : h->end_ev) == cudaSuccess;
+      h->fwd_ms[u] = f;
+    }
+    // the forward times of a serial round are clean (nothing else runs next to them)
+    if (ok && (h->round_cand == 0 || !h->fwd_valid)) h->fwd_valid = true;
+    cudaGetLastError();  // (clear a failed elapsed-time query)
+    h->rnd_pending = false;
+  }
+  if (h->sched_part != kSchedAuto) {
+    h->round_cand = -1;
+    return;
+  }
+  int cand = -1;
+  if (!h->fwd_valid) {
+    cand = 0;  // measure the forward first
+  } else {
+    for (int c = 0; c < kTuneCands && cand < 0; ++c)
+      if ((int)h->tune_ms[c].size() < kTuneSamples) cand = c;
+    if (cand < 0) {
+      double best = 0.0;
+      for (int c = 0; c < kTuneCands; ++c) {
+        const double m = median_of(h->tune_ms[c]);
+        if (cand < 0 || m < best) {
+          cand = c;
+          best = m;
+        }
+      }
+      if (h->tune_ms[cand].back() > 1.15 * best)  // the workload changed: measure again
+        for (auto& v : h->tune_ms) v.clear();
+      for (auto& v : h->tune_ms)  // keep a sliding window
+        if (v.size() > 8) v.erase(v.begin(), v.begin() + (v.size() - 8));
+    }
+  }
+  h->round_cand = cand;
+}
+
+static bool round_serial(edit_sync_t h) { return h->sched_part == kSchedAuto && h->round_cand == 0; }
 
 static edit_status_t sched_enqueue_next(edit_sync_t h, cudaStream_t gate = nullptr) {
   const int u = h->sched_next_sync++;
   Lane& ln = h->lanes[u % h->lanes.size()];
-  if (gate && h->sched_gate) {
+  if (gate && (h->sched_gate || round_serial(h))) {
     CUDA_TRY(h, cudaEventRecord(h->gate_ev[u], gate));
     CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->gate_ev[u], 0));
   }
@@ -1102,8 +1183,8 @@ static edit_status_t sched_enqueue_next(edit_sync_t h, cudaStream_t gate = nullp
     // so each lane's kernels get an equal share of the sched_part SMs
     const int nl = (int)h->lanes.size();
     per = std::max(1, (h->sched_part + nl - 1) / nl);
-  } else if (h->sched_part == kSchedAuto && u >= h->sched_full_units) {
-    per = sched_auto_sms(h, u);
+  } else if (h->sched_part == kSchedAuto && h->round_cand > 0 && u >= h->sched_full_units) {
+    per = partition_sms(h, u, kTuneFactors[h->round_cand]);
   }
   if (per > 0) {
     mode.cap = 0;
@@ -1111,7 +1192,7 @@ static edit_status_t sched_enqueue_next(edit_sync_t h, cudaStream_t gate = nullp
     mode.smem_kb = 0;
     mode.part = per;
   }
-  h->sched_sms[u] = per;
+  h->sched_sms[u] = round_serial(h) ? -1 : per;
   UnitPlan p;
   TRY(plan_unit(h, ln, u, h->sched_local[u], h->sched_anchor[u], h->sched_mom[u], ln.stream, mode, p));
   const NvtxRange range(h->nvtx, "edit_sync unit %d (scheduled)", u);
@@ -1136,24 +1217,15 @@ edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* 
   h->sched_next_sync = 0;
   h->sched_next_acquire = 0;
   h->sched_active = true;
-  // auto partition: the previous round's per-unit forward times (acquire(u) -> acquire(u+1),
-  // the last unit -> end_round), if those events have completed (no host blocking)
-  if (h->sched_part == kSchedAuto && h->acq_ev.size() == (size_t)L + 1 &&
-      cudaEventQuery(h->acq_ev[L]) == cudaSuccess && h->sched_rounds > 0) {
-    bool ok = true;
-    for (int u = 0; u < L && ok; ++u) {
-      float ms = 0.f;
-      ok = cudaEventElapsedTime(&ms, h->acq_ev[u], h->acq_ev[u + 1]) == cudaSuccess;
-      h->fwd_ms[u] = ms;
-    }
-    h->fwd_valid = ok;
-    cudaGetLastError();  // (clear a failed elapsed-time query)
-  }
+  tune_begin(h);
+  cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
+  CUDA_TRY(h, cudaEventRecord(h->rnd_ev0, cs));
   // the side streams (lanes) start after everything already on the compute stream (the
   // inner steps that produced the locals)
-  CUDA_TRY(h, cudaEventRecord(h->fork, static_cast<cudaStream_t>(compute_stream)));
+  CUDA_TRY(h, cudaEventRecord(h->fork, cs));
   for (Lane& ln : h->lanes) CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->fork, 0));
-  while (h->sched_next_sync < std::min(depth, L)) TRY(sched_enqueue_next(h));
+  if (!round_serial(h))
+    while (h->sched_next_sync < std::min(depth, L)) TRY(sched_enqueue_next(h));
   return EDIT_OK;
 }
 
@@ -1163,14 +1235,18 @@ edit_status_t edit_sched_acquire(edit_sync_t h, int32_t layer, void* compute_str
   if (!h->sched_active) return fail(EDIT_ERR_INVALID_ARG, "no active round");
   if (layer != h->sched_next_acquire) return fail(EDIT_ERR_INVALID_ARG, "acquire units in order 0..L-1");
   const int L = h->cfg.num_layers;
+  cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
-  while (h->sched_next_sync <= layer) TRY(sched_enqueue_next(h));  // (depth can only lag if acquire skipped ahead)
-  CUDA_TRY(h, cudaStreamWaitEvent(static_cast<cudaStream_t>(compute_stream), h->done[layer], 0));
-  // (auto partition) the forward of unit `layer` starts here on the compute stream
-  CUDA_TRY(h, cudaEventRecord(h->acq_ev[layer], static_cast<cudaStream_t>(compute_stream)));
+  // the forward of unit layer-1 ends here on the compute stream (auto mode's measurement)
+  CUDA_TRY(h, cudaEventRecord(h->pre_ev[layer], cs));
+  // serial: the sync of `layer` starts only now (gated on the compute stream); otherwise it
+  // was enqueued `depth` units ahead (depth can only lag if acquire skipped ahead)
+  while (h->sched_next_sync <= layer) TRY(sched_enqueue_next(h, round_serial(h) ? cs : nullptr));
+  CUDA_TRY(h, cudaStreamWaitEvent(cs, h->done[layer], 0));
+  CUDA_TRY(h, cudaEventRecord(h->post_ev[layer], cs));  // the forward of `layer` starts here
   h->sched_next_acquire = layer + 1;
-  if (h->sched_next_sync < L && h->sched_next_sync <= layer + h->sched_depth)
-    TRY(sched_enqueue_next(h, static_cast<cudaStream_t>(compute_stream)));
+  if (!round_serial(h) && h->sched_next_sync < L && h->sched_next_sync <= layer + h->sched_depth)
+    TRY(sched_enqueue_next(h, cs));
   return EDIT_OK;
 }
 
@@ -1180,19 +1256,29 @@ edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream) {
   if (!h->sched_active) return fail(EDIT_ERR_INVALID_ARG, "no active round");
   const int L = h->cfg.num_layers;
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
-  while (h->sched_next_sync < L) TRY(sched_enqueue_next(h));
   cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
-  // (auto partition) the forward of the last unit ends here -- valid only if every unit was
-  // acquired in this round
-  if (h->sched_next_acquire == L) {
-    CUDA_TRY(h, cudaEventRecord(h->acq_ev[L], cs));
-    h->sched_rounds += 1;
-  }
+  const bool complete = h->sched_next_acquire == L;  // every unit acquired: the round is measurable
+  if (complete) CUDA_TRY(h, cudaEventRecord(h->end_ev, cs));
+  while (h->sched_next_sync < L) TRY(sched_enqueue_next(h, round_serial(h) ? cs : nullptr));
   for (Lane& ln : h->lanes) {
     CUDA_TRY(h, cudaEventRecord(ln.tail, ln.stream));
     CUDA_TRY(h, cudaStreamWaitEvent(cs, ln.tail, 0));
   }
+  if (complete) {
+    CUDA_TRY(h, cudaEventRecord(h->rnd_ev1, cs));
+    h->rnd_pending = true;
+  }
   h->sched_active = false;
+  return EDIT_OK;
+}
+
+edit_status_t edit_sched_get_plan(edit_sync_t h, int32_t* candidate, int32_t* sms, double* median_ms) {
+  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
+  if (candidate) *candidate = h->round_cand;
+  if (sms)
+    for (int u = 0; u < h->cfg.num_layers; ++u) sms[u] = h->sched_sms[u];
+  if (median_ms)
+    for (int c = 0; c < kTuneCands; ++c) median_ms[c] = median_of(h->tune_ms[c]);
   return EDIT_OK;
 }
 
@@ -1219,6 +1305,8 @@ edit_status_t edit_sched_set_partition(edit_sync_t h, int32_t sms, int32_t full_
     CUDA_TRY(h, cudaStreamCreateWithPriority(&ln.stream, cudaStreamNonBlocking, prio));
   }
   clear_graphs(h);  // captured rounds reference the old lane streams' work order
+  if (sms == kSchedAuto && h->sched_part != kSchedAuto)
+    for (auto& v : h->tune_ms) v.clear();  // re-tune from scratch
   h->sched_part = sms;
   h->sched_full_units = full_units;
   return EDIT_OK;
@@ -1420,7 +1508,11 @@ edit_status_t edit_sync_destroy(edit_sync_t h) {
     if (e) cudaEventDestroy(e);
   for (auto e : h->gate_ev)
     if (e) cudaEventDestroy(e);
-  for (auto e : h->acq_ev)
+  for (auto e : h->pre_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto e : h->post_ev)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {h->end_ev, h->rnd_ev0, h->rnd_ev1})
     if (e) cudaEventDestroy(e);
   for (auto e : h->prof)
     if (e) cudaEventDestroy(e);

@@ -54,7 +54,9 @@ struct RoundGraph {
 };
 
 // How a unit's kernels are shaped (default full grids; the scheduler's modes).
-constexpr int kSchedAuto = -1;  // edit_sched_set_partition(sms = -1): sized per unit from the forward
+constexpr int kSchedAuto = -1;  // edit_sched_set_partition(sms = -1): the self-tuning default
+constexpr int kTuneCands = 4;   // serial + 3 partition factors
+constexpr int kTuneSamples = 2; // rounds measured per candidate before choosing
 
 struct Mode {
   int cap = 0;        // max CTAs of the LDG streaming kernels (0 = full grid)
@@ -62,6 +64,12 @@ struct Mode {
   int smem_kb = 0;    // shared-memory ring of the TMA peer kernels (0 = default)
   int part = 0;       // > 0: partition mode, K1 / K4 / peer kernels on <= part persistent CTAs
 };
+
+// EDIT_PEER_KERNELS=ldg|ldg2|tma (default ldg): the RS and AG + update kernels of full-speed
+// rounds -- non-persistent LDG full grids (measured on 2 B200s, 7B unit, N = 2: AG 0.70 ms vs
+// 0.77 ms for the TMA pipeline; equal at N = 4 where both pull at the NVLink ceiling,
+// profiles/r2_peer_kbench_ag.txt) or the persistent warp-specialised TMA pipelines, which the
+// scheduler's partition / co-resident modes always use (capped grids).
 
 }  // namespace edit
 
@@ -77,6 +85,7 @@ struct edit_sync {
   int peer_ctas = 148;                // persistent grid of the peer kernels (EDIT_PEER_CTAS env overrides)
   int peer_tile = edit::kPeerTileVec; // vectors per TMA tile (EDIT_PEER_TILE env; must match on all ranks)
   bool dev_xchg = true;               // scalar chain over NVLink mailboxes (EDIT_XCHG=nccl: NCCL gathers)
+  int peer_ldg = 1;                   // EDIT_PEER_KERNELS: 0 tma, 1 ldg, 2 ldg2 (full-speed rounds)
   unsigned long long timeout_ns = 0;  // mailbox wait bound (EDIT_XCHG_TIMEOUT_S; 0 = forever)
   // sticky exchange error: device flag read by every exchange, and its mapped-host mirror the
   // library polls at every call (no device sync needed to notice a dead peer)
@@ -95,11 +104,17 @@ struct edit_sync {
   int sched_part = -1;
   int sched_full_units = 2;
   double sm_gbps = 100.0;
-  std::vector<cudaEvent_t> acq_ev;   // [L + 1] timing events on the compute stream at acquire / end
-  std::vector<double> fwd_ms;        // [L] forward time of each unit in the last measured round
+  // auto mode = a self-tuning choice among kTuneCands plans per round (api.cpp): timing events
+  // on the compute stream at each acquire (before / after its wait), at end_round, and around
+  // the whole round
+  std::vector<cudaEvent_t> pre_ev, post_ev;  // [L]
+  cudaEvent_t end_ev = nullptr, rnd_ev0 = nullptr, rnd_ev1 = nullptr;
+  bool rnd_pending = false;                  // a measurable round is in flight
+  std::vector<double> fwd_ms;                // [L] forward time of each unit (last measurement)
   bool fwd_valid = false;
-  int64_t sched_rounds = 0;          // completed scheduled rounds (all units acquired)
-  std::vector<int> sched_sms;        // [L] SMs given to each unit's sync in the current round
+  int round_cand = -1;                       // candidate of the current round (-1: fixed setting)
+  std::vector<std::vector<float>> tune_ms;   // [kTuneCands] measured round times
+  std::vector<int> sched_sms;                // [L] SMs given to each unit's sync (0 full grid, -1 serial)
   int lane_prio = 0;             // priority the lanes were created with (env default)
   // gate (EDIT_SCHED_GATE=1): the sync of unit u+depth starts only when the forward of unit
   // u may start (an event on the compute stream at acquire(u)), not as soon as its lane frees

@@ -165,18 +165,34 @@ int launch_pg_norm_copy(int dtype, const void* local, const float* anchor, void*
 // RS (peer_kernels.cu): Dbar = sum_j w_j (anchor - L_j) over this rank's slice, written to its D;
 // ||Dbar_slice||^2 -> scr->send2 (persistent grid <= max_ctas; cta_parts needs that many slots).
 // smem_kb > 0: shared-memory ring budget per CTA (tiles shrink to fit; co-resident mode).
+// ldg: 0 = the persistent TMA pipeline on <= max_ctas CTAs (smem_kb ring budget); 1 = the
+// non-persistent LDG full grid (2: two vectors per thread in AG) -- EDIT_PEER_KERNELS.
 int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anchor, float* Dmine,
-              LayerScratch* scr, double* cta_parts, int max_ctas, int smem_kb, const FoldArgs& f, cudaStream_t st);
+              LayerScratch* scr, double* cta_parts, int max_ctas, int smem_kb, int ldg, const FoldArgs& f,
+              cudaStream_t st);
 // AG + update: Dbar pulled from each slice's owner, then the K4 math on the whole shard.
 int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl, int max_ctas,
-                     int smem_kb, cudaStream_t st);
+                     int smem_kb, int ldg, cudaStream_t st);
 // Partition mode of the prefetch scheduler (peer_kernels.cu): K1 (no S, no copy) and the
 // N == 1 K4 as persistent TMA pipelines on <= max_ctas CTAs, each with the full ~200 KB
 // ring (one CTA per SM, no GEMM CTA beside it).
 int launch_pg_norm_tma(int dtype, const void* local, const float* anchor, int64_t n, LayerScratch* scr,
                        double* cta_parts, int max_ctas, const FoldArgs& f, cudaStream_t st);
 int launch_update_tma(int dtype, const UpdateArgs& a, int max_ctas, cudaStream_t st);
-inline int64_t rs_partial_slots(int64_t, int) { return kMaxPeerCtas; }
+// The LDG reduce-scatter's grid over a slice of `cnt` vectors: one CTA per kThreads x
+// kRsLdgIters vectors; its per-CTA partial slots are sized by rs_partial_slots.
+constexpr int kRsLdgIters = 4;
+inline int64_t rs_ldg_grid(int64_t cnt) {
+  const int64_t per = (int64_t)kThreads * kRsLdgIters;
+  const int64_t g = (cnt + per - 1) / per;
+  return g < 1 ? 1 : g;
+}
+inline int64_t rs_partial_slots(int64_t n, int N) {
+  const int64_t nv = (n + 7) / 8, slice = (nv + N - 1) / N + 4096;  // >= any tile-rounded slice
+  const int64_t g = rs_ldg_grid(slice);
+  return g > kMaxPeerCtas ? g : kMaxPeerCtas;
+}
+
 // Warm-up gradient all-reduce (mean) over the sync row, peer path (peer_kernels.cu).
 int launch_warm_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, void* Dmine, const int* err, cudaStream_t st);
 int launch_warm_ag(int dtype, const PeerPtrs& pp, const Slicing& sl, void* out, const int* err, cudaStream_t st);

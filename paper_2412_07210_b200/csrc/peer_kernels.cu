@@ -20,6 +20,7 @@
 #include <math.h>
 
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -151,6 +152,65 @@ __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_const
   if (finish_partials_n<kPeerThreads>(accd, cta_parts, &scr->counter2, &scr->send2) && f.on) fold_dbar_norm(f, scr);
 }
 
+// RS, LDG variant (the default of the full-speed rounds): a non-persistent full grid over this
+// rank's slice, CTA b owning vectors [b T I, (b+1) T I) of it; each thread loads its vector of
+// the anchor and of every member's local (16-B LDG, the peers' over NVLink; members with
+// w_j == 0 are not read, R9) before any arithmetic.  Same math and fixed member order as the
+// TMA kernel; per-CTA partials of ||Dbar||^2 added in CTA order by the last CTA.
+template <typename T, int I>
+__global__ void __launch_bounds__(kThreads) rs_ldg_kernel(const __grid_constant__ PeerPtrs pp, Slicing sl,
+                                                          const float* __restrict__ anchor, float* __restrict__ Dmine,
+                                                          LayerScratch* __restrict__ scr,
+                                                          double* __restrict__ cta_parts,
+                                                          const __grid_constant__ FoldArgs f) {
+  const int N = sl.N;
+  float w[EDIT_MAX_SYNC];
+#pragma unroll
+  for (int j = 0; j < EDIT_MAX_SYNC; ++j) w[j] = j < N ? scr->w_all[j] : 0.f;
+  const bool skip = scr->rollback != 0;  // rollback (l.449) or an aborted unit
+  const int64_t n8 = sl.n >> 3;
+  const int64_t s0 = (int64_t)sl.me * sl.slice;
+  const int64_t s1 = min(s0 + sl.slice, n8);
+  float acc = 0.f;
+  if (!skip) {
+#pragma unroll 1
+    for (int it = 0; it < I; ++it) {
+      const int64_t v = s0 + ((int64_t)blockIdx.x * I + it) * kThreads + threadIdx.x;
+      if (v < s1) {
+        float a[8], d[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        float l[EDIT_MAX_SYNC][8];
+        load8(anchor + 8 * v, a);
+#pragma unroll
+        for (int j = 0; j < EDIT_MAX_SYNC; ++j)
+          if (w[j] != 0.f) load8(static_cast<const T*>(pp.L[j]) + 8 * v, l[j]);
+#pragma unroll
+        for (int j = 0; j < EDIT_MAX_SYNC; ++j)
+          if (w[j] != 0.f) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) d[k] = fmaf(w[j], a[k] - l[j][k], d[k]);
+          }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc = fmaf(d[k], d[k], acc);
+        store8(Dmine + 8 * (v - s0), d);
+      }
+    }
+  }
+  double accd = (double)acc;
+  // the partial last vector (n % 8 elements) belongs to the owner of vector n8
+  const int64_t tail = sl.n & 7;
+  if (!skip && tail && n8 >= s0 && n8 < s0 + sl.slice && blockIdx.x == 0 && threadIdx.x < tail) {
+    const int64_t k = 8 * n8 + threadIdx.x;
+    const float a = anchor[k];
+    float d = 0.f;
+    for (int j = 0; j < N; ++j)
+      if (w[j] != 0.f) d = fmaf(w[j], a - load1(static_cast<const T*>(pp.L[j]) + k), d);
+    accd += (double)(d * d);
+    Dmine[k - 8 * s0] = d;
+  }
+  accd = block_sum(accd);
+  if (finish_partials(accd, cta_parts, &scr->counter2, &scr->send2) && f.on) fold_dbar_norm(f, scr);
+}
+
 // ------------------------------------------------------------------------------ AG + update
 template <typename T, bool kG>
 __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs p,
@@ -276,6 +336,105 @@ __global__ void __launch_bounds__(kPeerThreads) ag_update_tma_kernel(UpdateArgs 
     anchor[k] = a1;
     store1(local + k, a1);
     if (kG) gather_store1_t<T>(p, k, a1);
+  }
+}
+
+// AG + update, LDG variant (EDIT_AG=ldg): a non-persistent full grid like K4 -- each CTA
+// one chunk of kThreads x U vectors inside one owner's slice, Dbar loaded straight from the
+// owner (16-B LDG over NVLink, no shared-memory staging), anchor / momentum from local HBM.
+// Chunks are dealt owner-interleaved (block b -> owner (b + me) mod N), so the CTAs resident
+// at any moment pull from every owner at once.
+template <typename T, bool kG, int U>
+__global__ void __launch_bounds__(kThreads) ag_update_ldg_kernel(UpdateArgs p, const __grid_constant__ PeerPtrs pp,
+                                                                 Slicing sl) {
+  __shared__ float s_beta;
+  __shared__ int s_rollback;
+  T* __restrict__ local = static_cast<T*>(p.local);
+  float* __restrict__ anchor = p.anchor;
+  float* __restrict__ mom = p.momentum;
+  if (threadIdx.x == 0) {  // Eq. 4 once per CTA (fp64)
+    double gsq = 0.0;
+    for (int i = 0; i < p.n_gparts; ++i) gsq += p.gparts[i];
+    const double gbar = sqrt(gsq);
+    double beta_d = p.phi / (gbar + p.eps);
+    beta_d = beta_d < 1.0 ? beta_d : 1.0;
+    if (p.flags & EDIT_NO_GC) beta_d = 1.0;
+    const int rb = *p.rollback;
+    if (blockIdx.x == 0 && rb != kAbort) {
+      p.rec->G_bar = rb ? 0.0 : gbar;
+      p.rec->beta = rb ? 1.0 : beta_d;
+      p.rec->rollback = rb;
+      p.rec->round += 1;
+    }
+    s_beta = (float)beta_d;
+    s_rollback = rb;
+  }
+  __syncthreads();
+  if (s_rollback == kAbort) return;
+  const float beta = s_beta, mu = p.mu, nu = p.nu;
+  const int64_t n8 = p.n >> 3;
+  const int N = sl.N;
+  if (s_rollback) {  // Alg. 2 l.449: local = rne(anchor)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += stride) {
+      float a[8];
+      load8(anchor + 8 * i, a);
+      store8(local + 8 * i, a);
+      if (kG) gather_store8_t<false, T>(p, 8 * i, a, 0);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (p.n & 7)) {
+      const int64_t k = 8 * n8 + threadIdx.x;
+      store1(local + k, anchor[k]);
+      if (kG) gather_store1_t<T>(p, k, anchor[k]);
+    }
+    return;
+  }
+  const int64_t cv = (int64_t)kThreads * U;
+  const int64_t cps = (sl.slice + cv - 1) / cv;  // chunks per slice
+  const int owner = (int)((blockIdx.x % N + sl.me) % N);
+  const int64_t k = blockIdx.x / N;
+  const int64_t s_lo = (int64_t)owner * sl.slice;
+  const int64_t v_lo = s_lo + k * cv;
+  const int64_t v_hi = min(min(v_lo + cv, s_lo + sl.slice), n8);
+  const float* __restrict__ D = pp.D[owner] - 8 * s_lo;  // indexed by the global vector
+  (void)cps;
+  float d[U][8], a[U][8], m[U][8];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t v = v_lo + threadIdx.x + (int64_t)u * kThreads;
+    if (v < v_hi) {
+      load8(D + 8 * v, d[u]);
+      load8(anchor + 8 * v, a[u]);
+      load8(mom + 8 * v, m[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t v = v_lo + threadIdx.x + (int64_t)u * kThreads;
+    if (v < v_hi) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float g = beta * d[u][j];               // Eq. 5
+        m[u][j] = fmaf(mu, m[u][j], g);               // m' = mu m + g
+        a[u][j] = a[u][j] - nu * fmaf(mu, m[u][j], g);  // a' = a - nu (g + mu m')
+      }
+      store8(mom + 8 * v, m[u]);
+      store8(anchor + 8 * v, a[u]);
+      store8(local + 8 * v, a[u]);
+      if (kG) gather_store8_t<false, T>(p, 8 * v, a[u], 0);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (p.n & 7)) {  // partial last vector
+    const int64_t kk = 8 * n8 + threadIdx.x;
+    const int64_t j = n8 / sl.slice;
+    const float dk = pp.D[j][kk - 8 * j * sl.slice];
+    const float g = beta * dk;
+    const float m1 = fmaf(mu, mom[kk], g);
+    const float a1 = anchor[kk] - nu * fmaf(mu, m1, g);
+    mom[kk] = m1;
+    anchor[kk] = a1;
+    store1(local + kk, a1);
+    if (kG) gather_store1_t<T>(p, kk, a1);
   }
 }
 
@@ -533,6 +692,10 @@ __global__ void xchg_kernel(const __grid_constant__ XchgArgs x, const double* sr
   }
 }
 
+}  // namespace
+
+namespace {
+
 int default_smem_budget() {
   static int b = [] {
     const char* e = getenv("EDIT_PEER_SMEM_KB");  // shared-memory ring per CTA (default 200 KB)
@@ -573,7 +736,17 @@ void rs_go(unsigned grid, const Ring& r, cudaStream_t st, const PeerPtrs& pp, co
 }
 
 int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anchor, float* Dmine,
-              LayerScratch* scr, double* cta_parts, int max_ctas, int smem_kb, const FoldArgs& f, cudaStream_t st) {
+              LayerScratch* scr, double* cta_parts, int max_ctas, int smem_kb, int ldg, const FoldArgs& f,
+              cudaStream_t st) {
+  if (ldg) {  // full-speed rounds: LDG
+    const int64_t n8 = sl.n >> 3;
+    const int64_t s0 = (int64_t)sl.me * sl.slice;
+    const int64_t cnt = std::max<int64_t>(0, std::min(s0 + sl.slice, n8) - s0);
+    const unsigned grid = (unsigned)rs_ldg_grid(cnt);
+    if (dtype == EDIT_BF16) rs_ldg_kernel<__nv_bfloat16, kRsLdgIters><<<grid, kThreads, 0, st>>>(pp, sl, anchor, Dmine, scr, cta_parts, f);
+    else rs_ldg_kernel<float, kRsLdgIters><<<grid, kThreads, 0, st>>>(pp, sl, anchor, Dmine, scr, cta_parts, f);
+    return 1;
+  }
   const int esz = dtype == EDIT_BF16 ? 2 : 4;
   const Ring r = ring_for(sl.tile, 8 * (4 + sl.N * esz), smem_kb);
   const int64_t n8 = sl.n >> 3;
@@ -597,8 +770,28 @@ void ag_go(unsigned grid, const Ring& r, cudaStream_t st, const UpdateArgs& a, c
   }
 }
 
+template <typename T, int U>
+void ag_ldg_go(cudaStream_t st, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl) {
+  const int64_t cv = (int64_t)kThreads * U;
+  const int64_t cps = (sl.slice + cv - 1) / cv;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, (int64_t)sl.N * cps);
+  if (a.gather_M > 0) ag_update_ldg_kernel<T, true, U><<<grid, kThreads, 0, st>>>(a, pp, sl);
+  else ag_update_ldg_kernel<T, false, U><<<grid, kThreads, 0, st>>>(a, pp, sl);
+}
+
+
 int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const Slicing& sl, int max_ctas,
-                     int smem_kb, cudaStream_t st) {
+                     int smem_kb, int ldg, cudaStream_t st) {
+  if (ldg) {
+    if (dtype == EDIT_BF16) {
+      if (ldg == 2) ag_ldg_go<__nv_bfloat16, 2>(st, a, pp, sl);
+      else ag_ldg_go<__nv_bfloat16, 1>(st, a, pp, sl);
+    } else {
+      if (ldg == 2) ag_ldg_go<float, 2>(st, a, pp, sl);
+      else ag_ldg_go<float, 1>(st, a, pp, sl);
+    }
+    return 1;
+  }
   const Ring r = ring_for(sl.tile, 8 * 12, smem_kb);
   const int64_t nq = (int64_t)sl.N * (sl.slice / r.V);
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nq, max_ctas));

@@ -25,7 +25,7 @@ NO_AE, NO_WA, NO_GC = 1, 2, 4
 EXPORTED = ("edit_sync_get_unique_id", "edit_sync_workspace_bytes", "edit_sync_init", "edit_layer_sync",
             "edit_layer_sync_host", "edit_sync_host_wait", "edit_sync_round", "edit_sync_register_locals",
             "edit_warmup_allreduce", "edit_sync_register_gather", "edit_sched_begin_round", "edit_sched_acquire",
-            "edit_sched_end_round", "edit_sched_set_partition",
+            "edit_sched_end_round", "edit_sched_set_partition", "edit_sched_get_plan",
             "edit_sync_stats", "edit_sync_get_state", "edit_sync_set_state", "edit_sync_kernel_launches",
             "edit_sync_set_profiling", "edit_sync_profile_collect", "edit_trigger_create", "edit_trigger_sync_now",
             "edit_trigger_in_warmup", "edit_trigger_mark_synced", "edit_trigger_syncs", "edit_trigger_destroy",
@@ -90,6 +90,7 @@ def load_library() -> ctypes.CDLL:
     lib.edit_sched_acquire.argtypes, lib.edit_sched_acquire.restype = [P, I32, P], S
     lib.edit_sched_end_round.argtypes, lib.edit_sched_end_round.restype = [P, P], S
     lib.edit_sched_set_partition.argtypes, lib.edit_sched_set_partition.restype = [P, I32, I32], S
+    lib.edit_sched_get_plan.argtypes, lib.edit_sched_get_plan.restype = [P, P, P, P], S
     lib.edit_sync_stats.argtypes = [P, I32, ctypes.POINTER(LayerStatsC)]
     lib.edit_sync_stats.restype = S
     lib.edit_sync_get_state.argtypes = [P, P, ctypes.POINTER(ctypes.c_size_t)]
@@ -253,6 +254,19 @@ class EditSync:
         persistent TMA CTAs (one per SM) while the forward keeps the other SMs.  sms = -1
         (default): sized per unit from the measured forward; > 0: fixed; 0: full grids."""
         _check(self._lib.edit_sched_set_partition(self._h, int(sms), int(full_units)))
+
+    PLAN_CANDIDATES = ("serial", "partition x1.0", "partition x1.6", "partition x2.5")
+
+    def sched_plan(self) -> dict:
+        """The scheduler's last-round plan (edit_sched_get_plan): the auto mode's candidate,
+        the SMs each unit's sync got (0 full grid, -1 serial), median round ms per candidate."""
+        cand = ctypes.c_int32()
+        sms = (ctypes.c_int32 * self.num_layers)()
+        med = (ctypes.c_double * 4)()
+        _check(self._lib.edit_sched_get_plan(self._h, ctypes.byref(cand), sms, med))
+        c = cand.value
+        return {"candidate": self.PLAN_CANDIDATES[c] if 0 <= c < 4 else "fixed", "sms_per_unit": list(sms),
+                "median_round_ms": dict(zip(self.PLAN_CANDIDATES, list(med)))}
 
     def _check_round(self, locals_, anchors, momenta):
         L = self.num_layers

@@ -208,14 +208,37 @@ def test_sim_mesh_parity(mesh, dtype, config, api):
         assert outs[0].anomalous[0] and np.allclose(outs[0].w[1:], 1.0 / (N - 1))
 
 
+TMA_CASES = [("2x2", "f32", "toy", "unit"), ("1x4", "bf16", "ragged", "round"), ("1x2", "bf16", "wrap", "reg"),
+             ("2x4", "bf16", "nan", "gather"), ("1x8", "bf16", "rollback", "round")]
+
+
+@pytest.mark.parametrize("mesh,dtype,config,api", TMA_CASES, ids=["-".join(c) for c in TMA_CASES])
+def test_sim_mesh_parity_tma_peer_kernels(mesh, dtype, config, api):
+    # the persistent TMA RS / AG pipelines at full grids (EDIT_PEER_KERNELS=tma; the default
+    # full-speed kernels are the LDG ones, the TMA ones also serve the scheduler's partition mode)
+    os.environ["EDIT_PEER_KERNELS"] = "tma"
+    try:
+        c = MeshCase(mesh, dtype, config)
+    finally:
+        os.environ.pop("EDIT_PEER_KERNELS", None)
+    try:
+        c.run(api)
+        c.check(api)
+    finally:
+        c.close()
+
+
 def test_sim_mesh_two_rounds_and_ring_wrap_small_grid():
-    # EDIT_PEER_CTAS=8: a 1M-element unit needs ~15 RS tiles and ~30 AG tiles per CTA, so both
-    # mbarrier rings wrap several times; then a second round on the updated state
+    # EDIT_PEER_KERNELS=tma, EDIT_PEER_CTAS=8: a 1M-element unit needs ~15 RS tiles and ~30 AG
+    # tiles per CTA, so both mbarrier rings wrap several times; then a second round on the
+    # updated state
     os.environ["EDIT_PEER_CTAS"] = "8"
+    os.environ["EDIT_PEER_KERNELS"] = "tma"   # the persistent TMA pipelines (partition mode's kernels)
     try:
         c = MeshCase("1x4", "bf16", "ragged")
     finally:
         os.environ.pop("EDIT_PEER_CTAS", None)
+        os.environ.pop("EDIT_PEER_KERNELS", None)
     try:
         c.run("round")
         c.check("round")

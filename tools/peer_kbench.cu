@@ -65,7 +65,7 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&mom[g], n * 4));
     CK(cudaMalloc(&D[g], sl0.slice * 8 * 4));
     CK(cudaMalloc(&scr[g], sizeof(LayerScratch)));
-    CK(cudaMalloc(&parts[g], kMaxPeerCtas * sizeof(double)));
+    CK(cudaMalloc(&parts[g], rs_partial_slots(n, N) * sizeof(double)));
     CK(cudaMalloc(&gparts[g], 8 * sizeof(double)));
     CK(cudaMalloc(&rec[g], sizeof(edit_layer_stats_t)));
     CK(cudaMemset(gparts[g], 0, 8 * sizeof(double)));
@@ -84,6 +84,8 @@ int main(int argc, char** argv) {
     pp.D[g] = D[g];
   }
   const bool local_only = argc > 6 && atoi(argv[6]) != 0;
+  const char* ke = getenv("EDIT_PEER_KERNELS");  // as the library: ldg (default) | ldg2 | tma
+  const int kern = ke && !strcmp(ke, "tma") ? 0 : ke && !strcmp(ke, "ldg2") ? 2 : 1;
   std::vector<float> rs_ms(N, 0.f), ag_ms(N, 0.f);
   FoldArgs nofold{};
   for (int r = 0; r < reps + 1; ++r) {
@@ -94,7 +96,7 @@ int main(int argc, char** argv) {
       CK(cudaEventCreate(&e1[g]));
       CK(cudaEventCreate(&e2[g]));
       CK(cudaEventRecord(e0[g], st[g]));
-      launch_rs(EDIT_BF16, pp, slicing_of(n, N, g, tile), anchor[g], D[g], scr[g], parts[g], ctas, 0, nofold, st[g]);
+      launch_rs(EDIT_BF16, pp, slicing_of(n, N, g, tile), anchor[g], D[g], scr[g], parts[g], ctas, 0, kern, nofold, st[g]);
       CK(cudaEventRecord(e1[g], st[g]));
     }
     for (int g = 0; g < N; ++g) {  // the barrier the scalar exchange provides in the library
@@ -120,7 +122,7 @@ int main(int argc, char** argv) {
       PeerPtrs pa = pp;
       if (local_only)
         for (int j = 0; j < N; ++j) pa.D[j] = D[g];
-      launch_ag_update(EDIT_BF16, a, pa, slicing_of(n, N, g, tile), ctas, 0, st[g]);
+      launch_ag_update(EDIT_BF16, a, pa, slicing_of(n, N, g, tile), ctas, 0, kern, st[g]);
       CK(cudaEventRecord(e2[g], st[g]));
     }
     for (int g = 0; g < N; ++g) {
@@ -138,9 +140,9 @@ int main(int argc, char** argv) {
   }
   for (int g = 0; g < N; ++g) {
     const double nvl_rs = 2.0 * n * (N - 1) / N, nvl_ag = 4.0 * n * (N - 1) / N;
-    printf("N=%d tile=%d ctas=%d gpu %d: RS %.3f ms (NVLink in %.0f GB/s, HBM %.0f GB/s)  AG %.3f ms (NVLink in %.0f "
+    printf("%s N=%d tile=%d ctas=%d gpu %d: RS %.3f ms (NVLink in %.0f GB/s, HBM %.0f GB/s)  AG %.3f ms (NVLink in %.0f "
            "GB/s, HBM %.0f GB/s incl. served D, %.0f GB/s algorithmic 20 B)\n",
-           N, tile, ctas, g, rs_ms[g], nvl_rs / rs_ms[g] / 1e6, (2.0 + 8.0 / N) * n / rs_ms[g] / 1e6, ag_ms[g],
+           kern == 0 ? "tma" : kern == 2 ? "ldg2" : "ldg", N, tile, ctas, g, rs_ms[g], nvl_rs / rs_ms[g] / 1e6, (2.0 + 8.0 / N) * n / rs_ms[g] / 1e6, ag_ms[g],
            nvl_ag / ag_ms[g] / 1e6, 22.0 * n / ag_ms[g] / 1e6, 20.0 * n / ag_ms[g] / 1e6);
   }
   return 0;
