@@ -565,8 +565,8 @@ def main() -> None:
             for sms in parts:
                 sync.set_partition(sms, args.full_units)
                 for depth in (1, 2):
-                    # warm-up rounds: the auto mode (-1) tunes itself over its first 8 rounds
-                    for _ in range(9 if sms == -1 else 1):
+                    # warm-up rounds: the auto mode (-1) tunes itself over its first 12 rounds
+                    for _ in range(13 if sms == -1 else 1):
                         once(fwd_and_sync(depth), True)
                     # paired measurement: the forward alone and forward + sync back to back, the
                     # exposed sync time = the median of the pair differences (the forward runs
@@ -612,7 +612,7 @@ def main() -> None:
                             "persistent TMA CTAs, one per SM; -1 = auto, the library default: per unit the fewest SMs that "
                             "finish its sync within the forward it overlaps, measured in the previous round); "
                             "h = 1 - exposed / t_sync_alone, exposed = median over pairs of (fwd+sync) - (fwd alone) run back to "
-                            "back; the auto mode is measured after its 8 tuning rounds")}
+                            "back; the auto mode is measured after its 12 tuning rounds")}
 
     # NEXT-3: warm-up gradient all-reduce (mean over the sync group) of a full set of bf16
     # gradient shards, library path vs torch.distributed/NCCL all_reduce on the same group

@@ -245,13 +245,14 @@ edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream);
  *   sms == -1 (the DEFAULT, "auto"): self-tuning.  Each round runs one of four plans and
  *     is timed on the compute stream (begin_round -> end_round): SERIAL (unit u's sync starts
  *     when the forward reaches acquire(u), on full grids: no overlap, i.e. never slower than
- *     the two back to back) or PARTITION with f = 1.0 / 1.6 / 2.5 x the fewest SMs that
- *     stream unit u's bytes within the forward time its sync overlaps (units u-depth .. u-1,
- *     measured per unit between acquire calls; EDIT_SM_GBPS, default 100 GB/s per SM, the
- *     measured per-SM streaming rate), in [4, #SMs].  Every plan is measured twice (serial
- *     first), then the fastest median is kept; a > 15 % drift of its newest round time
- *     re-measures all.  So after 8 rounds the default is the best of serial and the
- *     partitions for this forward (edit_sched_get_plan reports the choice).
+ *     the two back to back) or PARTITION with (f, depth) = (1.0, >= 2), (1.6, >= 2),
+ *     (1.0, the caller's depth): f x the fewest SMs that stream unit u's bytes within the
+ *     forward time its sync overlaps (units u-depth .. u-1, measured per unit between acquire
+ *     calls; EDIT_SM_GBPS, default 100 GB/s per SM, the measured per-SM streaming rate), in
+ *     [4, #SMs].  Every plan is measured 3 times (serial first), then the fastest median is
+ *     kept; a > 15 % drift of its newest round time re-measures all.  So after 12 rounds the
+ *     default is the best of serial and the partitions for this forward (edit_sched_get_plan
+ *     reports the choice).  The depth passed to begin_round is a minimum in this mode.
  *   sms > 0: fixed, ceil(sms / lanes) CTAs per lane's kernels (the lanes run concurrently).
  *   sms == 0: full grids at the lowest stream priority (the sync fills what the forward
  *     leaves free; measured worse than serial on a tensor-bound forward, DESIGN 7).
@@ -263,7 +264,7 @@ edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream);
 edit_status_t edit_sched_set_partition(edit_sync_t h, int32_t sms, int32_t full_units);
 /* The scheduler's plan of its last round (host values, no device sync): *candidate = -1 for a
  * fixed setting (sms >= 0), else the auto mode's choice: 0 = serial, 1..3 = partition with
- * 1.0 / 1.6 / 2.5 x the minimum SMs; sms[u] (nullable, [L]) = SMs given to unit u's sync
+ * (1.0, depth >= 2) / (1.6, depth >= 2) / (1.0, caller's depth) x the minimum SMs; sms[u] (nullable, [L]) = SMs given to unit u's sync
  * (0 = full grid, -1 = serial); median_ms (nullable, [4]) = the measured median round time of
  * each candidate so far (0 = not measured). */
 edit_status_t edit_sched_get_plan(edit_sync_t h, int32_t* candidate, int32_t* sms, double* median_ms);

@@ -243,7 +243,8 @@ edit_status_t create_local(const edit_sync_config_t* cfg, void* workspace, size_
   h->peer_ctas = h->num_sms;
   if (const char* e = getenv("EDIT_XCHG")) h->dev_xchg = strcmp(e, "nccl") != 0;
   if (const char* e = getenv("EDIT_GRAPH")) h->graph = atoi(e) != 0;
-  if (const char* e = getenv("EDIT_PEER_KERNELS")) h->peer_ldg = !strcmp(e, "tma") ? 0 : !strcmp(e, "ldg2") ? 2 : 1;
+  if (const char* e = getenv("EDIT_PEER_KERNELS"))
+    h->peer_ldg = !strcmp(e, "tma") ? 0 : !strcmp(e, "ldg2") ? 3 : !strcmp(e, "ldgall") ? 5 : 1;
   if (const char* e = getenv("EDIT_NVTX")) h->nvtx = atoi(e) != 0;
   if (const char* e = getenv("EDIT_PEER_TILE")) {
     const int v = atoi(e);
@@ -1094,14 +1095,16 @@ static double unit_bytes_per_param(edit_sync_t h, int u) {
 //   candidate 0 = serial: unit u's sync starts when the forward reaches acquire(u) (after the
 //                 forward of u-1) on full grids, and the forward of u waits for it -- no
 //                 overlap, never slower than running the two back to back;
-//   candidate c > 0 = partition: unit u's sync (enqueued depth units ahead) gets
-//                 f_c x the fewest SMs that stream its bytes within the forward time it
-//                 overlaps (units u-depth .. u-1, measured per unit between acquire calls)
-//                 at EDIT_SM_GBPS per SM; units < full_units keep full grids.
+//   candidate c > 0 = partition: unit u's sync (enqueued depth_c units ahead, depth_c =
+//                 max(caller's depth, 2, 2, 1 for c = 1, 2, 3)) gets f_c = 1.0, 1.6, 1.0 x the
+//                 fewest SMs that stream its bytes within the forward time it overlaps (units
+//                 u-depth_c .. u-1, measured per unit between acquire calls) at EDIT_SM_GBPS
+//                 per SM; units < full_units keep full grids.
 // Each candidate is measured kTuneSamples times (serial first: it also measures the forward
 // cleanly), then the one with the lowest median round time is kept; if its newest sample
 // drifts > 15 % from its median (the workload changed) every candidate is re-measured.
-static const double kTuneFactors[kTuneCands] = {0.0, 1.0, 1.6, 2.5};
+static const double kTuneFactors[kTuneCands] = {0.0, 1.0, 1.6, 1.0};
+static const int kTuneMinDepth[kTuneCands] = {1, 2, 2, 1};  // prefetch depth >= this (and >= the caller's)
 
 static int partition_sms(edit_sync_t h, int u, double factor) {
   double budget_ms = 0.0;
@@ -1213,11 +1216,11 @@ edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* 
   h->sched_local.assign(locals, locals + L);
   h->sched_anchor.assign(anchors, anchors + L);
   h->sched_mom.assign(momenta, momenta + L);
-  h->sched_depth = depth;
   h->sched_next_sync = 0;
   h->sched_next_acquire = 0;
   h->sched_active = true;
   tune_begin(h);
+  h->sched_depth = h->round_cand > 0 ? std::max(depth, kTuneMinDepth[h->round_cand]) : depth;
   cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
   CUDA_TRY(h, cudaEventRecord(h->rnd_ev0, cs));
   // the side streams (lanes) start after everything already on the compute stream (the

@@ -55,8 +55,8 @@ struct RoundGraph {
 
 // How a unit's kernels are shaped (default full grids; the scheduler's modes).
 constexpr int kSchedAuto = -1;  // edit_sched_set_partition(sms = -1): the self-tuning default
-constexpr int kTuneCands = 4;   // serial + 3 partition factors
-constexpr int kTuneSamples = 2; // rounds measured per candidate before choosing
+constexpr int kTuneCands = 4;   // serial + 3 partition plans
+constexpr int kTuneSamples = 3; // rounds measured per candidate before choosing
 
 struct Mode {
   int cap = 0;        // max CTAs of the LDG streaming kernels (0 = full grid)
@@ -65,11 +65,13 @@ struct Mode {
   int part = 0;       // > 0: partition mode, K1 / K4 / peer kernels on <= part persistent CTAs
 };
 
-// EDIT_PEER_KERNELS=ldg|ldg2|tma (default ldg): the RS and AG + update kernels of full-speed
-// rounds -- non-persistent LDG full grids (measured on 2 B200s, 7B unit, N = 2: AG 0.70 ms vs
-// 0.77 ms for the TMA pipeline; equal at N = 4 where both pull at the NVLink ceiling,
-// profiles/r2_peer_kbench_ag.txt) or the persistent warp-specialised TMA pipelines, which the
-// scheduler's partition / co-resident modes always use (capped grids).
+// EDIT_PEER_KERNELS=ldg|ldg2|ldgall|tma (default ldg): the kernels of full-speed rounds.
+// ldg: AG + update as a non-persistent LDG full grid (measured on 2 B200s, 7B unit, N = 2:
+// 0.70 ms vs 0.77 ms for the TMA pipeline; equal at N = 4 where both pull at the NVLink
+// ceiling, profiles/r2_peer_kbench_ag.txt), RS as the persistent TMA pipeline; ldg2: 2 vectors
+// per thread in AG; ldgall: RS as an LDG full grid too (slower in full rounds); tma: both as
+// the persistent warp-specialised TMA pipelines, which the scheduler's partition and
+// co-resident modes always use (capped grids).  Bits: 1 = AG LDG, 2 = 2 vectors, 4 = RS LDG.
 
 }  // namespace edit
 
@@ -85,7 +87,7 @@ struct edit_sync {
   int peer_ctas = 148;                // persistent grid of the peer kernels (EDIT_PEER_CTAS env overrides)
   int peer_tile = edit::kPeerTileVec; // vectors per TMA tile (EDIT_PEER_TILE env; must match on all ranks)
   bool dev_xchg = true;               // scalar chain over NVLink mailboxes (EDIT_XCHG=nccl: NCCL gathers)
-  int peer_ldg = 1;                   // EDIT_PEER_KERNELS: 0 tma, 1 ldg, 2 ldg2 (full-speed rounds)
+  int peer_ldg = 1;                   // EDIT_PEER_KERNELS bits (full-speed rounds): 1 AG LDG, 2 x2, 4 RS LDG
   unsigned long long timeout_ns = 0;  // mailbox wait bound (EDIT_XCHG_TIMEOUT_S; 0 = forever)
   // sticky exchange error: device flag read by every exchange, and its mapped-host mirror the
   // library polls at every call (no device sync needed to notice a dead peer)

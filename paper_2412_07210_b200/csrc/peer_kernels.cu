@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_const
   if (finish_partials_n<kPeerThreads>(accd, cta_parts, &scr->counter2, &scr->send2) && f.on) fold_dbar_norm(f, scr);
 }
 
-// RS, LDG variant (the default of the full-speed rounds): a non-persistent full grid over this
+// RS, LDG variant (EDIT_PEER_KERNELS=ldgall, experimental): a non-persistent full grid over this
 // rank's slice, CTA b owning vectors [b T I, (b+1) T I) of it; each thread loads its vector of
 // the anchor and of every member's local (16-B LDG, the peers' over NVLink; members with
 // w_j == 0 are not read, R9) before any arithmetic.  Same math and fixed member order as the
@@ -738,7 +738,8 @@ void rs_go(unsigned grid, const Ring& r, cudaStream_t st, const PeerPtrs& pp, co
 int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anchor, float* Dmine,
               LayerScratch* scr, double* cta_parts, int max_ctas, int smem_kb, int ldg, const FoldArgs& f,
               cudaStream_t st) {
-  if (ldg) {  // full-speed rounds: LDG
+  if (ldg & 4) {  // EDIT_PEER_KERNELS=ldgall: the LDG reduce-scatter (measured slower than the
+                  // TMA pipeline in full rounds: one vector's loads in flight per thread)
     const int64_t n8 = sl.n >> 3;
     const int64_t s0 = (int64_t)sl.me * sl.slice;
     const int64_t cnt = std::max<int64_t>(0, std::min(s0 + sl.slice, n8) - s0);
@@ -784,10 +785,10 @@ int launch_ag_update(int dtype, const UpdateArgs& a, const PeerPtrs& pp, const S
                      int smem_kb, int ldg, cudaStream_t st) {
   if (ldg) {
     if (dtype == EDIT_BF16) {
-      if (ldg == 2) ag_ldg_go<__nv_bfloat16, 2>(st, a, pp, sl);
+      if (ldg & 2) ag_ldg_go<__nv_bfloat16, 2>(st, a, pp, sl);
       else ag_ldg_go<__nv_bfloat16, 1>(st, a, pp, sl);
     } else {
-      if (ldg == 2) ag_ldg_go<float, 2>(st, a, pp, sl);
+      if (ldg & 2) ag_ldg_go<float, 2>(st, a, pp, sl);
       else ag_ldg_go<float, 1>(st, a, pp, sl);
     }
     return 1;

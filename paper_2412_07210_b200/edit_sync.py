@@ -255,7 +255,7 @@ class EditSync:
         (default): sized per unit from the measured forward; > 0: fixed; 0: full grids."""
         _check(self._lib.edit_sched_set_partition(self._h, int(sms), int(full_units)))
 
-    PLAN_CANDIDATES = ("serial", "partition x1.0", "partition x1.6", "partition x2.5")
+    PLAN_CANDIDATES = ("serial", "partition x1.0 depth>=2", "partition x1.6 depth>=2", "partition x1.0")
 
     def sched_plan(self) -> dict:
         """The scheduler's last-round plan (edit_sched_get_plan): the auto mode's candidate,

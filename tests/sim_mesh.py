@@ -60,6 +60,11 @@ class SimMesh:
                               outer_momentum, clip_threshold, clip_eps, anomaly_threshold, ema_alpha,
                               int(ema_warmup_rounds), int(flags), 0)
         plib = es.load_library()
+        # the members' exchange kernels wait on each other from different streams of this one
+        # context; the library's step-major enqueue keeps every wait satisfiable, and a short
+        # exchange timeout turns any unforeseen non-concurrency into a fast test failure (the
+        # first timeout poisons the handles: later exchanges return at once) instead of a hang
+        os.environ.setdefault("EDIT_XCHG_TIMEOUT_S", "60")
         nbytes = ctypes.c_size_t()
         es._check(plib.edit_sync_workspace_bytes(ctypes.byref(self._cfg), ctypes.byref(nbytes)))
         self.workspaces = [torch.empty(nbytes.value, dtype=torch.uint8, device=self.device) for _ in range(self.K)]

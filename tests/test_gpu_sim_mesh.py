@@ -228,6 +228,21 @@ def test_sim_mesh_parity_tma_peer_kernels(mesh, dtype, config, api):
         c.close()
 
 
+@pytest.mark.parametrize("mesh,dtype,config,api", TMA_CASES[:3], ids=["-".join(c) for c in TMA_CASES[:3]])
+def test_sim_mesh_parity_ldg_reduce_scatter(mesh, dtype, config, api):
+    # EDIT_PEER_KERNELS=ldgall: the LDG full-grid reduce-scatter variant as well
+    os.environ["EDIT_PEER_KERNELS"] = "ldgall"
+    try:
+        c = MeshCase(mesh, dtype, config)
+    finally:
+        os.environ.pop("EDIT_PEER_KERNELS", None)
+    try:
+        c.run(api)
+        c.check(api)
+    finally:
+        c.close()
+
+
 def test_sim_mesh_two_rounds_and_ring_wrap_small_grid():
     # EDIT_PEER_KERNELS=tma, EDIT_PEER_CTAS=8: a 1M-element unit needs ~15 RS tiles and ~30 AG
     # tiles per CTA, so both mbarrier rings wrap several times; then a second round on the

@@ -84,8 +84,8 @@ int main(int argc, char** argv) {
     pp.D[g] = D[g];
   }
   const bool local_only = argc > 6 && atoi(argv[6]) != 0;
-  const char* ke = getenv("EDIT_PEER_KERNELS");  // as the library: ldg (default) | ldg2 | tma
-  const int kern = ke && !strcmp(ke, "tma") ? 0 : ke && !strcmp(ke, "ldg2") ? 2 : 1;
+  const char* ke = getenv("EDIT_PEER_KERNELS");  // as the library: ldg (default) | ldg2 | ldgall | tma
+  const int kern = ke && !strcmp(ke, "tma") ? 0 : ke && !strcmp(ke, "ldg2") ? 3 : ke && !strcmp(ke, "ldgall") ? 5 : 1;
   std::vector<float> rs_ms(N, 0.f), ag_ms(N, 0.f);
   FoldArgs nofold{};
   for (int r = 0; r < reps + 1; ++r) {
@@ -142,7 +142,7 @@ int main(int argc, char** argv) {
     const double nvl_rs = 2.0 * n * (N - 1) / N, nvl_ag = 4.0 * n * (N - 1) / N;
     printf("%s N=%d tile=%d ctas=%d gpu %d: RS %.3f ms (NVLink in %.0f GB/s, HBM %.0f GB/s)  AG %.3f ms (NVLink in %.0f "
            "GB/s, HBM %.0f GB/s incl. served D, %.0f GB/s algorithmic 20 B)\n",
-           kern == 0 ? "tma" : kern == 2 ? "ldg2" : "ldg", N, tile, ctas, g, rs_ms[g], nvl_rs / rs_ms[g] / 1e6, (2.0 + 8.0 / N) * n / rs_ms[g] / 1e6, ag_ms[g],
+           kern == 0 ? "tma" : kern == 3 ? "ldg2" : kern == 5 ? "ldgall" : "ldg", N, tile, ctas, g, rs_ms[g], nvl_rs / rs_ms[g] / 1e6, (2.0 + 8.0 / N) * n / rs_ms[g] / 1e6, ag_ms[g],
            nvl_ag / ag_ms[g] / 1e6, 22.0 * n / ag_ms[g] / 1e6, 20.0 * n / ag_ms[g] / 1e6);
   }
   return 0;
