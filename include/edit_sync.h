@@ -243,9 +243,9 @@ edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream);
  * its SM; the concurrent forward keeps the other SMs.  Units u < full_units (the ones a
  * forward reaches before its first GEMM, e.g. the embedding: 2) keep full grids.
  *   sms == -1 (the DEFAULT, "auto"): self-tuning.  Each round runs one of four plans and
- *     is timed on the compute stream (begin_round -> end_round): SERIAL (unit u's sync starts
- *     when the forward reaches acquire(u), on full grids: no overlap, i.e. never slower than
- *     the two back to back) or PARTITION with (f, depth) = (1.0, >= 2), (1.6, >= 2),
+ *     is timed on the compute stream (begin_round -> end_round): SERIAL (the whole round
+ *     first, pipelined over the lanes on full grids exactly as edit_sync_round runs it, and
+ *     acquire(0) waits for all of it: no overlap, the cost of the two back to back) or PARTITION with (f, depth) = (1.0, >= 2), (1.6, >= 2),
  *     (1.0, the caller's depth): f x the fewest SMs that stream unit u's bytes within the
  *     forward time its sync overlaps (units u-depth .. u-1, measured per unit between acquire
  *     calls; EDIT_SM_GBPS, default 100 GB/s per SM, the measured per-SM streaming rate), in

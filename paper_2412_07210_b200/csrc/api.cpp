@@ -246,6 +246,10 @@ edit_status_t create_local(const edit_sync_config_t* cfg, void* workspace, size_
   if (const char* e = getenv("EDIT_PEER_KERNELS"))
     h->peer_ldg = !strcmp(e, "tma") ? 0 : !strcmp(e, "ldg2") ? 3 : !strcmp(e, "ldgall") ? 5 : 1;
   if (const char* e = getenv("EDIT_NVTX")) h->nvtx = atoi(e) != 0;
+  if (const char* e = getenv("EDIT_GROUP_NUMEL")) {
+    const long long v = atoll(e);
+    if (v >= 0 && v < (1ll << 31)) h->group_numel = v;
+  }
   if (const char* e = getenv("EDIT_PEER_TILE")) {
     const int v = atoi(e);
     if (v >= 32 && v <= 4096 && (v & 31) == 0) h->peer_tile = v;
@@ -550,6 +554,174 @@ edit_status_t enqueue_step(edit_sync_t h, UnitPlan& p, int step) {
   return EDIT_OK;
 }
 
+// ------------------------------------------------------------------------------ unit groups
+// Capacity of a lane's staging (elements) and D (vectors) buffers, as create_local sized them.
+static void lane_capacity(edit_sync_t h, int64_t* elems, int64_t* dvecs) {
+  int64_t max_numel = 0;
+  for (int64_t x : h->numel) max_numel = std::max(max_numel, x);
+  *elems = std::max<int64_t>(max_numel, 8);
+  *dvecs = slicing_of(max_numel, h->N, 0, h->peer_tile).slice;
+}
+
+std::vector<std::vector<int32_t>> form_groups(edit_sync_t h, const int32_t* layers, int nunits) {
+  std::vector<std::vector<int32_t>> out;
+  const bool on = h->peer && h->dev_xchg && h->K > 1 && h->group_numel > 0 && h->reg_gather.empty();
+  if (!on) {
+    for (int i = 0; i < nunits; ++i) out.push_back({layers[i]});
+    return out;
+  }
+  int64_t cap_e = 0, cap_d = 0;
+  lane_capacity(h, &cap_e, &cap_d);
+  cap_e = std::min<int64_t>(cap_e, h->group_numel);
+  std::vector<int32_t> cur;
+  int64_t used_e = 0, used_d = 0;
+  auto flush = [&] {
+    if (!cur.empty()) out.push_back(cur);
+    cur.clear();
+    used_e = used_d = 0;
+  };
+  for (int i = 0; i < nunits; ++i) {
+    const int32_t u = layers[i];
+    const int64_t n = h->numel[u];
+    const int64_t ne = (n + 7) / 8 * 8;                            // staging offsets stay 16-B aligned
+    const int64_t nd = slicing_of(n, h->N, 0, h->peer_tile).slice;  // D region (vectors)
+    if (n <= 0 || ne > cap_e || nd > cap_d) {  // alone (empty or large units)
+      flush();
+      out.push_back({u});
+      continue;
+    }
+    if ((int)cur.size() == kMaxGroup || used_e + ne > cap_e || used_d + nd > cap_d) flush();
+    cur.push_back(u);
+    used_e += ne;
+    used_d += nd;
+  }
+  flush();
+  return out;
+}
+
+edit_status_t plan_group(edit_sync_t h, Lane& ln, const std::vector<int32_t>& layers, void* const* locals,
+                         float* const* anchors, float* const* momenta, cudaStream_t st, GroupPlan& gp) {
+  gp.ln = &ln;
+  gp.st = st;
+  gp.units.assign(layers.size(), UnitPlan{});
+  GroupArgs& g = gp.g;
+  g = GroupArgs{};
+  g.B = (int32_t)layers.size();
+  g.M = h->M;
+  g.N = h->N;
+  g.my_n = h->sync_idx;
+  g.K = h->K;
+  g.alpha = h->cfg.ema_alpha;
+  g.delta = h->cfg.anomaly_threshold;
+  g.warmup = h->cfg.ema_warmup_rounds;
+  g.nu = h->cfg.outer_lr;
+  g.mu = h->cfg.outer_momentum;
+  g.phi = h->cfg.clip_threshold;
+  g.eps = h->cfg.clip_eps;
+  g.flags = h->cfg.flags;
+  const size_t esz = h->cfg.param_dtype == EDIT_BF16 ? 2 : 4;
+  int64_t off_e = 0, off_d = 0;
+  int32_t c1 = 0, c2 = 0, c3 = 0;
+  for (int s = 0; s < g.B; ++s) {
+    const int32_t u = layers[s];
+    Mode mode{};
+    mode.peer_ctas = h->peer_ctas;
+    TRY(plan_unit(h, ln, u, locals[s], anchors[s], momenta[s], st, mode, gp.units[s]));
+    const UnitPlan& p = gp.units[s];
+    GroupSeg& q = g.seg[s];
+    const int64_t n = h->numel[u];
+    q.local = locals[s];
+    q.anchor = anchors[s];
+    q.momentum = momenta[s];
+    q.n = n;
+    q.slice = p.sl.slice;
+    for (int j = 0; j < h->N; ++j) {
+      // registered locals are read in place; otherwise every member's staging copy, at the
+      // same offset on every member
+      q.L[j] = p.direct ? p.pp.L[j] : static_cast<const char*>(ln.pp.L[j]) + off_e * esz;
+      q.D[j] = ln.pp.D[j] + off_d * 8;
+    }
+    q.Lcopy = p.direct ? nullptr : static_cast<char*>(ln.Lown) + off_e * esz;
+    q.Dmine = ln.Down + off_d * 8;
+    q.scr = &h->scratch[u];
+    q.parts1 = h->part1[u];
+    q.parts2 = h->part2[u];
+    q.ema = h->ema + (size_t)u * h->N;
+    q.rec = h->rec + u;
+    q.c1 = c1;
+    q.c2 = c2;
+    q.c3 = c3;
+    const int64_t n8 = n >> 3, s0 = (int64_t)h->sync_idx * q.slice;
+    const int64_t cnt = std::max<int64_t>(0, std::min(s0 + q.slice, n8) - s0);
+    c1 += (int32_t)group_k1_ctas(n);
+    c2 += (int32_t)rs_ldg_grid(cnt);
+    c3 += (int32_t)group_ag_ctas(q.slice, h->N);
+    off_e += (n + 7) / 8 * 8;
+    off_d += q.slice;
+  }
+  g.c1_end = c1;
+  g.c2_end = c2;
+  g.c3_end = c3;
+  return EDIT_OK;
+}
+
+edit_status_t enqueue_group_step(edit_sync_t h, GroupPlan& gp, int step) {
+  Lane& ln = *gp.ln;
+  cudaStream_t st = gp.st;
+  const int dt = h->cfg.param_dtype;
+  int launched = 0;
+  auto mark = [&](int k) -> edit_status_t {  // profiling event k of every unit of the group
+    for (UnitPlan& p : gp.units)
+      if (p.ev) CUDA_TRY(h, record_event(p.ev[k], st));
+    return EDIT_OK;
+  };
+  switch (step) {
+    case kStepBegin:
+      if (!capturing(st)) {
+        CUDA_TRY(h, cudaStreamWaitEvent(st, ln.last, 0));
+        for (UnitPlan& p : gp.units) CUDA_TRY(h, cudaStreamWaitEvent(st, h->done[p.layer], 0));
+      }
+      TRY(mark(0));
+      break;
+    case kStepNorm:  // K1 of every unit + one exchange of the group's norms + K2 per unit
+      gp.g.x = xchg_args(h, ln, 0);
+      launched += launch_group_norm(dt, gp.g, st);
+      CUDA_TRY(h, cudaGetLastError());
+      TRY(mark(1));
+      break;
+    case kStepDecide:
+      TRY(mark(2));
+      break;
+    case kStepExchange:  // Eq. 3 RS of every unit + one exchange of the Dbar-norm partials
+      gp.g.x = xchg_args(h, ln, 1);
+      launched += launch_group_rs(dt, gp.g, st);
+      CUDA_TRY(h, cudaGetLastError());
+      TRY(mark(3));
+      break;
+    case kStepDbarNorm:
+      TRY(mark(4));
+      break;
+    case kStepUpdate:
+      launched += launch_group_ag(dt, gp.g, st);
+      CUDA_TRY(h, cudaGetLastError());
+      break;
+    case kStepGather:
+      break;  // (groups are not formed when the fused shard all-gather is registered)
+    case kStepEnd:
+      TRY(mark(5));
+      for (UnitPlan& p : gp.units) {
+        if (p.ev) h->pending.push_back(p.layer);
+        CUDA_TRY(h, record_event(h->done[p.layer], st));
+      }
+      CUDA_TRY(h, record_event(ln.last, st));
+      break;
+    default:
+      return fail(EDIT_ERR_INVALID_ARG, "bad step");
+  }
+  h->launches += launched;
+  return EDIT_OK;
+}
+
 edit_status_t enqueue_units(edit_sync_t const* hs, int nh, int nunits, const int32_t* layers,
                             void* const* locals, float* const* anchors, float* const* momenta,
                             const cudaStream_t* streams, bool use_lanes) {
@@ -561,12 +733,38 @@ edit_status_t enqueue_units(edit_sync_t const* hs, int nh, int nunits, const int
       CUDA_TRY(h, cudaEventRecord(h->fork, streams[k]));
       for (Lane& ln : h->lanes) CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->fork, 0));
     }
+  // edit_sync_round: runs of small units as groups (the same partition on every handle and
+  // rank); item i on lane i % lanes
+  std::vector<std::vector<int32_t>> groups;
+  if (use_lanes) groups = form_groups(hs[0], layers, nunits);
+  else
+    for (int i = 0; i < nunits; ++i) groups.push_back({layers[i]});
+  std::vector<int> first(groups.size());  // index into locals/anchors/momenta of each item
+  for (size_t gi = 0, at = 0; gi < groups.size(); at += groups[gi].size(), ++gi) first[gi] = (int)at;
   std::vector<UnitPlan> plans(nh);
-  for (int i = 0; i < nunits; ++i) {
+  std::vector<GroupPlan> gplans(nh);
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    if (groups[gi].size() > 1) {
+      const int i0 = first[gi];
+      for (int k = 0; k < nh; ++k) {
+        edit_sync_t h = hs[k];
+        Lane& ln = h->lanes[gi % h->lanes.size()];
+        const size_t at = (size_t)k * nunits + i0;
+        TRY(plan_group(h, ln, groups[gi], locals + at, anchors + at, momenta + at, ln.stream, gplans[k]));
+      }
+      for (int step = 0; step < kNumSteps; ++step)
+        for (int k = 0; k < nh; ++k) {
+          if (nh > 1) CUDA_TRY(hs[k], cudaSetDevice(hs[k]->cfg.device));
+          const NvtxRange range(hs[k]->nvtx && step == kStepBegin, "edit_sync group of %d units", (int)groups[gi].size());
+          TRY(enqueue_group_step(hs[k], gplans[k], step));
+        }
+      continue;
+    }
+    const int i = first[gi];
     const int32_t layer = layers[i];
     for (int k = 0; k < nh; ++k) {
       edit_sync_t h = hs[k];
-      Lane& ln = use_lanes ? h->lanes[layer % (int)h->lanes.size()] : h->lanes[0];
+      Lane& ln = use_lanes ? h->lanes[gi % h->lanes.size()] : h->lanes[0];
       Mode mode{};
       mode.peer_ctas = h->peer_ctas;
       const size_t at = (size_t)k * nunits + i;
@@ -695,7 +893,7 @@ edit_status_t edit_sync_workspace_bytes(const edit_sync_config_t* cfg, size_t* b
 // Settings every rank must agree on (slice layout, lane mapping, exchange protocol, units):
 // a digest of them is all-gathered at init and compared.
 struct ConfigDigest {
-  int32_t nlanes, peer_tile, dev_xchg, graph, algo, L, M, N, dtype, flags, peer_ldg, pad;
+  int32_t nlanes, peer_tile, dev_xchg, graph, algo, L, M, N, dtype, flags, peer_ldg, group_numel;
   uint64_t numel_hash;
 };
 
@@ -736,8 +934,9 @@ edit_status_t edit_sync_init(const edit_sync_config_t* cfg, const uint8_t id[EDI
       // exchange protocol (read per rank from the environment): compare digests
       ConfigDigest mine;
       memset(&mine, 0, sizeof mine);  // (padding too: the digests are compared bytewise)
-      const int32_t vals[11] = {nlanes, h->peer_tile, h->dev_xchg ? 1 : 0, h->graph ? 1 : 0, cfg->algo,
-                                cfg->num_layers, h->M, h->N, cfg->param_dtype, (int32_t)cfg->flags, h->peer_ldg};
+      const int32_t vals[12] = {nlanes, h->peer_tile, h->dev_xchg ? 1 : 0, h->graph ? 1 : 0, cfg->algo,
+                                cfg->num_layers, h->M, h->N, cfg->param_dtype, (int32_t)cfg->flags, h->peer_ldg,
+                                (int32_t)h->group_numel};
       memcpy(&mine, vals, sizeof vals);
       mine.numel_hash = 1469598103934665603ull;
       for (int64_t x : h->numel) mine.numel_hash = (mine.numel_hash ^ (uint64_t)x) * 1099511628211ull;
@@ -1092,9 +1291,12 @@ static double unit_bytes_per_param(edit_sync_t h, int u) {
 // A self-tuning controller over a few candidate plans, chosen per round by the measured
 // round time (compute stream, begin_round -> end_round; the caller's forward is the same work
 // every round, so the round time IS the objective):
-//   candidate 0 = serial: unit u's sync starts when the forward reaches acquire(u) (after the
-//                 forward of u-1) on full grids, and the forward of u waits for it -- no
-//                 overlap, never slower than running the two back to back;
+//   candidate 0 = serial: the whole round first, exactly as edit_sync_round runs it (every
+//                 unit enqueued at begin_round, pipelined over the lanes on full grids), and
+//                 the forward's first acquire waits for all of it -- no overlap, and the same
+//                 cost as running the round and the forward back to back (a per-unit gate,
+//                 the earlier form, exposed every small unit's whole latency chain: 350M 1x4
+//                 3.28 ms against 3.08 for the pipelined round, profiles/r2_4gpu_350M_1x4.json);
 //   candidate c > 0 = partition: unit u's sync (enqueued depth_c units ahead, depth_c =
 //                 max(caller's depth, 2, 2, 1 for c = 1, 2, 3)) gets f_c = 1.0, 1.6, 1.0 x the
 //                 fewest SMs that stream its bytes within the forward time it overlaps (units
@@ -1174,7 +1376,7 @@ static bool round_serial(edit_sync_t h) { return h->sched_part == kSchedAuto && 
 static edit_status_t sched_enqueue_next(edit_sync_t h, cudaStream_t gate = nullptr) {
   const int u = h->sched_next_sync++;
   Lane& ln = h->lanes[u % h->lanes.size()];
-  if (gate && (h->sched_gate || round_serial(h))) {
+  if (gate && h->sched_gate && !round_serial(h)) {
     CUDA_TRY(h, cudaEventRecord(h->gate_ev[u], gate));
     CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->gate_ev[u], 0));
   }
@@ -1227,8 +1429,14 @@ edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* 
   // inner steps that produced the locals)
   CUDA_TRY(h, cudaEventRecord(h->fork, cs));
   for (Lane& ln : h->lanes) CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->fork, 0));
-  if (!round_serial(h))
+  if (round_serial(h)) {
+    // the whole round ahead of the forward (edit_sync_round's enqueue order); acquire(0) joins
+    // every lane
+    while (h->sched_next_sync < L) TRY(sched_enqueue_next(h));
+    for (Lane& ln : h->lanes) CUDA_TRY(h, cudaEventRecord(ln.tail, ln.stream));
+  } else {
     while (h->sched_next_sync < std::min(depth, L)) TRY(sched_enqueue_next(h));
+  }
   return EDIT_OK;
 }
 
@@ -1242,9 +1450,12 @@ edit_status_t edit_sched_acquire(edit_sync_t h, int32_t layer, void* compute_str
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   // the forward of unit layer-1 ends here on the compute stream (auto mode's measurement)
   CUDA_TRY(h, cudaEventRecord(h->pre_ev[layer], cs));
-  // serial: the sync of `layer` starts only now (gated on the compute stream); otherwise it
-  // was enqueued `depth` units ahead (depth can only lag if acquire skipped ahead)
-  while (h->sched_next_sync <= layer) TRY(sched_enqueue_next(h, round_serial(h) ? cs : nullptr));
+  // serial: the whole round was enqueued at begin_round, the forward starts after all of it;
+  // otherwise unit `layer` was enqueued `depth` units ahead (depth can only lag if acquire
+  // skipped ahead)
+  while (h->sched_next_sync <= layer) TRY(sched_enqueue_next(h));
+  if (round_serial(h) && layer == 0)
+    for (Lane& ln : h->lanes) CUDA_TRY(h, cudaStreamWaitEvent(cs, ln.tail, 0));
   CUDA_TRY(h, cudaStreamWaitEvent(cs, h->done[layer], 0));
   CUDA_TRY(h, cudaEventRecord(h->post_ev[layer], cs));  // the forward of `layer` starts here
   h->sched_next_acquire = layer + 1;
@@ -1262,7 +1473,7 @@ edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream) {
   cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
   const bool complete = h->sched_next_acquire == L;  // every unit acquired: the round is measurable
   if (complete) CUDA_TRY(h, cudaEventRecord(h->end_ev, cs));
-  while (h->sched_next_sync < L) TRY(sched_enqueue_next(h, round_serial(h) ? cs : nullptr));
+  while (h->sched_next_sync < L) TRY(sched_enqueue_next(h));
   for (Lane& ln : h->lanes) {
     CUDA_TRY(h, cudaEventRecord(ln.tail, ln.stream));
     CUDA_TRY(h, cudaStreamWaitEvent(cs, ln.tail, 0));

@@ -271,13 +271,19 @@ __device__ __forceinline__ bool finish_partials(double cta_total, double* cta_pa
 }
 
 // ---------------------------------------------------------------- scalar exchange (mailboxes)
-// Called by every thread of ONE CTA (>= K threads): threads t < K store *src's value into rank
-// t's mailbox (value, then the sequence number with st.release.sys), then wait for sender t
-// in this rank's own mailbox (ld.acquire.sys) and write out[t].  Slots alternate by sequence
-// parity: a rank can only write seq+2 into a slot after the reader published seq+1, i.e.
-// after it finished reading seq -- no slot is overwritten early.  Returns false (in every
-// thread) if the handle already had an error or this wait timed out (the error is then set).
-static __device__ __noinline__ bool xchg_body(const XchgArgs& x, const double* src, double* out) {
+// Called by every thread of ONE CTA (>= K threads): threads t < K store the B values
+// (*src[0..B-1]) into rank t's mailbox (the values, then the sequence number with
+// st.release.sys), then wait for sender t in this rank's own mailbox (ld.acquire.sys) and
+// write out[s][t].  Slots alternate by sequence parity: a rank can only write seq+2 into a
+// slot after the reader published seq+1, i.e. after it finished reading seq -- no slot is
+// overwritten early.  Returns false (in every thread) if the handle already had an error or
+// this wait timed out (the error is then set).
+struct XchgIO {
+  int B;                          // values per message (1, or a group's units)
+  const double* src[kMaxGroup];
+  double* out[kMaxGroup];         // out[s][t] = sender t's value s
+};
+static __device__ __noinline__ bool xchg_body_n(const XchgArgs& x, const XchgIO& io) {
   __shared__ unsigned long long s_seq;
   __shared__ int s_ok;
   const int t = threadIdx.x;
@@ -293,23 +299,26 @@ static __device__ __noinline__ bool xchg_body(const XchgArgs& x, const double* s
   __syncthreads();
   if (!s_ok) return false;  // silent after an earlier error of this handle
   const unsigned long long seq = s_seq;
-  const int K = x.K, me = x.me;
+  const int K = x.K, me = x.me, B = io.B;
   const int base = (x.phase * 2 + (int)(seq & 1)) * K;
   if (t < K) {
-    const double v = *src;
-    unsigned long long* slot = x.mp.box[t] + 2 * (base + me);
-    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(slot), "l"((unsigned long long)__double_as_longlong(v))
-                 : "memory");
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot + 1), "l"(seq) : "memory");
+    unsigned long long* slot = x.mp.box[t] + (size_t)kSlotWords * (base + me);
+    for (int s = 0; s < B; ++s) {
+      const double v = *io.src[s];
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(slot + 1 + s),
+                   "l"((unsigned long long)__double_as_longlong(v))
+                   : "memory");
+    }
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot), "l"(seq) : "memory");
   }
   __syncthreads();  // (all publishes issued before anyone may leave on a timeout)
   if (t < K) {
-    unsigned long long* slot = x.mp.box[me] + 2 * (base + t);
+    unsigned long long* slot = x.mp.box[me] + (size_t)kSlotWords * (base + t);
     unsigned long long s = 0, t0, now;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     bool ok = true;
     while (true) {
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(s) : "l"(slot + 1) : "memory");
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(s) : "l"(slot) : "memory");
       if (s == seq) break;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
       if (x.timeout_ns && now - t0 > x.timeout_ns) {  // a peer stopped syncing: fatal
@@ -318,9 +327,11 @@ static __device__ __noinline__ bool xchg_body(const XchgArgs& x, const double* s
       }
     }
     if (ok) {
-      unsigned long long vb;
-      asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(vb) : "l"(slot) : "memory");
-      out[t] = __longlong_as_double((long long)vb);
+      for (int v = 0; v < B; ++v) {
+        unsigned long long vb;
+        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(vb) : "l"(slot + 1 + v) : "memory");
+        io.out[v][t] = __longlong_as_double((long long)vb);
+      }
     } else {
       atomicExch(x.err, 1);
       if (x.err_host) {
@@ -332,6 +343,14 @@ static __device__ __noinline__ bool xchg_body(const XchgArgs& x, const double* s
   }
   __syncthreads();
   return s_ok != 0;
+}
+// One value per rank.
+static __device__ __forceinline__ bool xchg_body(const XchgArgs& x, const double* src, double* out) {
+  XchgIO io;
+  io.B = 1;
+  io.src[0] = src;
+  io.out[0] = out;
+  return xchg_body_n(x, io);
 }
 
 // K1's last CTA (after finish_partials): the phase-0 exchange of the module-norm partials

@@ -88,6 +88,9 @@ struct edit_sync {
   int peer_tile = edit::kPeerTileVec; // vectors per TMA tile (EDIT_PEER_TILE env; must match on all ranks)
   bool dev_xchg = true;               // scalar chain over NVLink mailboxes (EDIT_XCHG=nccl: NCCL gathers)
   int peer_ldg = 1;                   // EDIT_PEER_KERNELS bits (full-speed rounds): 1 AG LDG, 2 x2, 4 RS LDG
+  // unit groups (internal.h GroupArgs): edit_sync_round syncs runs of consecutive units below
+  // this many elements as one group (EDIT_GROUP_NUMEL; 0 = off; must match on all ranks)
+  int64_t group_numel = 32ll << 20;
   unsigned long long timeout_ns = 0;  // mailbox wait bound (EDIT_XCHG_TIMEOUT_S; 0 = forever)
   // sticky exchange error: device flag read by every exchange, and its mapped-host mirror the
   // library polls at every call (no device sync needed to notice a dead peer)
@@ -203,6 +206,21 @@ enum Step {
 edit_status_t plan_unit(edit_sync_t h, Lane& ln, int32_t layer, void* local, float* anchor, float* momentum,
                         cudaStream_t st, const Mode& mode, UnitPlan& p);
 edit_status_t enqueue_step(edit_sync_t h, UnitPlan& p, int step);
+
+// A group of small units synced by the three group kernels (peer path, full-speed rounds):
+// the units' plans (for their events), the kernel arguments and the lane.
+struct GroupPlan {
+  Lane* ln = nullptr;
+  cudaStream_t st = nullptr;
+  std::vector<UnitPlan> units;
+  GroupArgs g{};
+};
+// Partition of a round's unit list into groups (deterministic from the numel list and the
+// settings, so identical on every rank); a group of one unit takes the single-unit path.
+std::vector<std::vector<int32_t>> form_groups(edit_sync_t h, const int32_t* layers, int nunits);
+edit_status_t plan_group(edit_sync_t h, Lane& ln, const std::vector<int32_t>& layers, void* const* locals,
+                         float* const* anchors, float* const* momenta, cudaStream_t st, GroupPlan& gp);
+edit_status_t enqueue_group_step(edit_sync_t h, GroupPlan& gp, int step);
 
 // Enqueue syncs of `nunits` units on each of nh handles (production: nh == 1; the simulated
 // mesh: nh == K members), unit by unit and, inside a unit, step-major across the handles.

@@ -110,14 +110,17 @@ inline Slicing slicing_of(int64_t n, int N, int me, int tile = kPeerTileVec) {
 // Device-side scalar exchange over NVLink (replaces the tiny NCCL all-gathers of the scalar
 // chain): every rank's mailbox, mapped in every rank through CUDA IPC (or, in the single-GPU
 // simulated mesh of tests/sim, plain device pointers of the other members' mailboxes).
-// Slot layout: box[((phase * 2 + (seq & 1)) * K + src) * 2 + {0: value bits, 1: seq}].
+// A message carries up to kMaxGroup fp64 values (one per unit of a group, below).
+// Slot layout: box[((phase * 2 + (seq & 1)) * K + src) * kSlotWords + {0: seq, 1 + s: value s}].
 // Phases: 0 = module norms (fused into K1), 1 = ||Dbar|| partials (fused into RS),
 // 2 = barriers (fused shard all-gather, warm-up all-reduce).
 constexpr int kXchgPhases = 3;
+constexpr int kMaxGroup = 16;
+constexpr int kSlotWords = 1 + kMaxGroup;
 struct MailPtrs {
   unsigned long long* box[kMaxRanks];
 };
-inline size_t mailbox_bytes(int K) { return sizeof(unsigned long long) * 2 * 2 * kXchgPhases * (size_t)K; }
+inline size_t mailbox_bytes(int K) { return sizeof(unsigned long long) * kSlotWords * 2 * kXchgPhases * (size_t)K; }
 
 // One exchange of one fp64 per rank: publish to every rank's mailbox, wait for all K.
 //  seq:  host-passed sequence number (dseq == nullptr), else the lane's device counter
@@ -150,6 +153,51 @@ struct FoldArgs {
 
 int launch_xchg(const XchgArgs& x, const double* src, double* out, int32_t* rollback, cudaStream_t st,
                 const DecideArgs* dec = nullptr);
+
+// ---------------------------------------------------------------- unit groups
+// Small units (350M / 1B shards: 7-28 M params per rank) are latency-bound when each runs its
+// own chain K1 -> RS -> AG with two scalar exchanges.  edit_sync_round therefore syncs runs
+// of consecutive small units as a GROUP: one K1, one RS and one AG launch for the whole
+// group (each CTA finds its unit in the segment table), and ONE exchange message per phase
+// carrying the group's values.  Per-unit semantics are unchanged (module norms, z-tests,
+// weights, beta are per unit, from each unit's own scratch; R4).  Peer path only.
+struct GroupSeg {
+  const void* L[EDIT_MAX_SYNC];   // every member's local of this unit (registered) or staging copy
+  const float* D[EDIT_MAX_SYNC];  // every member's D buffer at this unit's offset
+  void* local;
+  float* anchor;
+  float* momentum;
+  void* Lcopy;                    // non-registered local: my staging copy at this unit's offset
+  float* Dmine;                   // my D buffer at this unit's offset
+  int64_t n, slice;               // elements; vectors per owner slice (slicing_of)
+  LayerScratch* scr;
+  double* parts1;                 // per-CTA partials of K1 / RS
+  double* parts2;
+  edit_ema_t* ema;                // [N] of this unit
+  edit_layer_stats_t* rec;
+  int32_t c1, c2, c3;             // first CTA of this unit in the K1 / RS / AG grids
+};
+struct GroupArgs {
+  GroupSeg seg[kMaxGroup];
+  int32_t B, M, N, my_n, K;
+  int32_t c1_end, c2_end, c3_end;
+  XchgArgs x;                     // the exchange of the launching kernel (phase 0: K1, 1: RS)
+  double alpha, delta;            // K2
+  int64_t warmup;
+  float nu, mu;                   // K4
+  double phi, eps;
+  uint32_t flags;
+};
+int launch_group_norm(int dtype, const GroupArgs& g, cudaStream_t st);
+int launch_group_rs(int dtype, const GroupArgs& g, cudaStream_t st);
+int launch_group_ag(int dtype, const GroupArgs& g, cudaStream_t st);
+// CTA counts of a unit of n elements in the three group kernels (c1/c2/c3 strides)
+inline int64_t group_k1_ctas(int64_t n) { return grid_of(n, kVecReduce); }
+constexpr int kGroupAgVec = 1;  // vectors per thread of the group AG
+inline int64_t group_ag_ctas(int64_t slice, int N) {
+  const int64_t cv = (int64_t)kThreads * kGroupAgVec;
+  return (int64_t)N * ((slice + cv - 1) / cv);
+}
 
 // Launchers (kernels.cu).  Each returns the number of kernels launched.
 // cta_parts: grid_of(n, kVecReduce) fp64 slots for the per-CTA partials.

@@ -57,6 +57,11 @@ def _units(config):
         plant = {(0, 0): 4.0}
     elif config == "wrap":       # enough tiles that every persistent RS/AG CTA wraps its ring
         units = [synth.Unit("big", 16_000_003, ())]
+    elif config == "many_small":  # 20 small units: two groups (kMaxGroup = 16) in the round API;
+        # a planted replica in unit 3, every replica planted (rollback) in unit 5
+        sizes = [7, 65539, 1000, 300_001, 8, 123_457, 4096, 77_777]
+        units = [synth.Unit(f"s{i}", sizes[i % 8] + i, ()) for i in range(20)]
+        plant = {(3, 1): 4.0, **{(5, n): 4.0 for n in range(8)}}
     elif config == "llama350m":  # 350M-shaped units: embedding, decoder layer 0, head
         all_units = synth.llama_units("350M")
         units = [all_units[0], all_units[1], all_units[33]]
@@ -353,5 +358,55 @@ def test_sim_mesh_silent_peer_poisons_instead_of_applying_stale_data():
         with pytest.raises(EditSyncError, match="EDIT_ERR_STATE"):
             c.sim.layer_sync(1, [c.loc[0][1]], [c.anc[0][1]], [c.mom[0][1]], members=[0])
         assert c.sim.members[1].stats(0).round == 0  # the silent member: untouched, healthy
+    finally:
+        c.close()
+
+
+# Unit groups (internal.h GroupArgs): edit_sync_round syncs runs of consecutive small units with
+# one K1 / RS / AG launch and one exchange message per phase.  (mesh, dtype, config, api,
+# EDIT_GROUP_NUMEL): the default cap (32 Mi elements) groups every unit of these configs; 300,000
+# splits "ragged" into {a} + {b, c}; 0 turns groups off (the single-unit round path).
+GROUP_CASES = [
+    ("1x4", "bf16", "many_small", "round", None), ("1x2", "f32", "many_small", "reg", None),
+    ("2x4", "bf16", "many_small", "round", None), ("1x8", "bf16", "many_small", "reg", None),
+    ("2x2", "bf16", "many_small", "round", None), ("1x2", "bf16", "ragged", "round", "300000"),
+    ("1x4", "bf16", "ragged", "round", "0"), ("2x2", "f32", "toy", "round", "0"), ("1x8", "bf16", "nan", "reg", "0"),
+]
+
+
+@pytest.mark.parametrize("mesh,dtype,config,api,cap", GROUP_CASES, ids=["-".join(map(str, c)) for c in GROUP_CASES])
+def test_sim_mesh_unit_groups(mesh, dtype, config, api, cap):
+    if cap is not None:
+        os.environ["EDIT_GROUP_NUMEL"] = cap
+    try:
+        c = MeshCase(mesh, dtype, config)
+    finally:
+        os.environ.pop("EDIT_GROUP_NUMEL", None)
+    try:
+        c.run(api)
+        outs = c.check(api)
+        if config == "many_small":
+            N = c.N
+            assert outs[3].anomalous[1] and outs[3].w[1] == 0.0 and not outs[3].rollback
+            assert outs[5].rollback and all(outs[5].anomalous[:N])
+            assert not any(o.rollback for i, o in enumerate(outs) if i != 5)
+        # a second round through the same groups (tickets re-armed, mailbox sequence advanced)
+        L = len(c.units)
+        ema_gpu = c.sim.members[0].get_state()
+        c.ema0 = [[oracle.Ema(float(ema_gpu[i, n]["mu"]), float(ema_gpu[i, n]["sigma"]), int(ema_gpu[i, n]["count"]))
+                   for n in range(c.N)] for i in range(L)]
+        for k in range(c.K):
+            m, n = k % c.M, k // c.M
+            for i, u in enumerate(c.units):
+                c.loc[k][i].copy_(synth.shard_local(u, i, c.M, m, n, c.anc[k][i], c.dtype, DEV, c.recipe, 1.0, 7))
+        c.o_in = []
+        for i in range(L):
+            locs = np.stack([np.stack([parity.to_oracle_local(c.loc[n * c.M + m][i]) for n in range(c.N)])
+                             for m in range(c.M)])
+            c.o_in.append((locs, np.stack([c.anc[m][i].cpu().numpy() for m in range(c.M)]),
+                           np.stack([c.mom[m][i].cpu().numpy() for m in range(c.M)])))
+        c.run(api)
+        c.check(api)
+        assert c.sim.members[0].stats(0).round == 2
     finally:
         c.close()
