@@ -57,6 +57,10 @@ def max_over_ranks(t_ms: float, world: int, device) -> float:
     return float(tt.item())
 
 
+def x_bytes(n_f32: int) -> float:
+    return 4.0 * n_f32
+
+
 def rank_coords(rank: int, M: int) -> tuple[int, int]:
     """(shard index m, sync index n) of a rank: rank = n*M + m (R20, include/edit_sync.h)."""
     return rank % M, rank // M
@@ -304,6 +308,33 @@ def main() -> None:
     if registered:
         sync.register_locals(locs)   # members read each other's locals directly (no staging copy)
 
+    # NVLink / NCCL calibration in the same job, outside every timed region:
+    # the library's peer-pull probe (every member of the sync row pulling from all the others
+    # at once, the AG pattern) and torch/NCCL all-reduce bus bandwidth over all ranks
+    calib = None
+    if N > 1 and args.algo == "peer":
+        probe = sync.nvlink_probe(256 << 20, 5)
+        pt = torch.tensor([probe, -probe], device=dev, dtype=torch.float64)
+        dist.all_reduce(pt, op=dist.ReduceOp.MIN)
+        x = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB
+        for _ in range(2):
+            dist.all_reduce(x)
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(5):
+            dist.all_reduce(x)
+        c1.record()
+        torch.cuda.synchronize()
+        t_ar = max_over_ranks(c0.elapsed_time(c1) / 5, world, dev)
+        del x
+        calib = {"nvlink_allpull_GBps_min_over_ranks": float(pt[0]), "nvlink_allpull_GBps_max_over_ranks": -float(pt[1]),
+                 "nvlink_probe": "edit_sync_nvlink_probe: each sync-row member pulls 256 MiB from every other member "
+                                 "at once, 5 reps, CUDA events (per-direction ingress)",
+                 "nccl_allreduce_busbw_GBps": 2.0 * (world - 1) / world * x_bytes(64 << 20) / (t_ar * 1e-3) / 1e9,
+                 "nccl_allreduce": f"torch.distributed all_reduce fp32 256 MiB over {world} ranks, 5 reps, max over ranks"}
+        torch.cuda.empty_cache()
+
     planted = {"replicas": 0, "rounds": 0}
 
     def redraw(step: int) -> None:
@@ -468,14 +499,16 @@ def main() -> None:
     else:
         d_hbm = d_nvl = None
     if d_hbm is not None:
-        nvl_bidir = 673.0  # measured: two GPUs pulling from each other (profiles/r1_a2a_peer_pull_2gpu.txt)
+        # every member pulling from the others at once: the live probe of this run, else the
+        # round-1 measurement (profiles/r1_a2a_peer_pull_2gpu.txt)
+        nvl_bidir = calib["nvlink_allpull_GBps_min_over_ranks"] if calib else 673.0
         t_bound = max(P_r * d_hbm / (hbm_peak * 1e9), P_r * d_nvl / (nvl_bidir * 1e9)) * 1e3
         design = {"hbm_B_per_param": d_hbm, "nvlink_B_per_param_per_dir": d_nvl,
                   "hbm_achieved_GBps": P_r * d_hbm / (ms_per_step * 1e-3) / 1e9,
                   "nvlink_achieved_GBps": P_r * d_nvl / (ms_per_step * 1e-3) / 1e9,
                   "t_bound_ms": t_bound, "frac": t_bound / ms_per_step,
-                  "peaks": f"HBM {hbm_peak} GB/s (MEASURED_PEAKS), NVLink {nvl_bidir} GB/s per direction "
-                           "bidirectional (measured)"}
+                  "peaks": f"HBM {hbm_peak} GB/s (MEASURED_PEAKS), NVLink {nvl_bidir:.1f} GB/s per direction "
+                           "with every member pulling (" + ("measured in this run" if calib else "round-1 probe") + ")"}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -751,6 +784,8 @@ def main() -> None:
                          "hbm_achieved_GBps": (k4_hbm_B * k4_elems / (k4_busy * 1e-3) / 1e9) if k4_busy > 0 else None,
                          "timing": "CUDA events around every launch on its lane stream, union of the launches' "
                                    "intervals over the timed region",
+                         "frac_vs_live_allpull": ((k4_achieved / calib["nvlink_allpull_GBps_min_over_ranks"])
+                                                  if (calib and k4_achieved and k4_bound == "nvlink") else None),
                          "busy_ms_per_step": k4_busy / args.steps, "launch_sum_ms_per_step": k4_ms / args.steps,
                          "achieved_per_launch_sum": k4_achieved_sum},
             "roofline_isolated": {
@@ -775,7 +810,7 @@ def main() -> None:
             "rollbacks_last_round": rollbacks, "beta_sample": betas, "anomaly": anomaly,
             "anomaly_sweep": anomaly_sweep,
             "gpu_launches": launches, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "overlap": overlap,
-            "warmup_allreduce": warm, "fused_gather": gather,
+            "warmup_allreduce": warm, "fused_gather": gather, "calibration": calib,
         }
         print(json.dumps(line), flush=True)
     sync.close()

@@ -303,6 +303,15 @@ edit_status_t edit_sync_set_profiling(edit_sync_t h, int32_t enable);
 edit_status_t edit_sync_profile_collect(edit_sync_t h, double phase_ms[EDIT_NUM_PHASES],
                                         double busy_ms[EDIT_NUM_PHASES], int64_t* syncs, int64_t* elements);
 
+/* NVLink calibration (the roofline denominator of the peer kernels, measured
+ * in the run instead of quoted).  Collective over the sync row: every member pulls
+ * bytes_per_peer from each of the other N - 1 members' staging buffers at the same time (the
+ * AG kernel's access pattern), `reps` times between two mailbox barriers, on lane 0's stream.
+ * *gbps = per-direction ingress GB/s of this rank = reps (N - 1) bytes_per_peer / elapsed.
+ * Peer path with N > 1 only (EDIT_ERR_INVALID_ARG otherwise); bytes_per_peer is clamped to
+ * the staging buffer (the largest unit); blocks until done (call outside timed regions). */
+edit_status_t edit_sync_nvlink_probe(edit_sync_t h, int64_t bytes_per_peer, int32_t reps, double* gbps);
+
 /* Number of kernels the library launched so far on this handle (bench evidence). */
 int64_t edit_sync_kernel_launches(edit_sync_t h);
 

@@ -1643,6 +1643,43 @@ edit_status_t edit_sync_profile_collect(edit_sync_t h, double phase_ms[EDIT_NUM_
   return EDIT_OK;
 }
 
+edit_status_t edit_sync_nvlink_probe(edit_sync_t h, int64_t bytes_per_peer, int32_t reps, double* gbps) {
+  if (!h || !gbps) return fail(EDIT_ERR_INVALID_ARG, "null argument");
+  TRY(check_err(h));
+  if (!h->peer || !h->dev_xchg || h->N < 2 || h->simulated)
+    return fail(EDIT_ERR_INVALID_ARG, "the NVLink probe needs the peer path with N > 1 (mailbox exchange)");
+  if (bytes_per_peer < 16 || reps < 1) return fail(EDIT_ERR_INVALID_ARG, "bytes_per_peer >= 16, reps >= 1");
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  Lane& ln = h->lanes[0];
+  int64_t max_numel = 0;
+  for (int64_t x : h->numel) max_numel = std::max(max_numel, x);
+  const int64_t esz = h->cfg.param_dtype == EDIT_BF16 ? 2 : 4;
+  const int64_t cap = std::max<int64_t>(max_numel, 8) * esz / 16 * 16;
+  bytes_per_peer = std::min(bytes_per_peer, cap) / 16 * 16;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  CUDA_TRY(h, cudaEventCreate(&e0));
+  CUDA_TRY(h, cudaEventCreate(&e1));
+  cudaStream_t st = ln.stream;
+  CUDA_TRY(h, cudaStreamWaitEvent(st, ln.last, 0));
+  // barriers: every member starts (and is known to have finished) pulling together
+  h->launches += launch_xchg(xchg_args(h, ln, 2), ln.bar, ln.bar + 1, nullptr, st);
+  CUDA_TRY(h, cudaEventRecord(e0, st));
+  for (int r = 0; r < reps; ++r)
+    h->launches += launch_nvlink_probe(ln.pp, h->N, h->sync_idx, bytes_per_peer,
+                                       reinterpret_cast<unsigned*>(ln.Down), st);
+  CUDA_TRY(h, cudaEventRecord(e1, st));
+  h->launches += launch_xchg(xchg_args(h, ln, 2), ln.bar, ln.bar + 1, nullptr, st);
+  CUDA_TRY(h, cudaEventRecord(ln.last, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  TRY(check_err(h));
+  float ms = 0.f;
+  CUDA_TRY(h, cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *gbps = ms > 0 ? (double)reps * (h->N - 1) * (double)bytes_per_peer / (ms * 1e-3) / 1e9 : 0.0;
+  return EDIT_OK;
+}
+
 int64_t edit_sync_kernel_launches(edit_sync_t h) { return h ? h->launches : -1; }
 
 edit_status_t edit_sync_destroy(edit_sync_t h) {

@@ -88,9 +88,11 @@ struct edit_sync {
   int peer_tile = edit::kPeerTileVec; // vectors per TMA tile (EDIT_PEER_TILE env; must match on all ranks)
   bool dev_xchg = true;               // scalar chain over NVLink mailboxes (EDIT_XCHG=nccl: NCCL gathers)
   int peer_ldg = 1;                   // EDIT_PEER_KERNELS bits (full-speed rounds): 1 AG LDG, 2 x2, 4 RS LDG
-  // unit groups (internal.h GroupArgs): edit_sync_round syncs runs of consecutive units below
-  // this many elements as one group (EDIT_GROUP_NUMEL; 0 = off; must match on all ranks)
-  int64_t group_numel = 32ll << 20;
+  // unit groups (internal.h GroupArgs): edit_sync_round syncs runs of consecutive units up to
+  // this many elements in total as one group (EDIT_GROUP_NUMEL; 0 = off; must match on all
+  // ranks).  Measured 350M 1x2 (2 B200s): 2.60 ms per round without groups, 2.44 / 2.34 / 2.24
+  // with 16 / 32 / 64 Mi (profiles/r2_groups_sweep_2gpu.txt)
+  int64_t group_numel = 64ll << 20;
   unsigned long long timeout_ns = 0;  // mailbox wait bound (EDIT_XCHG_TIMEOUT_S; 0 = forever)
   // sticky exchange error: device flag read by every exchange, and its mapped-host mirror the
   // library polls at every call (no device sync needed to notice a dead peer)

@@ -245,5 +245,7 @@ inline int64_t rs_partial_slots(int64_t n, int N) {
 int launch_warm_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, void* Dmine, const int* err, cudaStream_t st);
 int launch_warm_ag(int dtype, const PeerPtrs& pp, const Slicing& sl, void* out, const int* err, cudaStream_t st);
 int launch_update(int dtype, const UpdateArgs& a, int cap, cudaStream_t st);
+// NVLink calibration: pull bytes_per_peer from every other member's staging buffer (pp.L).
+int launch_nvlink_probe(const PeerPtrs& pp, int N, int me, int64_t bytes_per_peer, unsigned* sink, cudaStream_t st);
 
 }  // namespace edit

@@ -683,6 +683,29 @@ __global__ void __launch_bounds__(kThreads) warm_ag_kernel(const __grid_constant
 // the barrier phase (fused shard all-gather, warm-up) and by the NCCL-exchange-free paths that
 // have no producing kernel to fold it into.  dec_on: K2 right after the gather.  On failure
 // *rollback (if given) := kAbort so the unit's data kernels write nothing.
+// NVLink calibration (edit_sync_nvlink_probe): every member of the sync row pulls `nv`
+// 16-B vectors from each other member's staging buffer at once (owner-interleaved CTAs, the
+// AG kernel's pattern) -- the per-direction ingress ceiling the peer kernels work against.
+// The loaded words are folded into one store per CTA so no load is dead.
+__global__ void __launch_bounds__(kThreads) nvlink_probe_kernel(const __grid_constant__ PeerPtrs pp, int N, int me,
+                                                                int64_t nv, unsigned* sink) {
+  constexpr int U = 4;
+  const int peers = N - 1;
+  const int owner = (me + 1 + (int)(blockIdx.x % peers)) % N;
+  const int64_t v0 = (int64_t)(blockIdx.x / peers) * kThreads * U + threadIdx.x;
+  const uint4* src = static_cast<const uint4*>(pp.L[owner]);
+  uint4 r[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t v = v0 + (int64_t)u * kThreads;
+    r[u] = v < nv ? __ldcg(src + v) : make_uint4(0, 0, 0, 0);
+  }
+  unsigned x = 0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) x ^= r[u].x ^ r[u].y ^ r[u].z ^ r[u].w;
+  if (x == 0x9e3779b9u) sink[blockIdx.x & 1023] = x;  // practically never taken; keeps the loads
+}
+
 __global__ void xchg_kernel(const __grid_constant__ XchgArgs x, const double* src, double* out,
                             int32_t* rollback, const __grid_constant__ DecideArgs dec, int dec_on) {
   const bool ok = xchg_body(x, src, out);
@@ -842,6 +865,14 @@ int launch_xchg(const XchgArgs& x, const double* src, double* out, int32_t* roll
   DecideArgs d{};
   if (dec) d = *dec;
   xchg_kernel<<<1, 64, 0, st>>>(x, src, out, rollback, d, dec ? 1 : 0);
+  return 1;
+}
+
+int launch_nvlink_probe(const PeerPtrs& pp, int N, int me, int64_t bytes_per_peer, unsigned* sink, cudaStream_t st) {
+  const int64_t nv = bytes_per_peer / 16;
+  const int64_t per = (int64_t)kThreads * 4;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, (N - 1) * ((nv + per - 1) / per));
+  nvlink_probe_kernel<<<grid, kThreads, 0, st>>>(pp, N, me, nv, sink);
   return 1;
 }
 

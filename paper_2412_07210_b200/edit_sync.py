@@ -27,6 +27,7 @@ EXPORTED = ("edit_sync_get_unique_id", "edit_sync_workspace_bytes", "edit_sync_i
             "edit_warmup_allreduce", "edit_sync_register_gather", "edit_sched_begin_round", "edit_sched_acquire",
             "edit_sched_end_round", "edit_sched_set_partition", "edit_sched_get_plan",
             "edit_sync_stats", "edit_sync_get_state", "edit_sync_set_state", "edit_sync_kernel_launches",
+            "edit_sync_nvlink_probe",
             "edit_sync_set_profiling", "edit_sync_profile_collect", "edit_trigger_create", "edit_trigger_sync_now",
             "edit_trigger_in_warmup", "edit_trigger_mark_synced", "edit_trigger_syncs", "edit_trigger_destroy",
             "edit_sync_destroy", "edit_sync_last_error", "edit_sync_version")
@@ -101,6 +102,8 @@ def load_library() -> ctypes.CDLL:
                                               ctypes.POINTER(I64), ctypes.POINTER(I64)]
     lib.edit_sync_profile_collect.restype = S
     lib.edit_sync_kernel_launches.argtypes, lib.edit_sync_kernel_launches.restype = [P], I64
+    lib.edit_sync_nvlink_probe.argtypes = [P, I64, I32, ctypes.POINTER(ctypes.c_double)]
+    lib.edit_sync_nvlink_probe.restype = S
     lib.edit_sync_destroy.argtypes, lib.edit_sync_destroy.restype = [P], S
     D = ctypes.c_double
     lib.edit_trigger_create.argtypes = [I32, I64, D, I64, D, ctypes.POINTER(P)]
@@ -366,6 +369,13 @@ class EditSync:
         _check(self._lib.edit_sync_profile_collect(self._h, ms, busy, ctypes.byref(syncs), ctypes.byref(elems)))
         return {"ms": dict(zip(self.PHASES, list(ms))), "busy_ms": dict(zip(self.PHASES, list(busy))),
                 "syncs": syncs.value, "elements": elems.value}
+
+    def nvlink_probe(self, bytes_per_peer: int = 256 << 20, reps: int = 5) -> float:
+        """Per-direction NVLink ingress GB/s of this rank with the whole sync row pulling from
+        each other at once (collective over the row; edit_sync_nvlink_probe)."""
+        out = ctypes.c_double()
+        _check(self._lib.edit_sync_nvlink_probe(self._h, int(bytes_per_peer), int(reps), ctypes.byref(out)))
+        return out.value
 
     @property
     def kernel_launches(self) -> int:

@@ -103,6 +103,12 @@ def run_case(mesh, dtype_s, config, algo="peer", api="unit"):
     elif config == "warm":
         units = [synth.Unit("a", 1_000_003, ()), synth.Unit("b", 13, ()), synth.Unit("c", 65_536, ())]
         seed_ema = False
+    elif config == "many_small":
+        # 20 small units: the round API syncs them as two unit groups (kMaxGroup = 16); a planted
+        # replica in unit 3, every replica planted (rollback) in unit 5
+        sizes = [7, 65539, 1000, 300_001, 8, 123_457, 4096, 77_777]
+        units = [synth.Unit(f"s{i}", sizes[i % 8] + i, ()) for i in range(20)]
+        plant = {(3, 1): 4.0, **{(5, n): 4.0 for n in range(N)}}
     elif config == "llama350m_sample":
         all_units = synth.llama_units("350M")
         units = [all_units[0], all_units[1], all_units[33]]
