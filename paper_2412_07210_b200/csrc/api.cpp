@@ -1362,8 +1362,13 @@ static void tune_begin(edit_sync_t h) {
           best = m;
         }
       }
-      if (h->tune_ms[cand].back() > 1.15 * best)  // the workload changed: measure again
+      // the workload changed (3 rounds in a row > 15 % above the choice's median; one slow
+      // round -- a straggling peer, a clock dip -- is noise): measure again
+      h->tune_drift = h->tune_ms[cand].back() > 1.15 * best ? h->tune_drift + 1 : 0;
+      if (h->tune_drift >= 3) {
         for (auto& v : h->tune_ms) v.clear();
+        h->tune_drift = 0;
+      }
       for (auto& v : h->tune_ms)  // keep a sliding window
         if (v.size() > 8) v.erase(v.begin(), v.begin() + (v.size() - 8));
     }
@@ -1430,10 +1435,15 @@ edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* 
   CUDA_TRY(h, cudaEventRecord(h->fork, cs));
   for (Lane& ln : h->lanes) CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->fork, 0));
   if (round_serial(h)) {
-    // the whole round ahead of the forward (edit_sync_round's enqueue order); acquire(0) joins
-    // every lane
-    while (h->sched_next_sync < L) TRY(sched_enqueue_next(h));
-    for (Lane& ln : h->lanes) CUDA_TRY(h, cudaEventRecord(ln.tail, ln.stream));
+    // the whole round ahead of the forward, exactly as edit_sync_round runs it (unit groups,
+    // lanes); the compute stream then waits for all of it
+    std::vector<int32_t> all(L);
+    for (int u = 0; u < L; ++u) {
+      all[u] = u;
+      h->sched_sms[u] = -1;
+    }
+    TRY(enqueue_units(&h, 1, L, all.data(), locals, anchors, momenta, &cs, true));
+    h->sched_next_sync = L;
   } else {
     while (h->sched_next_sync < std::min(depth, L)) TRY(sched_enqueue_next(h));
   }
@@ -1454,8 +1464,6 @@ edit_status_t edit_sched_acquire(edit_sync_t h, int32_t layer, void* compute_str
   // otherwise unit `layer` was enqueued `depth` units ahead (depth can only lag if acquire
   // skipped ahead)
   while (h->sched_next_sync <= layer) TRY(sched_enqueue_next(h));
-  if (round_serial(h) && layer == 0)
-    for (Lane& ln : h->lanes) CUDA_TRY(h, cudaStreamWaitEvent(cs, ln.tail, 0));
   CUDA_TRY(h, cudaStreamWaitEvent(cs, h->done[layer], 0));
   CUDA_TRY(h, cudaEventRecord(h->post_ev[layer], cs));  // the forward of `layer` starts here
   h->sched_next_acquire = layer + 1;

@@ -120,6 +120,7 @@ struct edit_sync {
   std::vector<double> fwd_ms;                // [L] forward time of each unit (last measurement)
   bool fwd_valid = false;
   int round_cand = -1;                       // candidate of the current round (-1: fixed setting)
+  int tune_drift = 0;                        // consecutive rounds far above the choice's median
   std::vector<std::vector<float>> tune_ms;   // [kTuneCands] measured round times
   std::vector<int> sched_sms;                // [L] SMs given to each unit's sync (0 full grid, -1 serial)
   int lane_prio = 0;             // priority the lanes were created with (env default)
