@@ -62,6 +62,8 @@ def _units(config):
         sizes = [7, 65539, 1000, 300_001, 8, 123_457, 4096, 77_777]
         units = [synth.Unit(f"s{i}", sizes[i % 8] + i, ()) for i in range(20)]
         plant = {(3, 1): 4.0, **{(5, n): 4.0 for n in range(8)}}
+    elif config == "llama7b_layer0":  # a full-size 7B decoder unit (202,383,360 params)
+        units = [synth.llama_units("7B")[1]]
     elif config == "llama350m":  # 350M-shaped units: embedding, decoder layer 0, head
         all_units = synth.llama_units("350M")
         units = [all_units[0], all_units[1], all_units[33]]
@@ -408,5 +410,19 @@ def test_sim_mesh_unit_groups(mesh, dtype, config, api, cap):
         c.run(api)
         c.check(api)
         assert c.sim.members[0].stats(0).round == 2
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("mesh", ["1x2", "2x2"])
+def test_sim_mesh_full_size_7b_unit_bench_launch_config(mesh):
+    # BASELINE's 7B workload at full size on the N > 1 path, in the launch configuration
+    # bench.py times (defaults: TMA RS on 148 persistent CTAs -- every CTA's ring wraps ~80
+    # times at 1x2 --, LDG AG full grid), every element against the whole-mesh oracle
+    c = MeshCase(mesh, "bf16", "llama7b_layer0")
+    try:
+        c.run("reg")
+        outs = c.check("reg")
+        assert outs[0].beta < 1.0 and not outs[0].rollback   # G ~ 28.5 > phi = 10: the clip is active
     finally:
         c.close()
