@@ -157,16 +157,19 @@ __global__ void __launch_bounds__(kPeerThreads) rs_tma_kernel(const __grid_const
 // the anchor and of every member's local (16-B LDG, the peers' over NVLink; members with
 // w_j == 0 are not read, R9) before any arithmetic.  Same math and fixed member order as the
 // TMA kernel; per-CTA partials of ||Dbar||^2 added in CTA order by the last CTA.
-template <typename T, int I>
+// NM = the row size rounded up to 2 / 4 / 8 (register arrays sized at compile time: with the
+// EDIT_MAX_SYNC-sized arrays the kernel needed 128 registers, 2 CTAs per SM); P = vectors per
+// thread whose loads are issued together.
+template <typename T, int I, int NM, int P>
 __global__ void __launch_bounds__(kThreads) rs_ldg_kernel(const __grid_constant__ PeerPtrs pp, Slicing sl,
                                                           const float* __restrict__ anchor, float* __restrict__ Dmine,
                                                           LayerScratch* __restrict__ scr,
                                                           double* __restrict__ cta_parts,
                                                           const __grid_constant__ FoldArgs f) {
   const int N = sl.N;
-  float w[EDIT_MAX_SYNC];
+  float w[NM];
 #pragma unroll
-  for (int j = 0; j < EDIT_MAX_SYNC; ++j) w[j] = j < N ? scr->w_all[j] : 0.f;
+  for (int j = 0; j < NM; ++j) w[j] = j < N ? scr->w_all[j] : 0.f;
   const bool skip = scr->rollback != 0;  // rollback (l.449) or an aborted unit
   const int64_t n8 = sl.n >> 3;
   const int64_t s0 = (int64_t)sl.me * sl.slice;
@@ -174,24 +177,33 @@ __global__ void __launch_bounds__(kThreads) rs_ldg_kernel(const __grid_constant_
   float acc = 0.f;
   if (!skip) {
 #pragma unroll 1
-    for (int it = 0; it < I; ++it) {
-      const int64_t v = s0 + ((int64_t)blockIdx.x * I + it) * kThreads + threadIdx.x;
-      if (v < s1) {
-        float a[8], d[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        float l[EDIT_MAX_SYNC][8];
-        load8(anchor + 8 * v, a);
+    for (int it = 0; it < I; it += P) {
+      float a[P][8], l[P][NM][8];
 #pragma unroll
-        for (int j = 0; j < EDIT_MAX_SYNC; ++j)
-          if (w[j] != 0.f) load8(static_cast<const T*>(pp.L[j]) + 8 * v, l[j]);
+      for (int p = 0; p < P; ++p) {
+        const int64_t v = s0 + ((int64_t)blockIdx.x * I + it + p) * kThreads + threadIdx.x;
+        if (v < s1) {
+          load8(anchor + 8 * v, a[p]);
 #pragma unroll
-        for (int j = 0; j < EDIT_MAX_SYNC; ++j)
-          if (w[j] != 0.f) {
+          for (int j = 0; j < NM; ++j)
+            if (w[j] != 0.f) load8(static_cast<const T*>(pp.L[j]) + 8 * v, l[p][j]);
+        }
+      }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) d[k] = fmaf(w[j], a[k] - l[j][k], d[k]);
-          }
+      for (int p = 0; p < P; ++p) {
+        const int64_t v = s0 + ((int64_t)blockIdx.x * I + it + p) * kThreads + threadIdx.x;
+        if (v < s1) {
+          float d[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc = fmaf(d[k], d[k], acc);
-        store8(Dmine + 8 * (v - s0), d);
+          for (int j = 0; j < NM; ++j)
+            if (w[j] != 0.f) {
+#pragma unroll
+              for (int k = 0; k < 8; ++k) d[k] = fmaf(w[j], a[p][k] - l[p][j][k], d[k]);
+            }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc = fmaf(d[k], d[k], acc);
+          store8(Dmine + 8 * (v - s0), d);
+        }
       }
     }
   }
@@ -758,6 +770,25 @@ void rs_go(unsigned grid, const Ring& r, cudaStream_t st, const PeerPtrs& pp, co
   rs_tma_kernel<T><<<grid, kPeerThreads, r.K * r.stage_bytes, st>>>(pp, sl, anchor, Dmine, scr, cta_parts, r.K, r.V, f);
 }
 
+template <typename T>
+void rs_ldg_go(unsigned grid, cudaStream_t st, const PeerPtrs& pp, const Slicing& sl, const float* anchor,
+               float* Dmine, LayerScratch* scr, double* cta_parts, const FoldArgs& f) {
+  constexpr int I = kRsLdgIters;
+  static const int two = [] {  // EDIT_RS_LDG_P=1|2: vectors per thread in flight (experiment knob)
+    const char* e = getenv("EDIT_RS_LDG_P");
+    return e && atoi(e) == 1 ? 0 : 1;
+  }();
+  if (sl.N <= 2) {
+    if (two) rs_ldg_kernel<T, I, 2, 2><<<grid, kThreads, 0, st>>>(pp, sl, anchor, Dmine, scr, cta_parts, f);
+    else rs_ldg_kernel<T, I, 2, 1><<<grid, kThreads, 0, st>>>(pp, sl, anchor, Dmine, scr, cta_parts, f);
+  } else if (sl.N <= 4) {
+    if (two) rs_ldg_kernel<T, I, 4, 2><<<grid, kThreads, 0, st>>>(pp, sl, anchor, Dmine, scr, cta_parts, f);
+    else rs_ldg_kernel<T, I, 4, 1><<<grid, kThreads, 0, st>>>(pp, sl, anchor, Dmine, scr, cta_parts, f);
+  } else {
+    rs_ldg_kernel<T, I, 8, 1><<<grid, kThreads, 0, st>>>(pp, sl, anchor, Dmine, scr, cta_parts, f);
+  }
+}
+
 int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anchor, float* Dmine,
               LayerScratch* scr, double* cta_parts, int max_ctas, int smem_kb, int ldg, const FoldArgs& f,
               cudaStream_t st) {
@@ -767,8 +798,8 @@ int launch_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, const float* anc
     const int64_t s0 = (int64_t)sl.me * sl.slice;
     const int64_t cnt = std::max<int64_t>(0, std::min(s0 + sl.slice, n8) - s0);
     const unsigned grid = (unsigned)rs_ldg_grid(cnt);
-    if (dtype == EDIT_BF16) rs_ldg_kernel<__nv_bfloat16, kRsLdgIters><<<grid, kThreads, 0, st>>>(pp, sl, anchor, Dmine, scr, cta_parts, f);
-    else rs_ldg_kernel<float, kRsLdgIters><<<grid, kThreads, 0, st>>>(pp, sl, anchor, Dmine, scr, cta_parts, f);
+    if (dtype == EDIT_BF16) rs_ldg_go<__nv_bfloat16>(grid, st, pp, sl, anchor, Dmine, scr, cta_parts, f);
+    else rs_ldg_go<float>(grid, st, pp, sl, anchor, Dmine, scr, cta_parts, f);
     return 1;
   }
   const int esz = dtype == EDIT_BF16 ? 2 : 4;
