@@ -774,9 +774,11 @@ template <typename T>
 void rs_ldg_go(unsigned grid, cudaStream_t st, const PeerPtrs& pp, const Slicing& sl, const float* anchor,
                float* Dmine, LayerScratch* scr, double* cta_parts, const FoldArgs& f) {
   constexpr int I = kRsLdgIters;
-  static const int two = [] {  // EDIT_RS_LDG_P=1|2: vectors per thread in flight (experiment knob)
+  // EDIT_RS_LDG_P=2: two vectors per thread in flight (experiment knob; measured slower: 7B unit
+  // at N = 2 541 vs 600 GB/s NVLink in, profiles/r2_rs_variants_4gpu.txt)
+  static const int two = [] {
     const char* e = getenv("EDIT_RS_LDG_P");
-    return e && atoi(e) == 1 ? 0 : 1;
+    return e && atoi(e) == 2 ? 1 : 0;
   }();
   if (sl.N <= 2) {
     if (two) rs_ldg_kernel<T, I, 2, 2><<<grid, kThreads, 0, st>>>(pp, sl, anchor, Dmine, scr, cta_parts, f);
