@@ -656,16 +656,29 @@ def main() -> None:
         groups = [dist.new_group([n * M + m for n in range(N)]) for m in range(M)]
         my_group = groups[m_idx]
 
-        def lib_warm():
-            for i in range(len(units)):
-                sync.warmup_allreduce(i, grads[i], stream)
+        def lib_warm(algo):
+            def run():
+                os.environ["EDIT_WARMUP_ALGO"] = algo   # read per call by the library
+                for i in range(len(units)):
+                    sync.warmup_allreduce(i, grads[i], stream)
+            return run
+
+        def lib_warm_round(algo):
+            def run():
+                os.environ["EDIT_WARMUP_ALGO"] = algo
+                sync.warmup_allreduce_round(grads, stream)
+            return run
 
         def torch_warm():
             for i in range(len(units)):
                 dist.all_reduce(grads[i], op=dist.ReduceOp.AVG, group=my_group)
 
         res = {}
-        for name, fn in (("library", lib_warm), ("torch_nccl", torch_warm)):
+        algo0 = os.environ.get("EDIT_WARMUP_ALGO")
+        variants = [("library", lib_warm("nccl")), ("library_peer", lib_warm("peer")),
+                    ("library_round_nccl", lib_warm_round("nccl")), ("library_round_peer", lib_warm_round("peer")),
+                    ("torch_nccl", torch_warm)]
+        for name, fn in variants:
             ts = []
             for s_ in range(4):
                 barrier()
@@ -678,9 +691,16 @@ def main() -> None:
                 if s_ > 0:
                     ts.append(t)
             res[name] = sum(ts) / len(ts)
+        if algo0 is None:
+            os.environ.pop("EDIT_WARMUP_ALGO", None)
+        else:
+            os.environ["EDIT_WARMUP_ALGO"] = algo0
         warm = {"ms_per_round": res, "params_per_rank": P_r, "sync_row": row,
                 "GBps_of_grad_bytes_per_gpu": {k: P_r * b_l / (v * 1e-3) / 1e9 for k, v in res.items()},
-                "note": "all units' bf16 gradient shards averaged over the sync group (Alg. 1 l.422-424)"}
+                "note": "all units' bf16 gradient shards averaged over the sync group (Alg. 1 l.422-424); "
+                        "library = per-unit edit_warmup_allreduce on the caller stream, library_round = "
+                        "edit_warmup_allreduce_round (units pipelined over the lanes); nccl / peer = "
+                        "EDIT_WARMUP_ALGO"}
         del grads
 
     # NEXT-2: fused write-back -> shard-group all-gather (M > 1): a round with the gathered

@@ -281,6 +281,14 @@ edit_status_t edit_sched_get_plan(edit_sync_t h, int32_t* candidate, int32_t* sm
  * NVLink and rounds it once, then pulls every averaged slice from its owner.  N == 1: no-op. */
 edit_status_t edit_warmup_allreduce(edit_sync_t h, int32_t layer, void* grad, void* stream);
 
+/* The warm-up all-reduce of EVERY unit in one call: grads [num_layers] (the same layout and
+ * meaning as above, one per unit; units with layer_numel == 0 are skipped), unit u on the
+ * library's lane u % lanes after a fork from `stream`, which then waits for all lanes -- so
+ * unit u+1's staging and barriers overlap unit u's NVLink pulls (a per-unit call on one stream
+ * serialises them).  Same algorithm choice as edit_warmup_allreduce (EDIT_WARMUP_ALGO).
+ * Collective over the sync row.  N == 1: no-op. */
+edit_status_t edit_warmup_allreduce_round(edit_sync_t h, void* const* grads, void* stream);
+
 /* Blocks until this unit's last enqueued sync has completed, then copies its
  * outcome record to *out. */
 edit_status_t edit_sync_stats(edit_sync_t h, int32_t layer, edit_layer_stats_t* out);

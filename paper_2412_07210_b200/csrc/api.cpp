@@ -793,8 +793,12 @@ edit_status_t enqueue_units(edit_sync_t const* hs, int nh, int nunits, const int
 // gradient where the row can read it; barrier; each member averages its 1/N slice from every
 // member; barrier; every member pulls each averaged slice from its owner.
 edit_status_t enqueue_warmup(edit_sync_t const* hs, int nh, int32_t layer, void* const* grads,
-                             const cudaStream_t* streams, bool force_peer) {
+                             const cudaStream_t* streams, bool force_peer, bool on_lane) {
   const char* wa = getenv("EDIT_WARMUP_ALGO");
+  // on_lane: unit `layer` runs on lane layer % lanes, on the lane's stream (the round API
+  // forked the caller's stream to the lanes); else lane 0 on the caller's stream
+  auto lane_of = [&](edit_sync_t h) -> Lane& { return on_lane ? h->lanes[layer % h->lanes.size()] : h->lanes[0]; };
+  auto stream_of = [&](edit_sync_t h, int k) { return on_lane ? lane_of(h).stream : streams[k]; };
   for (int k = 0; k < nh; ++k) {
     edit_sync_t h = hs[k];
     TRY(check_unit_args(h, layer, grads[k], grads[k], grads[k]));
@@ -802,37 +806,31 @@ edit_status_t enqueue_warmup(edit_sync_t const* hs, int nh, int32_t layer, void*
     const bool warm_peer = h->peer && (force_peer || (wa && !strcmp(wa, "peer")));
     if (!warm_peer) {
       if (nh > 1) return fail(EDIT_ERR_INVALID_ARG, "the simulated mesh runs the peer warm-up only");
-      // a pure mean (no compute to fuse): NCCL's all-reduce measured faster than the peer
-      // kernels (1x4 bf16 7B: 34.6 vs 54.1 ms; 2x2: 14.2 vs 16.3 ms), so it is the default
       const int dt = h->cfg.param_dtype;
       CUDA_TRY(h, cudaSetDevice(h->cfg.device));
-      cudaStream_t st = streams[0];
-      Lane& ln = h->lanes[0];
+      Lane& ln = lane_of(h);
+      cudaStream_t st = stream_of(h, 0);
       CUDA_TRY(h, cudaStreamWaitEvent(st, ln.last, 0));
       NCCL_TRY(h, ncclAllReduce(grads[0], grads[0], (size_t)h->numel[layer],
                                 dt == EDIT_BF16 ? ncclBfloat16 : ncclFloat32, ncclAvg, ln.sync, st));
       CUDA_TRY(h, cudaEventRecord(ln.last, st));
       return EDIT_OK;
     }
-    CUDA_TRY(h, cudaSetDevice(h->cfg.device));
-    if (!h->dev_xchg && !h->warm_dev)
-      CUDA_TRY(h, cudaMalloc(reinterpret_cast<void**>(&h->warm_dev), sizeof(double) * (h->N + 1)));
   }
-  auto barrier = [&](edit_sync_t h, cudaStream_t st) -> edit_status_t {
-    Lane& ln = h->lanes[0];
+  auto barrier = [&](edit_sync_t h, Lane& ln, cudaStream_t st) -> edit_status_t {
     if (h->dev_xchg) {
       h->launches += launch_xchg(xchg_args(h, ln, 2), ln.bar, ln.bar + 1, nullptr, st);
       CUDA_TRY(h, cudaGetLastError());
     } else {
-      NCCL_TRY(h, ncclAllGather(h->warm_dev, h->warm_dev + 1, 1, ncclFloat64, ln.sync, st));
+      NCCL_TRY(h, ncclAllGather(ln.bar, ln.bar + 1, 1, ncclFloat64, ln.sync, st));
     }
     return EDIT_OK;
   };
   for (int step = 0; step < 6; ++step)
     for (int k = 0; k < nh; ++k) {
       edit_sync_t h = hs[k];
-      Lane& ln = h->lanes[0];
-      cudaStream_t st = streams[k];
+      Lane& ln = lane_of(h);
+      cudaStream_t st = stream_of(h, k);
       const int dt = h->cfg.param_dtype;
       const size_t esz = dt == EDIT_BF16 ? 2 : 4;
       const Slicing sl = slicing_of(h->numel[layer], h->N, h->sync_idx, h->peer_tile);
@@ -844,7 +842,7 @@ edit_status_t enqueue_warmup(edit_sync_t const* hs, int nh, int32_t layer, void*
           break;
         case 1:  // staging complete on every member before any RS reads it
         case 3:  // every averaged slice complete before any AG pulls it
-          TRY(barrier(h, st));
+          TRY(barrier(h, ln, st));
           break;
         case 2:
           h->launches += launch_warm_rs(dt, ln.pp, sl, ln.Down, h->err_dev, st);
@@ -859,6 +857,32 @@ edit_status_t enqueue_warmup(edit_sync_t const* hs, int nh, int32_t layer, void*
           break;
       }
     }
+  return EDIT_OK;
+}
+
+edit_status_t enqueue_warmup_units(edit_sync_t const* hs, int nh, int nunits, void* const* grads,
+                                   const cudaStream_t* streams, bool force_peer) {
+  for (int k = 0; k < nh; ++k) {
+    edit_sync_t h = hs[k];
+    TRY(check_err(h));
+    CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+    CUDA_TRY(h, cudaEventRecord(h->fork, streams[k]));
+    for (Lane& ln : h->lanes) CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->fork, 0));
+  }
+  std::vector<void*> g(nh);
+  for (int u = 0; u < nunits; ++u) {
+    if (hs[0]->numel[u] == 0) continue;
+    for (int k = 0; k < nh; ++k) g[k] = grads[(size_t)k * nunits + u];
+    TRY(enqueue_warmup(hs, nh, u, g.data(), streams, force_peer, true));
+  }
+  for (int k = 0; k < nh; ++k) {
+    edit_sync_t h = hs[k];
+    if (nh > 1) CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+    for (Lane& ln : h->lanes) {
+      CUDA_TRY(h, cudaEventRecord(ln.tail, ln.stream));
+      CUDA_TRY(h, cudaStreamWaitEvent(streams[k], ln.tail, 0));
+    }
+  }
   return EDIT_OK;
 }
 
@@ -1216,6 +1240,15 @@ edit_status_t edit_warmup_allreduce(edit_sync_t h, int32_t layer, void* grad, vo
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   return enqueue_warmup(&h, 1, layer, &grad, &st, false);
+}
+
+edit_status_t edit_warmup_allreduce_round(edit_sync_t h, void* const* grads, void* stream) {
+  if (!h) return fail(EDIT_ERR_INVALID_ARG, "null handle");
+  if (!grads) return fail(EDIT_ERR_INVALID_ARG, "null grads");
+  TRY(check_err(h));
+  if (h->N == 1) return EDIT_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return enqueue_warmup_units(&h, 1, h->cfg.num_layers, grads, &st, false);
 }
 
 edit_status_t edit_layer_sync_host(edit_sync_t h, int32_t layer, void* local_host, float* anchor_host,

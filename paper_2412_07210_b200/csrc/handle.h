@@ -237,7 +237,11 @@ edit_status_t enqueue_units(edit_sync_t const* hs, int nh, int nunits, const int
 // Warm-up all-reduce of one unit on nh handles (same step-major rule); force_peer selects the
 // peer-memory variant regardless of EDIT_WARMUP_ALGO.
 edit_status_t enqueue_warmup(edit_sync_t const* hs, int nh, int32_t layer, void* const* grads,
-                             const cudaStream_t* streams, bool force_peer);
+                             const cudaStream_t* streams, bool force_peer, bool on_lane = false);
+// Warm-up all-reduce of every unit (grads [nh][nunits]), unit u on lane u % lanes after a
+// fork from streams[k]; streams[k] then joins every lane (edit_warmup_allreduce_round).
+edit_status_t enqueue_warmup_units(edit_sync_t const* hs, int nh, int nunits, void* const* grads,
+                                   const cudaStream_t* streams, bool force_peer);
 
 // Init split: everything that needs no other rank (validation, workspace carving, streams,
 // events, exchange buffers, the mapped error flag); then, for a real mesh, the NCCL

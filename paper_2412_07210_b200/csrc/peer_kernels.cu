@@ -630,7 +630,8 @@ __global__ void __launch_bounds__(kPeerThreads) update_tma_kernel(UpdateArgs p, 
 // (fixed member order), then every member pulls each averaged slice from its owner.
 // Full-grid LDG (the gradient is consumed right after; plain loads reach ~780 GB/s from a
 // peer with the whole GPU, profiles/r1_peer_bench_2gpu.txt).
-template <typename T>
+// NM = the row size rounded up to 2 / 4 / 8 (register arrays sized at compile time)
+template <typename T, int NM>
 __global__ void __launch_bounds__(kThreads) warm_rs_kernel(const __grid_constant__ PeerPtrs pp, Slicing sl,
                                                            T* __restrict__ Dmine, const int* __restrict__ err) {
   if (*err) return;  // the barrier before this kernel failed: peers' staging may be stale
@@ -643,13 +644,13 @@ __global__ void __launch_bounds__(kThreads) warm_rs_kernel(const __grid_constant
   const int64_t i = s0 + (int64_t)blockIdx.x * kThreads + threadIdx.x;
   const float inv = 1.f / (float)sl.N;
   if (i < s1) {
-    float g[EDIT_MAX_SYNC][8];
+    float g[NM][8];
 #pragma unroll
-    for (int j = 0; j < EDIT_MAX_SYNC; ++j)  // all members' loads in flight together
+    for (int j = 0; j < NM; ++j)  // all members' loads in flight together
       if (j < sl.N) load8(static_cast<const T*>(pp.L[j]) + 8 * i, g[j]);
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int j = 0; j < EDIT_MAX_SYNC; ++j)
+    for (int j = 0; j < NM; ++j)
       if (j < sl.N) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) acc[k] += g[j][k];
@@ -667,20 +668,26 @@ __global__ void __launch_bounds__(kThreads) warm_rs_kernel(const __grid_constant
   }
 }
 
+// A pure copy of each owner's rounded mean.  CTAs interleave the owners (CTA b pulls chunk
+// b / N of owner (b % N + me) % N), so every member reads from all N owners at once -- the AG
+// kernel's pattern; consecutive CTAs pulling from one owner leave the other links idle.
 template <typename T>
 __global__ void __launch_bounds__(kThreads) warm_ag_kernel(const __grid_constant__ PeerPtrs pp, Slicing sl,
                                                            T* __restrict__ out, const int* __restrict__ err) {
   if (*err) return;
   const int64_t n8 = sl.n >> 3;
-  const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if (i < n8) {  // a pure copy of the owner's rounded mean (16 B per bf16 vector)
-    const int64_t j = i / sl.slice;
-    const T* src = reinterpret_cast<const T*>(pp.D[j]) + 8 * (i - j * sl.slice);
+  const int N = sl.N;
+  const int owner = (int)((blockIdx.x % N + sl.me) % N);
+  const int64_t s_lo = (int64_t)owner * sl.slice;
+  const int64_t i = s_lo + (int64_t)(blockIdx.x / N) * kThreads + threadIdx.x;
+  if (i < min(s_lo + sl.slice, n8)) {
+    const T* src = reinterpret_cast<const T*>(pp.D[owner]) + 8 * (i - s_lo);
     if (sizeof(T) == 2) {
       *reinterpret_cast<uint4*>(out + 8 * i) = *reinterpret_cast<const uint4*>(src);
     } else {
-      *reinterpret_cast<uint4*>(out + 8 * i) = *reinterpret_cast<const uint4*>(src);
-      *reinterpret_cast<uint4*>(out + 8 * i + 4) = *reinterpret_cast<const uint4*>(src + 4);
+      const uint4 a = *reinterpret_cast<const uint4*>(src), b = *reinterpret_cast<const uint4*>(src + 4);
+      *reinterpret_cast<uint4*>(out + 8 * i) = a;
+      *reinterpret_cast<uint4*>(out + 8 * i + 4) = b;
     }
   }
   if (blockIdx.x == 0 && threadIdx.x < (sl.n & 7)) {
@@ -690,11 +697,6 @@ __global__ void __launch_bounds__(kThreads) warm_ag_kernel(const __grid_constant
   }
 }
 
-// ------------------------------------------------------------------------------ scalar exchange
-// One CTA: the mailbox exchange (xchg_body, device_common.cuh) as its own launch -- used for
-// the barrier phase (fused shard all-gather, warm-up) and by the NCCL-exchange-free paths that
-// have no producing kernel to fold it into.  dec_on: K2 right after the gather.  On failure
-// *rollback (if given) := kAbort so the unit's data kernels write nothing.
 // NVLink calibration (edit_sync_nvlink_probe): every member of the sync row pulls `nv`
 // 16-B vectors from each other member's staging buffer at once (owner-interleaved CTAs, the
 // AG kernel's pattern) -- the per-direction ingress ceiling the peer kernels work against.
@@ -718,6 +720,11 @@ __global__ void __launch_bounds__(kThreads) nvlink_probe_kernel(const __grid_con
   if (x == 0x9e3779b9u) sink[blockIdx.x & 1023] = x;  // practically never taken; keeps the loads
 }
 
+// ------------------------------------------------------------------------------ scalar exchange
+// One CTA: the mailbox exchange (xchg_body, device_common.cuh) as its own launch -- used for
+// the barrier phase (fused shard all-gather, warm-up) and by the NCCL-exchange-free paths that
+// have no producing kernel to fold it into.  dec_on: K2 right after the gather.  On failure
+// *rollback (if given) := kAbort so the unit's data kernels write nothing.
 __global__ void xchg_kernel(const __grid_constant__ XchgArgs x, const double* src, double* out,
                             int32_t* rollback, const __grid_constant__ DecideArgs dec, int dec_on) {
   const bool ok = xchg_body(x, src, out);
@@ -909,20 +916,26 @@ int launch_nvlink_probe(const PeerPtrs& pp, int N, int me, int64_t bytes_per_pee
   return 1;
 }
 
+template <typename T>
+void warm_rs_go(unsigned grid, cudaStream_t st, const PeerPtrs& pp, const Slicing& sl, T* Dmine, const int* err) {
+  if (sl.N <= 2) warm_rs_kernel<T, 2><<<grid, kThreads, 0, st>>>(pp, sl, Dmine, err);
+  else if (sl.N <= 4) warm_rs_kernel<T, 4><<<grid, kThreads, 0, st>>>(pp, sl, Dmine, err);
+  else warm_rs_kernel<T, 8><<<grid, kThreads, 0, st>>>(pp, sl, Dmine, err);
+}
+
 int launch_warm_rs(int dtype, const PeerPtrs& pp, const Slicing& sl, void* Dmine, const int* err, cudaStream_t st) {
   const int64_t n8 = sl.n >> 3;
   const int64_t s0 = (int64_t)sl.me * sl.slice;
   const int64_t cnt = std::max<int64_t>(0, std::min(s0 + sl.slice, n8) - s0);
   const unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + kThreads - 1) / kThreads);
-  if (dtype == EDIT_BF16)
-    warm_rs_kernel<__nv_bfloat16><<<grid, kThreads, 0, st>>>(pp, sl, static_cast<__nv_bfloat16*>(Dmine), err);
-  else
-    warm_rs_kernel<float><<<grid, kThreads, 0, st>>>(pp, sl, static_cast<float*>(Dmine), err);
+  if (dtype == EDIT_BF16) warm_rs_go<__nv_bfloat16>(grid, st, pp, sl, static_cast<__nv_bfloat16*>(Dmine), err);
+  else warm_rs_go<float>(grid, st, pp, sl, static_cast<float*>(Dmine), err);
   return 1;
 }
 
 int launch_warm_ag(int dtype, const PeerPtrs& pp, const Slicing& sl, void* out, const int* err, cudaStream_t st) {
-  const unsigned grid = (unsigned)std::max<int64_t>(1, ((sl.n >> 3) + kThreads - 1) / kThreads);
+  // N owners x ceil(slice / kThreads) chunks (owner-interleaved, see warm_ag_kernel)
+  const unsigned grid = (unsigned)std::max<int64_t>(1, (int64_t)sl.N * ((sl.slice + kThreads - 1) / kThreads));
   if (dtype == EDIT_BF16)
     warm_ag_kernel<__nv_bfloat16><<<grid, kThreads, 0, st>>>(pp, sl, static_cast<__nv_bfloat16*>(out), err);
   else warm_ag_kernel<float><<<grid, kThreads, 0, st>>>(pp, sl, static_cast<float*>(out), err);

@@ -24,7 +24,7 @@ NO_AE, NO_WA, NO_GC = 1, 2, 4
 
 EXPORTED = ("edit_sync_get_unique_id", "edit_sync_workspace_bytes", "edit_sync_init", "edit_layer_sync",
             "edit_layer_sync_host", "edit_sync_host_wait", "edit_sync_round", "edit_sync_register_locals",
-            "edit_warmup_allreduce", "edit_sync_register_gather", "edit_sched_begin_round", "edit_sched_acquire",
+            "edit_warmup_allreduce", "edit_warmup_allreduce_round", "edit_sync_register_gather", "edit_sched_begin_round", "edit_sched_acquire",
             "edit_sched_end_round", "edit_sched_set_partition", "edit_sched_get_plan",
             "edit_sync_stats", "edit_sync_get_state", "edit_sync_set_state", "edit_sync_kernel_launches",
             "edit_sync_nvlink_probe",
@@ -86,6 +86,7 @@ def load_library() -> ctypes.CDLL:
     lib.edit_sync_round.argtypes, lib.edit_sync_round.restype = [P, P, P, P, P], S
     lib.edit_sync_register_locals.argtypes, lib.edit_sync_register_locals.restype = [P, P], S
     lib.edit_warmup_allreduce.argtypes, lib.edit_warmup_allreduce.restype = [P, I32, P, P], S
+    lib.edit_warmup_allreduce_round.argtypes, lib.edit_warmup_allreduce_round.restype = [P, P, P], S
     lib.edit_sync_register_gather.argtypes, lib.edit_sync_register_gather.restype = [P, P], S
     lib.edit_sched_begin_round.argtypes, lib.edit_sched_begin_round.restype = [P, P, P, P, I32, P], S
     lib.edit_sched_acquire.argtypes, lib.edit_sched_acquire.restype = [P, I32, P], S
@@ -292,6 +293,19 @@ class EditSync:
             raise ValueError(f"grad: need a contiguous {self.param_dtype} tensor of {n} elements on {self.device}")
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         _check(self._lib.edit_warmup_allreduce(self._h, int(layer), grad.data_ptr(), st.cuda_stream))
+
+    def warmup_allreduce_round(self, grads, stream=None) -> None:
+        """The warm-up all-reduce of every unit in one call, pipelined over the lanes."""
+        L = self.num_layers
+        if len(grads) != L:
+            raise ValueError(f"need {L} gradient tensors")
+        for u, g in enumerate(grads):
+            if g.device != self.device or g.dtype != self.param_dtype or not g.is_contiguous() or \
+                    g.numel() != self.layer_numel[u]:
+                raise ValueError(f"unit {u} grad: wrong device/dtype/shape")
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        arr = (ctypes.c_void_p * L)(*[g.data_ptr() for g in grads])
+        _check(self._lib.edit_warmup_allreduce_round(self._h, arr, st.cuda_stream))
 
     def register_gather(self, full_bufs) -> None:
         """NEXT-2: per unit a buffer of M * layer_numel elements that every sync fills with the

@@ -109,4 +109,12 @@ edit_status_t edit_sim_warmup_allreduce(edit_sync_t const* hs, int nh, int32_t l
   return enqueue_warmup(hs, nh, layer, grads, reinterpret_cast<const cudaStream_t*>(streams), true);
 }
 
+// edit_warmup_allreduce_round (peer-memory variant) on each member: every unit, pipelined over
+// the lanes.  grads: [nh][L]; streams: [nh].
+edit_status_t edit_sim_warmup_allreduce_round(edit_sync_t const* hs, int nh, void* const* grads,
+                                              void* const* streams) {
+  return enqueue_warmup_units(hs, nh, hs[0]->cfg.num_layers, grads, reinterpret_cast<const cudaStream_t*>(streams),
+                              true);
+}
+
 }  // extern "C"

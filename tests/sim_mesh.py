@@ -36,6 +36,7 @@ def load():
         lib.edit_sim_layer_sync.argtypes, lib.edit_sim_layer_sync.restype = [P, S, I32, P, P, P, P], S
         lib.edit_sim_round.argtypes, lib.edit_sim_round.restype = [P, S, P, P, P, P], S
         lib.edit_sim_warmup_allreduce.argtypes, lib.edit_sim_warmup_allreduce.restype = [P, S, I32, P, P], S
+        lib.edit_sim_warmup_allreduce_round.argtypes, lib.edit_sim_warmup_allreduce_round.restype = [P, S, P, P], S
         _lib = lib
     return _lib
 
@@ -130,6 +131,15 @@ class SimMesh:
         self._fork(members)
         rc = self.lib.edit_sim_warmup_allreduce(self._handles(members), self.K, int(layer), _ptrs(grads),
                                                 self._streams(members))
+        self._join(members)
+        es._check(rc)
+
+    def warmup_allreduce_round(self, grads):
+        """grads [K][L]: every unit of every member, pipelined over each member's lanes."""
+        members = list(range(self.K))
+        self._fork(members)
+        rc = self.lib.edit_sim_warmup_allreduce_round(self._handles(members), self.K,
+                                                      _ptrs([t for row in grads for t in row]), self._streams(members))
         self._join(members)
         es._check(rc)
 

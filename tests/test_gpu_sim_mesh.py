@@ -305,9 +305,11 @@ def test_sim_mesh_alternating_caller_streams():
         c.close()
 
 
-@pytest.mark.parametrize("mesh,dtype", [("1x2", "bf16"), ("1x2", "f32"), ("2x2", "bf16"), ("1x4", "f32"),
-                                        ("2x4", "bf16"), ("1x8", "bf16")])
-def test_sim_mesh_warmup_allreduce(mesh, dtype):
+@pytest.mark.parametrize("mesh,dtype,api", [("1x2", "bf16", "unit"), ("1x2", "f32", "unit"), ("2x2", "bf16", "unit"),
+                                            ("1x4", "f32", "unit"), ("2x4", "bf16", "unit"), ("1x8", "bf16", "unit"),
+                                            ("1x2", "bf16", "round"), ("1x4", "bf16", "round"),
+                                            ("2x4", "f32", "round"), ("1x8", "bf16", "round")])
+def test_sim_mesh_warmup_allreduce(mesh, dtype, api):
     # NEXT-3 (Alg. 1 l.422-424): grad <- mean over the sync row, peer-memory kernels, against
     # oracle.allreduce_mean; bit-identical along every row
     M, N = (int(x) for x in mesh.split("x"))
@@ -326,8 +328,11 @@ def test_sim_mesh_warmup_allreduce(mesh, dtype):
                 row.append(g.to(dt))
             grads.append(row)
         inputs = [[parity.to_oracle_local(g) for g in row] for row in grads]
-        for i in range(len(units)):
-            sim.warmup_allreduce(i, [grads[k][i] for k in range(M * N)])
+        if api == "round":   # every unit in one call, pipelined over the lanes
+            sim.warmup_allreduce_round(grads)
+        else:
+            for i in range(len(units)):
+                sim.warmup_allreduce(i, [grads[k][i] for k in range(M * N)])
         torch.cuda.synchronize()
         for i in range(len(units)):
             for m in range(M):
