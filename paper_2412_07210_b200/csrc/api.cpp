@@ -1411,12 +1411,32 @@ static void tune_begin(edit_sync_t h) {
 
 static bool round_serial(edit_sync_t h) { return h->sched_part == kSchedAuto && h->round_cand == 0; }
 
+// The scheduler's work items are the round API's: runs of small units form unit groups
+// (form_groups, deterministic from the numel list), every other unit is its own item; item i
+// runs on lane i % lanes.  So every plan -- whichever one a rank's tuner picked for this round
+// -- enqueues the same exchanges in the same order on every rank: plans differ only in how
+// many SMs a single-unit item's kernels get and in when items are enqueued.
+static int item_first(edit_sync_t h, int i) { return h->sched_items[i][0]; }
+
 static edit_status_t sched_enqueue_next(edit_sync_t h, cudaStream_t gate = nullptr) {
-  const int u = h->sched_next_sync++;
-  Lane& ln = h->lanes[u % h->lanes.size()];
+  const int i = h->sched_next_sync++;
+  const std::vector<int32_t>& item = h->sched_items[i];
+  Lane& ln = h->lanes[i % h->lanes.size()];
+  const int u = item[0];
   if (gate && h->sched_gate && !round_serial(h)) {
     CUDA_TRY(h, cudaEventRecord(h->gate_ev[u], gate));
     CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->gate_ev[u], 0));
+  }
+  if (item.size() > 1) {
+    // a unit group: the group kernels at full speed under every plan (small units lose with
+    // any overlapped plan, DESIGN 7)
+    for (int32_t v : item) h->sched_sms[v] = round_serial(h) ? -1 : 0;
+    GroupPlan gp;
+    TRY(plan_group(h, ln, item, h->sched_local.data() + u, h->sched_anchor.data() + u, h->sched_mom.data() + u,
+                   ln.stream, gp));
+    const NvtxRange range(h->nvtx, "edit_sync group of %d units (scheduled)", (int)item.size());
+    for (int step = 0; step < kNumSteps; ++step) TRY(enqueue_group_step(h, gp, step));
+    return EDIT_OK;
   }
   Mode mode{h->sched_ctas, h->sched_ctas > 0 ? h->sched_ctas : h->peer_ctas, h->sched_ctas > 0 ? h->sched_smem_kb : 0,
             0};
@@ -1458,6 +1478,11 @@ edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* 
   h->sched_mom.assign(momenta, momenta + L);
   h->sched_next_sync = 0;
   h->sched_next_acquire = 0;
+  {
+    std::vector<int32_t> all(L);
+    for (int u = 0; u < L; ++u) all[u] = u;
+    h->sched_items = form_groups(h, all.data(), L);
+  }
   h->sched_active = true;
   tune_begin(h);
   h->sched_depth = h->round_cand > 0 ? std::max(depth, kTuneMinDepth[h->round_cand]) : depth;
@@ -1467,18 +1492,17 @@ edit_status_t edit_sched_begin_round(edit_sync_t h, void* const* locals, float* 
   // inner steps that produced the locals)
   CUDA_TRY(h, cudaEventRecord(h->fork, cs));
   for (Lane& ln : h->lanes) CUDA_TRY(h, cudaStreamWaitEvent(ln.stream, h->fork, 0));
+  const int nitems = (int)h->sched_items.size();
   if (round_serial(h)) {
-    // the whole round ahead of the forward, exactly as edit_sync_round runs it (unit groups,
+    // the whole round ahead of the forward, as edit_sync_round runs it (the same items and
     // lanes); the compute stream then waits for all of it
-    std::vector<int32_t> all(L);
-    for (int u = 0; u < L; ++u) {
-      all[u] = u;
-      h->sched_sms[u] = -1;
+    while (h->sched_next_sync < nitems) TRY(sched_enqueue_next(h));
+    for (Lane& ln : h->lanes) {
+      CUDA_TRY(h, cudaEventRecord(ln.tail, ln.stream));
+      CUDA_TRY(h, cudaStreamWaitEvent(cs, ln.tail, 0));
     }
-    TRY(enqueue_units(&h, 1, L, all.data(), locals, anchors, momenta, &cs, true));
-    h->sched_next_sync = L;
   } else {
-    while (h->sched_next_sync < std::min(depth, L)) TRY(sched_enqueue_next(h));
+    while (h->sched_next_sync < nitems && item_first(h, h->sched_next_sync) < depth) TRY(sched_enqueue_next(h));
   }
   return EDIT_OK;
 }
@@ -1496,11 +1520,12 @@ edit_status_t edit_sched_acquire(edit_sync_t h, int32_t layer, void* compute_str
   // serial: the whole round was enqueued at begin_round, the forward starts after all of it;
   // otherwise unit `layer` was enqueued `depth` units ahead (depth can only lag if acquire
   // skipped ahead)
-  while (h->sched_next_sync <= layer) TRY(sched_enqueue_next(h));
+  const int nitems = (int)h->sched_items.size();
+  while (h->sched_next_sync < nitems && item_first(h, h->sched_next_sync) <= layer) TRY(sched_enqueue_next(h));
   CUDA_TRY(h, cudaStreamWaitEvent(cs, h->done[layer], 0));
   CUDA_TRY(h, cudaEventRecord(h->post_ev[layer], cs));  // the forward of `layer` starts here
   h->sched_next_acquire = layer + 1;
-  if (!round_serial(h) && h->sched_next_sync < L && h->sched_next_sync <= layer + h->sched_depth)
+  while (!round_serial(h) && h->sched_next_sync < nitems && item_first(h, h->sched_next_sync) <= layer + h->sched_depth)
     TRY(sched_enqueue_next(h, cs));
   return EDIT_OK;
 }
@@ -1514,7 +1539,7 @@ edit_status_t edit_sched_end_round(edit_sync_t h, void* compute_stream) {
   cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
   const bool complete = h->sched_next_acquire == L;  // every unit acquired: the round is measurable
   if (complete) CUDA_TRY(h, cudaEventRecord(h->end_ev, cs));
-  while (h->sched_next_sync < L) TRY(sched_enqueue_next(h));
+  while (h->sched_next_sync < (int)h->sched_items.size()) TRY(sched_enqueue_next(h));
   for (Lane& ln : h->lanes) {
     CUDA_TRY(h, cudaEventRecord(ln.tail, ln.stream));
     CUDA_TRY(h, cudaStreamWaitEvent(cs, ln.tail, 0));

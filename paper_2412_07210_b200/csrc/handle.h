@@ -163,7 +163,8 @@ struct edit_sync {
   // prefetch scheduler state
   std::vector<void*> sched_local;
   std::vector<float*> sched_anchor, sched_mom;
-  int sched_depth = 0, sched_next_sync = 0, sched_next_acquire = 0;
+  std::vector<std::vector<int32_t>> sched_items;  // the round's work items (form_groups)
+  int sched_depth = 0, sched_next_sync = 0, sched_next_acquire = 0;  // next_sync: item index
   bool sched_active = false;
   bool poisoned = false;
   int64_t launches = 0;

@@ -431,3 +431,61 @@ def test_sim_mesh_full_size_7b_unit_bench_launch_config(mesh):
         assert outs[0].beta < 1.0 and not outs[0].rollback   # G ~ 28.5 > phi = 10: the clip is active
     finally:
         c.close()
+
+
+def _next_round_inputs(c, salt):
+    """Fresh locals from the updated anchors; the oracle continues from the GPU's EMA state
+    (bitwise identical on every member) and the current anchors / momenta."""
+    L = len(c.units)
+    ema_gpu = c.sim.members[0].get_state()
+    c.ema0 = [[oracle.Ema(float(ema_gpu[i, n]["mu"]), float(ema_gpu[i, n]["sigma"]), int(ema_gpu[i, n]["count"]))
+               for n in range(c.N)] for i in range(L)]
+    for k in range(c.K):
+        m, n = k % c.M, k // c.M
+        for i, u in enumerate(c.units):
+            c.loc[k][i].copy_(synth.shard_local(u, i, c.M, m, n, c.anc[k][i], c.dtype, DEV, c.recipe, 1.0, salt))
+    c.o_in = []
+    for i in range(L):
+        locs = np.stack([np.stack([parity.to_oracle_local(c.loc[n * c.M + m][i]) for n in range(c.N)])
+                         for m in range(c.M)])
+        c.o_in.append((locs, np.stack([c.anc[m][i].cpu().numpy() for m in range(c.M)]),
+                       np.stack([c.mom[m][i].cpu().numpy() for m in range(c.M)])))
+
+
+SCHED_CASES = [("1x4", "bf16", "many_small", -1), ("2x2", "bf16", "ragged", -1), ("1x2", "f32", "toy", 8),
+               ("2x4", "bf16", "ragged", 0)]
+
+
+@pytest.mark.parametrize("mesh,dtype,config,sms", SCHED_CASES, ids=["-".join(map(str, c)) for c in SCHED_CASES])
+def test_sim_mesh_prefetch_scheduler(mesh, dtype, config, sms):
+    # a8 (P:70, Alg. 1 l.408-412) on every member: begin_round / acquire(u) + a "forward" of
+    # unit u on the member's compute stream / end_round, 5 rounds.  With sms = -1 (the default
+    # auto mode) the tuner walks its plans (serial first, then the partitions); unit groups
+    # are scheduled as items, so every member enqueues the same exchanges whatever plan it
+    # picked.  Every round against the oracle; the forward of u must see unit u synced.
+    c = MeshCase(mesh, dtype, config)
+    try:
+        for e in c.sim.members:
+            e.set_partition(sms, 1)
+        L = len(c.units)
+        for rnd in range(5):
+            if rnd > 0:
+                _next_round_inputs(c, 100 + rnd)
+            seen = [[None] * L for _ in range(c.K)]
+            for k, e in enumerate(c.sim.members):
+                e.begin_round(c.loc[k], c.anc[k], c.mom[k], 1 + rnd % 2, c.sim.streams[k])
+            for u in range(L):
+                for k, e in enumerate(c.sim.members):
+                    e.acquire(u, c.sim.streams[k])
+                    with torch.cuda.stream(c.sim.streams[k]):
+                        seen[k][u] = c.loc[k][u].float().sum()   # the "forward" reads the synced local
+            for k, e in enumerate(c.sim.members):
+                e.end_round(c.sim.streams[k])
+            torch.cuda.synchronize()
+            c.check("sched")
+            for k in range(c.K):
+                for u in range(L):
+                    assert float(seen[k][u]) == float(c.anc[k][u].to(c.dtype).float().sum()), \
+                        f"round {rnd} member {k}: forward of unit {u} ran before its sync"
+    finally:
+        c.close()
