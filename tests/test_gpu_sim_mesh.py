@@ -452,17 +452,12 @@ def _next_round_inputs(c, salt):
                        np.stack([c.mom[m][i].cpu().numpy() for m in range(c.M)])))
 
 
-SCHED_CASES = [("1x4", "bf16", "many_small", -1), ("2x2", "bf16", "ragged", -1), ("1x2", "f32", "toy", 8),
-               ("2x4", "bf16", "ragged", 0)]
+SCHED_CASES = [("1x4", "bf16", "many_small", -1, 2), ("2x2", "bf16", "ragged", -1, 2), ("1x2", "f32", "toy", 8, 2),
+               ("2x4", "bf16", "ragged", 0, 1)]
 
 
-@pytest.mark.parametrize("mesh,dtype,config,sms", SCHED_CASES, ids=["-".join(map(str, c)) for c in SCHED_CASES])
-def test_sim_mesh_prefetch_scheduler(mesh, dtype, config, sms):
-    # a8 (P:70, Alg. 1 l.408-412) on every member: begin_round / acquire(u) + a "forward" of
-    # unit u on the member's compute stream / end_round, 5 rounds.  With sms = -1 (the default
-    # auto mode) the tuner walks its plans (serial first, then the partitions); unit groups
-    # are scheduled as items, so every member enqueues the same exchanges whatever plan it
-    # picked.  Every round against the oracle; the forward of u must see unit u synced.
+def run_sched_case(mesh, dtype, config, sms):
+    """Body of test_sim_mesh_prefetch_scheduler (runs in a child process, see there)."""
     c = MeshCase(mesh, dtype, config)
     try:
         for e in c.sim.members:
@@ -489,3 +484,25 @@ def test_sim_mesh_prefetch_scheduler(mesh, dtype, config, sms):
                         f"round {rnd} member {k}: forward of unit {u} ran before its sync"
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("mesh,dtype,config,sms,lanes", SCHED_CASES, ids=["-".join(map(str, c)) for c in SCHED_CASES])
+def test_sim_mesh_prefetch_scheduler(mesh, dtype, config, sms, lanes):
+    # a8 (P:70, Alg. 1 l.408-412) on every member: begin_round / acquire(u) + a "forward" of
+    # unit u on the member's compute stream / end_round, 5 rounds.  With sms = -1 (the default
+    # auto mode) the tuner walks its plans (serial first, then the partitions); unit groups
+    # are scheduled as items, so every member enqueues the same exchanges whatever plan it
+    # picked.  Every round against the oracle; the forward of u must see unit u synced.
+    # Child process: the scheduler enqueues a whole item per member call (not step-major
+    # across members like the round API), so on ONE device the members' streams must not share
+    # hardware queues (CUDA_DEVICE_MAX_CONNECTIONS=32, few lanes) -- else member 1's K1 can queue
+    # behind member 0's RS, which waits for it: a deadlock of the single-GPU harness only (real
+    # ranks are separate devices).
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32", EDIT_LANES=str(lanes), EDIT_XCHG_TIMEOUT_S="60")
+    code = (f"import sys; sys.path.insert(0, {root!r}); from tests.test_gpu_sim_mesh import run_sched_case; "
+            f"run_sched_case({mesh!r}, {dtype!r}, {config!r}, {sms}); print('SCHED OK')")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "SCHED OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
