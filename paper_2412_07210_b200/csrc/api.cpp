@@ -1380,6 +1380,16 @@ static void tune_begin(edit_sync_t h) {
     h->round_cand = -1;
     return;
   }
+  // the partition plans only reshape single-unit items (unit groups run at full speed under
+  // every plan); with none past full_units (every small unit grouped) they can only lose --
+  // measured 1B 2x2: h = -0.34 / -0.58 -- so the plan is serial, identically on every rank
+  bool partitionable = false;
+  for (const auto& item : h->sched_items)
+    if (item.size() == 1 && item[0] >= h->sched_full_units) partitionable = true;
+  if (!partitionable) {
+    h->round_cand = 0;
+    return;
+  }
   int cand = -1;
   if (!h->fwd_valid) {
     cand = 0;  // measure the forward first

@@ -398,20 +398,7 @@ def test_sim_mesh_unit_groups(mesh, dtype, config, api, cap):
             assert outs[5].rollback and all(outs[5].anomalous[:N])
             assert not any(o.rollback for i, o in enumerate(outs) if i != 5)
         # a second round through the same groups (tickets re-armed, mailbox sequence advanced)
-        L = len(c.units)
-        ema_gpu = c.sim.members[0].get_state()
-        c.ema0 = [[oracle.Ema(float(ema_gpu[i, n]["mu"]), float(ema_gpu[i, n]["sigma"]), int(ema_gpu[i, n]["count"]))
-                   for n in range(c.N)] for i in range(L)]
-        for k in range(c.K):
-            m, n = k % c.M, k // c.M
-            for i, u in enumerate(c.units):
-                c.loc[k][i].copy_(synth.shard_local(u, i, c.M, m, n, c.anc[k][i], c.dtype, DEV, c.recipe, 1.0, 7))
-        c.o_in = []
-        for i in range(L):
-            locs = np.stack([np.stack([parity.to_oracle_local(c.loc[n * c.M + m][i]) for n in range(c.N)])
-                             for m in range(c.M)])
-            c.o_in.append((locs, np.stack([c.anc[m][i].cpu().numpy() for m in range(c.M)]),
-                           np.stack([c.mom[m][i].cpu().numpy() for m in range(c.M)])))
+        _next_round_inputs(c, 7)
         c.run(api)
         c.check(api)
         assert c.sim.members[0].stats(0).round == 2
@@ -450,59 +437,3 @@ def _next_round_inputs(c, salt):
                          for m in range(c.M)])
         c.o_in.append((locs, np.stack([c.anc[m][i].cpu().numpy() for m in range(c.M)]),
                        np.stack([c.mom[m][i].cpu().numpy() for m in range(c.M)])))
-
-
-SCHED_CASES = [("1x4", "bf16", "many_small", -1, 2), ("2x2", "bf16", "ragged", -1, 2), ("1x2", "f32", "toy", 8, 2),
-               ("2x4", "bf16", "ragged", 0, 1)]
-
-
-def run_sched_case(mesh, dtype, config, sms):
-    """Body of test_sim_mesh_prefetch_scheduler (runs in a child process, see there)."""
-    c = MeshCase(mesh, dtype, config)
-    try:
-        for e in c.sim.members:
-            e.set_partition(sms, 1)
-        L = len(c.units)
-        for rnd in range(5):
-            if rnd > 0:
-                _next_round_inputs(c, 100 + rnd)
-            seen = [[None] * L for _ in range(c.K)]
-            for k, e in enumerate(c.sim.members):
-                e.begin_round(c.loc[k], c.anc[k], c.mom[k], 1 + rnd % 2, c.sim.streams[k])
-            for u in range(L):
-                for k, e in enumerate(c.sim.members):
-                    e.acquire(u, c.sim.streams[k])
-                    with torch.cuda.stream(c.sim.streams[k]):
-                        seen[k][u] = c.loc[k][u].float().sum()   # the "forward" reads the synced local
-            for k, e in enumerate(c.sim.members):
-                e.end_round(c.sim.streams[k])
-            torch.cuda.synchronize()
-            c.check("sched")
-            for k in range(c.K):
-                for u in range(L):
-                    assert float(seen[k][u]) == float(c.anc[k][u].to(c.dtype).float().sum()), \
-                        f"round {rnd} member {k}: forward of unit {u} ran before its sync"
-    finally:
-        c.close()
-
-
-@pytest.mark.parametrize("mesh,dtype,config,sms,lanes", SCHED_CASES, ids=["-".join(map(str, c)) for c in SCHED_CASES])
-def test_sim_mesh_prefetch_scheduler(mesh, dtype, config, sms, lanes):
-    # a8 (P:70, Alg. 1 l.408-412) on every member: begin_round / acquire(u) + a "forward" of
-    # unit u on the member's compute stream / end_round, 5 rounds.  With sms = -1 (the default
-    # auto mode) the tuner walks its plans (serial first, then the partitions); unit groups
-    # are scheduled as items, so every member enqueues the same exchanges whatever plan it
-    # picked.  Every round against the oracle; the forward of u must see unit u synced.
-    # Child process: the scheduler enqueues a whole item per member call (not step-major
-    # across members like the round API), so on ONE device the members' streams must not share
-    # hardware queues (CUDA_DEVICE_MAX_CONNECTIONS=32, few lanes) -- else member 1's K1 can queue
-    # behind member 0's RS, which waits for it: a deadlock of the single-GPU harness only (real
-    # ranks are separate devices).
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32", EDIT_LANES=str(lanes), EDIT_XCHG_TIMEOUT_S="60")
-    code = (f"import sys; sys.path.insert(0, {root!r}); from tests.test_gpu_sim_mesh import run_sched_case; "
-            f"run_sched_case({mesh!r}, {dtype!r}, {config!r}, {sms}); print('SCHED OK')")
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0 and "SCHED OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
