@@ -188,6 +188,9 @@ struct GroupArgs {
   double phi, eps;
   uint32_t flags;
 };
+// passed by value as __grid_constant__ kernel parameters (4,496 B; CUDA 12.1+ on sm_70+ allows
+// 32,764 B of kernel parameters)
+static_assert(sizeof(GroupArgs) <= 32764, "GroupArgs exceeds the kernel parameter limit");
 int launch_group_norm(int dtype, const GroupArgs& g, cudaStream_t st);
 int launch_group_rs(int dtype, const GroupArgs& g, cudaStream_t st);
 int launch_group_ag(int dtype, const GroupArgs& g, cudaStream_t st);
