@@ -790,7 +790,10 @@ def main() -> None:
                                     else "none (N = 1)"),
                        "api": "edit_layer_sync x L (sequential)" if args.sequential else
                        f"edit_sync_round ({os.environ.get('EDIT_LANES', '4' if N > 1 else '2')} lanes"
-                       + (", CUDA-graph replay" if os.environ.get("EDIT_GRAPH", "0") != "0" else "") + ")",
+                       + (", CUDA-graph replay" if os.environ.get("EDIT_GRAPH", "0") != "0" else "")
+                       + (f", unit groups <= {os.environ.get('EDIT_GROUP_NUMEL', '67108864')} elements"
+                          if (N > 1 and args.algo == "peer" and os.environ.get("EDIT_GROUP_NUMEL", "1") != "0") else "")
+                       + ")",
                        "l2": "inputs (%.1f GB/rank) larger than L2" % (P_r * (b_l + 8) / 1e9),
                        "inner_steps": "locals redrawn as cast(anchor - D) between steps, outside the timed region",
                        "anomaly_rate": args.anomaly_rate},
