@@ -1733,6 +1733,14 @@ edit_status_t edit_sync_nvlink_probe(edit_sync_t h, int64_t bytes_per_peer, int3
   const int64_t cap = std::max<int64_t>(max_numel, 8) * esz / 16 * 16;
   bytes_per_peer = std::min(bytes_per_peer, cap) / 16 * 16;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  struct EventGuard {  // destroyed on every return path
+    cudaEvent_t* a;
+    cudaEvent_t* b;
+    ~EventGuard() {
+      if (*a) cudaEventDestroy(*a);
+      if (*b) cudaEventDestroy(*b);
+    }
+  } guard{&e0, &e1};
   CUDA_TRY(h, cudaEventCreate(&e0));
   CUDA_TRY(h, cudaEventCreate(&e1));
   cudaStream_t st = ln.stream;
@@ -1750,8 +1758,6 @@ edit_status_t edit_sync_nvlink_probe(edit_sync_t h, int64_t bytes_per_peer, int3
   TRY(check_err(h));
   float ms = 0.f;
   CUDA_TRY(h, cudaEventElapsedTime(&ms, e0, e1));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   *gbps = ms > 0 ? (double)reps * (h->N - 1) * (double)bytes_per_peer / (ms * 1e-3) / 1e9 : 0.0;
   return EDIT_OK;
 }
