@@ -195,12 +195,20 @@ edit_status_t edit_sync_register_locals(edit_sync_t h, void* const* locals);
 edit_status_t edit_sync_register_gather(edit_sync_t h, void* const* full_bufs);
 
 /* One full sync round: every unit 0..L-1 (arrays of L device pointers), equivalent to
- * calling edit_layer_sync for u = 0..L-1 in order but pipelined: units are dealt
- * round-robin over the library's lanes (EDIT_LANES; default 4 for N > 1, 2 for N == 1;
+ * calling edit_layer_sync for u = 0..L-1 in order but pipelined: work items (units, or the
+ * unit groups below) are dealt round-robin over the library's lanes (EDIT_LANES; default 4 for N > 1, 2 for N == 1;
  * each lane = an internal stream + its own NCCL communicators + exchange buffers), so unit u+1's norm pass and
  * scalar gathers overlap unit u's exchange and update.  Starts after the work already on
- * `stream`; `stream` waits for the whole round.  Same results, bit for bit, as the
- * sequential calls (every unit's arithmetic and reduction order is unchanged).
+ * `stream`; `stream` waits for the whole round.
+ * Unit groups (peer path, N > 1, mailbox exchange, no registered gather buffers): runs of
+ * consecutive units up to EDIT_GROUP_NUMEL elements in total (default 67,108,864; 0 = off;
+ * equal on every rank) are synced as one work item -- one norm, one reduce-scatter and one
+ * update launch for the group, and one exchange message per phase carrying every unit's
+ * scalars; per-unit semantics (norms, z-tests, EMA, weights, rollback, clip) unchanged.
+ * Results: N == 1 (no groups) bit for bit those of the sequential calls; within a group the
+ * reduce-scatter's per-CTA partition of ||Dbar||^2 differs from the single-unit kernel's, so
+ * beta (hence anchor/momentum/local) can differ from the sequential calls in the last bits
+ * (within the R17 tolerance; decisions identical), and is identical on every rank.
  * EDIT_GRAPH=1 in the environment at init (equal on every rank; opt-in): the round is
  * captured into a CUDA graph on the first call with a given set of 3L pointers and replayed
  * on later calls with the same set (up to 4 sets cached); same results. */
